@@ -1,0 +1,228 @@
+/*
+ * sl_abi.h — C ABI of the B200-native sparse level-format kernels.
+ *
+ * This is the drop-in boundary for the reference's hot path: the executor
+ * loop nest `_Executor.run_node` / `run_fused` (reference
+ * pkg/src/sparselevels/engine.py:580-713) specialised, per SURVEY.md §8(a16),
+ * to the five expression/format patterns of BASELINE.json, plus the level
+ * functions those loop nests call (levels.py:215-394).
+ *
+ * Conventions
+ *   - Every pointer is a caller-owned DEVICE pointer (cudaMalloc / torch), except
+ *     where a parameter is documented as a host pointer.
+ *   - Coordinates and positions are int32 (the reference uses Python ints; the
+ *     configs fit int32, and sizes above INT32_MAX return SL_ERR_RANGE).
+ *     Values are IEEE binary64.
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *     Every call is asynchronous and stream-ordered; nothing here synchronises
+ *     the host except the functions documented as "synchronous".
+ *   - No call allocates device memory.  Scratch comes from a caller workspace
+ *     sized by the matching sl_*_workspace_bytes() function.
+ *   - Return value: SL_OK (0) or an SL_ERR_* code.  The Python host package
+ *     maps them 1:1 onto the reference exception classes (errors.py:4-55).
+ *   - Reentrant; the only global state is a cached per-device SM count.
+ *
+ * Arithmetic contract ("Exact arithmetic"):
+ *   SpMV     y[i] = ((+0.0 + a_i,j1*x_j1) + a_i,j2*x_j2) + ...   in storage
+ *            order, one rounding per multiply and per add (no FMA contraction):
+ *            bit-identical to engine.py:303,320 (scatter) / :606-633 (CSR).
+ *   A+B      sorted union per row; value a+b where both stored, else the copy;
+ *            explicit zeros kept (engine.py:387-413): bit-identical.
+ *   MTTKRP   A[i,r] = sum of (x*B[j,r])*C[k,r] (engine.py:528-529 association);
+ *            the sum over a slice is a parallel reduction, so A matches the
+ *            sequential reference within |d| <= 1e-12 * sum|terms|.
+ */
+#ifndef SL_ABI_H
+#define SL_ABI_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes (errors.py:4-55) ------------------------------------- */
+enum {
+  SL_OK = 0,
+  SL_ERR_INVALID = 1,              /* bad argument (null pointer, negative size)        */
+  SL_ERR_UNSUPPORTED_CAPABILITY = 2,/* UnsupportedCapabilityError  errors.py:8 / levels.py:197 */
+  SL_ERR_ASSEMBLY = 3,             /* AssemblyError               errors.py:16          */
+  SL_ERR_HASH_SEGMENT_FULL = 4,    /* HashSegmentFullError        errors.py:20 / levels.py:330 */
+  SL_ERR_UNSUPPORTED_MERGE = 5,    /* UnsupportedMergeError       errors.py:46          */
+  SL_ERR_UNSUPPORTED_OUTPUT = 6,   /* UnsupportedOutputError      errors.py:50          */
+  SL_ERR_RANGE = 7,                /* size beyond the int32 index contract               */
+  SL_ERR_WORKSPACE = 8,            /* workspace too small                                */
+  SL_ERR_CUDA = 9                  /* CUDA launch/runtime failure                        */
+};
+
+/* ---- level kinds (levels.py:25-31) -------------------------------------- */
+enum {
+  SL_DENSE = 0, SL_RANGE = 1, SL_COMPRESSED = 2,
+  SL_SINGLETON = 3, SL_OFFSET = 4, SL_HASHED = 5
+};
+
+/* One storage level as the reference's LevelStorage (levels.py:173-191).
+ * Which fields are meaningful depends on `kind`, exactly as in the reference. */
+typedef struct sl_level {
+  int32_t kind;
+  int32_t crd_stride;      /* interleaved (AoS) crd arrays: stride, default 1     */
+  int32_t crd_base;        /* interleaved (AoS) crd arrays: lane, default 0       */
+  int32_t noffset;         /* length of `offset` (range/offset levels)            */
+  int64_t n;               /* dense/range: dimension size                         */
+  int64_t m;               /* range: the other dimension's extent                 */
+  int64_t w;               /* hashed: segment width                               */
+  int64_t range_n;         /* offset: enclosing range level's n                   */
+  const int32_t* pos;      /* compressed                                           */
+  const int32_t* crd;      /* compressed / singleton / hashed                      */
+  const int32_t* offset;   /* range / offset (shared DIA offsets)                  */
+} sl_level;
+
+/* Level-function ids for sl_level_query (levels.py:215-294). */
+enum {
+  SL_FN_COORD_BOUNDS = 0,  /* in: a = prefix last coord      out: o0 = lo, o1 = hi     */
+  SL_FN_COORD_ACCESS = 1,  /* in: a = parent_pos, b = coord  out: o0 = pos, o1 = found */
+  SL_FN_POS_BOUNDS = 2,    /* in: a = parent_pos             out: o0 = lo, o1 = hi     */
+  SL_FN_POS_ACCESS = 3,    /* in: a = pos, b = prefix last   out: o0 = coord, o1 = found */
+  SL_FN_LOCATE = 4,        /* in: a = parent_pos, b = coord  out: o0 = pos, o1 = found */
+  SL_FN_SIZE = 5           /* in: a = parent_size            out: o0 = size            */
+};
+
+/* ---- library ----------------------------------------------------------- */
+int         sl_version(void);                 /* ABI version, 0x0100 = 1.0 */
+const char* sl_status_string(int status);     /* static string, never NULL */
+/* Synchronous: clears and returns the sticky error of the last CUDA call. */
+int         sl_last_cuda_error(void);
+/* Number of SMs of the current device (cached). Synchronous. */
+int         sl_device_sm_count(int32_t* out);
+
+/* ---- level functions, batched on the device ------------------------------
+ * Replaces: LevelStorage.coord_bounds/coord_access/pos_bounds/pos_access/
+ * locate/size (levels.py:215-294).  `lv` is a HOST pointer to the level
+ * descriptor whose array pointers are device pointers.  For each query q,
+ * evaluates function `fn` on (a[q], b[q]) and writes (o0[q], o1[q]).
+ * Returns SL_ERR_UNSUPPORTED_CAPABILITY (without launching) when the kind
+ * lacks the capability, exactly as LevelStorage._require (levels.py:197-199).
+ * b and o1 may be NULL when the function does not use them. */
+int sl_level_query(const sl_level* lv, int32_t fn, int64_t nq,
+                   const int64_t* a, const int64_t* b,
+                   int64_t* o0, int64_t* o1, void* stream);
+
+/* ---- hashed level: locate and insert --------------------------------------
+ * Replaces: LevelStorage.locate for hashed levels (levels.py:270-280) —
+ * linear probing from (coord % w) inside segment parent_pos, first match wins,
+ * first -1 or a full scan of the segment means "absent" (pos -1, found 0).
+ * Warp-cooperative: `group` lanes (1, 4, 8, 16 or 32) probe consecutive slots
+ * of one query at once; the result is the first match-or-empty in probe order.
+ * parent_pos may be NULL (all queries in segment 0: a hash vector). */
+int sl_hashed_locate(int64_t nq, const int32_t* parent_pos, const int32_t* coord,
+                     int64_t w, const int32_t* crd,
+                     int32_t* out_pos, uint8_t* out_found, int32_t group,
+                     void* stream);
+
+/* Replaces: LevelStorage.insert_init + insert_coord (levels.py:303-333) in bulk.
+ * crd must already hold -1 in empty slots (sl_hashed_insert_init does that).
+ * Concurrent inserts use atomicCAS, so the final slot of a coordinate is the
+ * one some sequential insertion order would give; the SET of stored
+ * coordinates per segment and every locate result's `found` are identical to
+ * the reference's.  Idempotent.  Overflow is reported through *err_flag
+ * (device int32, set to SL_ERR_HASH_SEGMENT_FULL) — the call itself is async. */
+int sl_hashed_insert_init(int64_t size, int32_t* crd, void* stream);
+int sl_hashed_insert(int64_t nq, const int32_t* parent_pos, const int32_t* coord,
+                     int64_t w, int32_t* crd, int32_t* err_flag, void* stream);
+
+/* ---- SpMV  y(i) = A(i,j) * x(j), dense x and y --------------------------
+ * COO-SoA (formats.py:132-133): rows/cols = L0/L1 crd, row-major sorted
+ * (the compressed(~U) level is ordered).  Replaces run_fused over i(+)j with
+ * scatter into y (engine.py:636-713, 281-320).  No conversion to CSR: tiles of
+ * nonzeros are staged, products formed in parallel, and each row is summed in
+ * storage order by the thread that owns the row's first nonzero.  Empty rows
+ * are written as +0.0 in the same launch (no memset). */
+int sl_spmv_coo_f64(int64_t nrows, int64_t ncols, int64_t nnz,
+                    const int32_t* rows, const int32_t* cols, const double* vals,
+                    const double* x, double* y, void* stream);
+
+/* CSR (formats.py:126-127). Replaces run_node(i) -> run_node(j) with
+ * locate of x (engine.py:591-634).
+ * variant 0 = row-block (rows tiled; nonzeros of the tile staged through
+ *             shared memory in coalesced chunks; thread per row sums in order);
+ * variant 1 = vector-per-row (a warp per row; lanes load the row's nonzeros
+ *             coalesced, lane 0 sums them in order from registers via shuffles);
+ * variant 2 = merge-path (nnz+rows balanced tiles; row-owner sums in order);
+ * All variants are bit-identical.  ws may be NULL for variants 0 and 1. */
+size_t sl_spmv_csr_workspace_bytes(int64_t nrows, int64_t nnz, int32_t variant);
+int sl_spmv_csr_f64(int64_t nrows, int64_t ncols, int64_t nnz, const int32_t* pos,
+                    const int32_t* crd, const double* vals,
+                    const double* x, double* y, int32_t variant,
+                    void* ws, size_t ws_bytes, void* stream);
+
+/* ELL (formats.py:164-169): slot-major crd/vals [nslots * nrows], position
+ * s*nrows + i (levels.py:230), padding (col 0, 0.0) visited like the
+ * reference (its 0.0*x[0] terms are added after the row's real entries). */
+int sl_spmv_ell_f64(int64_t nrows, int64_t ncols, int32_t nslots,
+                    const int32_t* crd, const double* vals,
+                    const double* x, double* y, void* stream);
+
+/* DIA (formats.py:170-175): ndiag sorted offsets (HOST or device pointer,
+ * see offsets_on_host), vals [ndiag * nrows] at d*nrows + i.  Row i takes the
+ * term of diagonal d iff 0 <= i + offset[d] < ncols (range level bounds,
+ * levels.py:220-222), in ascending-offset order. */
+int sl_spmv_dia_f64(int64_t nrows, int64_t ncols, int32_t ndiag,
+                    const int32_t* offsets, int32_t offsets_on_host,
+                    const double* vals, const double* x, double* y, void* stream);
+
+/* CSR x hash-vector: y(i) = A(i,j) * x(j) with x a hashed level of width w
+ * (crd[w] with -1 empties, vals[w] by slot).  x is located per nonzero
+ * (engine.py:558-572 -> levels.py:270-280); a miss contributes no term. */
+int sl_spmv_csr_hashx_f64(int64_t nrows, const int32_t* pos, const int32_t* crd,
+                          const double* vals, int64_t w, const int32_t* x_crd,
+                          const double* x_vals, double* y, void* stream);
+
+/* ---- C(i,j) = A(i,j) + B(i,j) -> CSR --------------------------------------
+ * A is CSR; B is COO-SoA (b_pos == NULL, b_rows given) or CSR (b_pos given).
+ * Replaces the co-iteration of engine.py:591-634 with the gather-append
+ * writer (engine.py:330-434).  Two passes:
+ *   count: c_pos[0] = 0, c_pos[i+1] = |row i of A  union  row i of B|, then an
+ *          in-place exclusive scan -> c_pos is the final CSR row pointer;
+ *   fill:  writes c_crd/c_vals in sorted-union order.
+ * nnz_c = c_pos[nrows] (read it back, or size c_crd/c_vals at nnz_a + nnz_b). */
+size_t sl_add_csr_workspace_bytes(int64_t nrows, int64_t b_nnz);
+int sl_add_csr_count(int64_t nrows,
+                     const int32_t* a_pos, const int32_t* a_crd,
+                     int64_t b_nnz, const int32_t* b_pos, const int32_t* b_rows,
+                     const int32_t* b_cols,
+                     int32_t* c_pos, void* ws, size_t ws_bytes, void* stream);
+int sl_add_csr_fill(int64_t nrows,
+                    const int32_t* a_pos, const int32_t* a_crd, const double* a_vals,
+                    int64_t b_nnz, const int32_t* b_pos, const int32_t* b_rows,
+                    const int32_t* b_cols, const double* b_vals,
+                    const int32_t* c_pos, int32_t* c_crd, double* c_vals,
+                    void* ws, size_t ws_bytes, void* stream);
+
+/* ---- MTTKRP  A(i,r) = X(i,j,k) * B(j,r) * C(k,r) ----------------------------
+ * B [J x R], C [K x R], A [I x R] row-major dense (dense-2 layout).
+ * COO-3 (formats.py:138-140): i, j, k = L0/L1/L2 crd, lexicographically sorted.
+ * CSF (formats.py:136-137): pos0/crd0 slices, pos1/crd1 fibers, pos2/crd2.
+ * Rows of A with no nonzeros are written +0.0 in-kernel.  Deterministic:
+ * partial sums of slices split across work chunks are combined by a fix-up
+ * kernel in a fixed order. */
+size_t sl_mttkrp_workspace_bytes(int64_t nnz, int32_t R);
+int sl_mttkrp_coo3_f64(int64_t I, int64_t J, int64_t K, int32_t R, int64_t nnz,
+                       const int32_t* i, const int32_t* j, const int32_t* k,
+                       const double* vals, const double* B, const double* C,
+                       double* A, void* ws, size_t ws_bytes, void* stream);
+int sl_mttkrp_csf_f64(int64_t I, int64_t J, int64_t K, int32_t R,
+                      int64_t nslices, int64_t nfibers, int64_t nnz,
+                      const int32_t* crd0, const int32_t* pos1, const int32_t* crd1,
+                      const int32_t* pos2, const int32_t* crd2,
+                      const double* vals, const double* B, const double* C,
+                      double* A, void* ws, size_t ws_bytes, void* stream);
+
+/* ---- utilities used by the benchmark ------------------------------------- */
+/* Writes `bytes` of junk into `buf` to evict L2 between timed iterations. */
+int sl_l2_flush(void* buf, size_t bytes, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SL_ABI_H */

@@ -1,0 +1,237 @@
+"""numpy wrappers around the C oracle (oracle/sl_oracle.c).
+
+TEST INFRASTRUCTURE ONLY: imported by tests/, __graft_entry__.smoke() and
+bench.py's CPU-baseline / --impl reference legs, as the checker or the CPU
+baseline.  The product package (paper_1804_10112_b200) never imports it.
+
+Every function follows the reference interpreter's evaluation order (see the
+per-function citations in sl_oracle.c) and is pinned against golden vectors
+made by running the reference itself (tests/golden/make_golden.py).
+Reductions return (out, sum_abs_terms) so callers can apply the
+condition-scaled tolerance |gpu - ref| <= 1e-12 * max(|ref|, sum|terms|).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+from pathlib import Path
+
+import numpy as np
+
+HERE = Path(__file__).resolve().parent
+LIB_PATH = HERE / "build" / "libsl_oracle.so"
+
+_i64 = ctypes.c_int64
+_i32 = ctypes.c_int32
+_ptr = ctypes.c_void_p
+
+
+def build(force: bool = False) -> Path:
+    src = HERE / "sl_oracle.c"
+    if force or not LIB_PATH.exists() or LIB_PATH.stat().st_mtime < src.stat().st_mtime:
+        subprocess.run(["make", "-s", "-C", str(HERE)], check=True)
+    return LIB_PATH
+
+
+_LIB = None
+
+
+def lib():
+    global _LIB
+    if _LIB is None:
+        if not LIB_PATH.exists():
+            build()
+        L = ctypes.CDLL(str(LIB_PATH))
+        sig = {
+            "or_spmv_coo": [_i64, _i64, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr],
+            "or_spmv_coo_mt": [_i64, _i64, _ptr, _ptr, _ptr, _ptr, _ptr, ctypes.c_int],
+            "or_spmv_csr": [_i64, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr],
+            "or_spmv_csr_mt": [_i64, _ptr, _ptr, _ptr, _ptr, _ptr, ctypes.c_int],
+            "or_spmv_ell": [_i64, _i32, _ptr, _ptr, _ptr, _ptr, _ptr],
+            "or_spmv_ell_mt": [_i64, _i32, _ptr, _ptr, _ptr, _ptr, ctypes.c_int],
+            "or_spmv_dia": [_i64, _i64, _i32, _ptr, _ptr, _ptr, _ptr, _ptr],
+            "or_spmv_dia_mt": [_i64, _i64, _i32, _ptr, _ptr, _ptr, _ptr, ctypes.c_int],
+            "or_hashed_locate": [_i64, _ptr, _ptr, _i64, _ptr, _ptr, _ptr],
+            "or_hashed_insert": [_i64, _ptr, _ptr, _i64, _ptr],
+            "or_spmv_csr_hashx": [_i64, _ptr, _ptr, _ptr, _i64, _ptr, _ptr, _ptr, _ptr],
+            "or_spmv_csr_hashx_mt": [_i64, _ptr, _ptr, _ptr, _i64, _ptr, _ptr, _ptr, ctypes.c_int],
+            "or_add_csr": [_i64, _ptr, _ptr, _ptr, _i64, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr],
+            "or_add_csr_mt": [_i64, _ptr, _ptr, _ptr, _i64, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr,
+                              _ptr, ctypes.c_int],
+            "or_mttkrp_coo3": [_i64, _i32, _i64, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr],
+            "or_mttkrp_coo3_mt": [_i64, _i32, _i64, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr,
+                                  ctypes.c_int],
+            "or_mttkrp_csf": [_i64, _i32, _i64, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr,
+                              _ptr, _ptr],
+            "or_mttkrp_csf_mt": [_i64, _i32, _i64, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr,
+                                 _ptr, _ptr, ctypes.c_int],
+            "or_num_threads": [],
+        }
+        for name, args in sig.items():
+            fn = getattr(L, name)
+            fn.argtypes = args
+        L.or_add_csr.restype = _i64
+        L.or_add_csr_mt.restype = _i64
+        L.or_hashed_insert.restype = ctypes.c_int
+        L.or_num_threads.restype = ctypes.c_int
+        _LIB = L
+    return _LIB
+
+
+def _p(a):
+    return None if a is None else a.ctypes.data
+
+
+def _c(a, dt):
+    return None if a is None else np.ascontiguousarray(a, dtype=dt)
+
+
+def num_threads() -> int:
+    return int(lib().or_num_threads())
+
+
+def spmv_coo(nrows, rows, cols, vals, x, threads=None):
+    rows, cols = _c(rows, np.int32), _c(cols, np.int32)
+    vals, x = _c(vals, np.float64), _c(x, np.float64)
+    y = np.empty(nrows, dtype=np.float64)
+    if threads is None:
+        a = np.empty(nrows, dtype=np.float64)
+        lib().or_spmv_coo(nrows, len(rows), _p(rows), _p(cols), _p(vals), _p(x), _p(y), _p(a))
+        return y, a
+    lib().or_spmv_coo_mt(nrows, len(rows), _p(rows), _p(cols), _p(vals), _p(x), _p(y), threads)
+    return y
+
+
+def spmv_csr(nrows, pos, crd, vals, x, threads=None):
+    pos, crd = _c(pos, np.int32), _c(crd, np.int32)
+    vals, x = _c(vals, np.float64), _c(x, np.float64)
+    y = np.empty(nrows, dtype=np.float64)
+    if threads is None:
+        a = np.empty(nrows, dtype=np.float64)
+        lib().or_spmv_csr(nrows, _p(pos), _p(crd), _p(vals), _p(x), _p(y), _p(a))
+        return y, a
+    lib().or_spmv_csr_mt(nrows, _p(pos), _p(crd), _p(vals), _p(x), _p(y), threads)
+    return y
+
+
+def spmv_ell(nrows, nslots, crd, vals, x, threads=None):
+    crd, vals, x = _c(crd, np.int32), _c(vals, np.float64), _c(x, np.float64)
+    y = np.empty(nrows, dtype=np.float64)
+    if threads is None:
+        a = np.empty(nrows, dtype=np.float64)
+        lib().or_spmv_ell(nrows, nslots, _p(crd), _p(vals), _p(x), _p(y), _p(a))
+        return y, a
+    lib().or_spmv_ell_mt(nrows, nslots, _p(crd), _p(vals), _p(x), _p(y), threads)
+    return y
+
+
+def spmv_dia(nrows, ncols, offsets, vals, x, threads=None):
+    offsets, vals, x = _c(offsets, np.int32), _c(vals, np.float64), _c(x, np.float64)
+    y = np.empty(nrows, dtype=np.float64)
+    if threads is None:
+        a = np.empty(nrows, dtype=np.float64)
+        lib().or_spmv_dia(nrows, ncols, len(offsets), _p(offsets), _p(vals), _p(x), _p(y), _p(a))
+        return y, a
+    lib().or_spmv_dia_mt(nrows, ncols, len(offsets), _p(offsets), _p(vals), _p(x), _p(y), threads)
+    return y
+
+
+def hashed_locate(coords, w, crd, parent=None):
+    coords, crd = _c(coords, np.int32), _c(crd, np.int32)
+    parent = _c(parent, np.int32)
+    pos = np.empty(len(coords), dtype=np.int32)
+    found = np.empty(len(coords), dtype=np.uint8)
+    lib().or_hashed_locate(len(coords), _p(parent), _p(coords), w, _p(crd), _p(pos), _p(found))
+    return pos, found.astype(bool)
+
+
+def hashed_insert(coords, w, nseg=1, parent=None, crd=None):
+    coords, parent = _c(coords, np.int32), _c(parent, np.int32)
+    crd = np.full(nseg * w, -1, dtype=np.int32) if crd is None else _c(crd, np.int32).copy()
+    st = lib().or_hashed_insert(len(coords), _p(parent), _p(coords), w, _p(crd))
+    return crd, st
+
+
+def spmv_csr_hashx(nrows, pos, crd, vals, w, xcrd, xvals, threads=None):
+    pos, crd, vals = _c(pos, np.int32), _c(crd, np.int32), _c(vals, np.float64)
+    xcrd, xvals = _c(xcrd, np.int32), _c(xvals, np.float64)
+    y = np.empty(nrows, dtype=np.float64)
+    if threads is None:
+        a = np.empty(nrows, dtype=np.float64)
+        lib().or_spmv_csr_hashx(nrows, _p(pos), _p(crd), _p(vals), w, _p(xcrd), _p(xvals), _p(y),
+                                _p(a))
+        return y, a
+    lib().or_spmv_csr_hashx_mt(nrows, _p(pos), _p(crd), _p(vals), w, _p(xcrd), _p(xvals), _p(y),
+                               threads)
+    return y
+
+
+def add_csr(nrows, a_pos, a_crd, a_vals, b_cols, b_vals, b_rows=None, b_pos=None, threads=None):
+    a_pos, a_crd, a_vals = _c(a_pos, np.int32), _c(a_crd, np.int32), _c(a_vals, np.float64)
+    b_cols, b_vals = _c(b_cols, np.int32), _c(b_vals, np.float64)
+    b_rows, b_pos = _c(b_rows, np.int32), _c(b_pos, np.int32)
+    cap = len(a_crd) + len(b_cols)
+    c_pos = np.empty(nrows + 1, dtype=np.int32)
+    c_crd = np.empty(max(cap, 1), dtype=np.int32)
+    c_vals = np.empty(max(cap, 1), dtype=np.float64)
+    args = (nrows, _p(a_pos), _p(a_crd), _p(a_vals), len(b_cols), _p(b_pos), _p(b_rows),
+            _p(b_cols), _p(b_vals), _p(c_pos), _p(c_crd), _p(c_vals))
+    if threads is None:
+        n = lib().or_add_csr(*args)
+    else:
+        n = lib().or_add_csr_mt(*args, threads)
+    return c_pos, c_crd[:n].copy(), c_vals[:n].copy()
+
+
+def mttkrp_coo3(I, i, j, k, vals, B, C, threads=None):
+    i, j, k = _c(i, np.int32), _c(j, np.int32), _c(k, np.int32)
+    vals, B, C = _c(vals, np.float64), _c(B, np.float64), _c(C, np.float64)
+    R = B.shape[1]
+    A = np.empty((I, R), dtype=np.float64)
+    if threads is None:
+        a = np.empty((I, R), dtype=np.float64)
+        lib().or_mttkrp_coo3(I, R, len(i), _p(i), _p(j), _p(k), _p(vals), _p(B), _p(C), _p(A),
+                             _p(a))
+        return A, a
+    lib().or_mttkrp_coo3_mt(I, R, len(i), _p(i), _p(j), _p(k), _p(vals), _p(B), _p(C), _p(A),
+                            threads)
+    return A
+
+
+def mttkrp_csf(I, crd0, pos1, crd1, pos2, crd2, vals, B, C, threads=None):
+    crd0, pos1, crd1 = _c(crd0, np.int32), _c(pos1, np.int32), _c(crd1, np.int32)
+    pos2, crd2 = _c(pos2, np.int32), _c(crd2, np.int32)
+    vals, B, C = _c(vals, np.float64), _c(B, np.float64), _c(C, np.float64)
+    R = B.shape[1]
+    A = np.empty((I, R), dtype=np.float64)
+    if threads is None:
+        a = np.empty((I, R), dtype=np.float64)
+        lib().or_mttkrp_csf(I, R, len(crd0), _p(crd0), _p(pos1), _p(crd1), _p(pos2), _p(crd2),
+                            _p(vals), _p(B), _p(C), _p(A), _p(a))
+        return A, a
+    lib().or_mttkrp_csf_mt(I, R, len(crd0), _p(crd0), _p(pos1), _p(crd1), _p(pos2), _p(crd2),
+                           _p(vals), _p(B), _p(C), _p(A), threads)
+    return A
+
+
+def bits_equal(a, b) -> bool:
+    """Bit-exact equality of float64 arrays, treating +0.0 and -0.0 as different."""
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    b = np.ascontiguousarray(b, dtype=np.float64)
+    return a.shape == b.shape and bool(np.array_equal(a.view(np.int64), b.view(np.int64)))
+
+
+def within_condition(gpu, ref, sum_abs, rtol=1e-12):
+    """Condition-scaled check |gpu - ref| <= rtol * max(|ref|, sum|terms|)."""
+    gpu = np.asarray(gpu, dtype=np.float64)
+    ref = np.asarray(ref, dtype=np.float64)
+    scale = np.maximum(np.abs(ref), np.asarray(sum_abs, dtype=np.float64))
+    err = np.abs(gpu - ref)
+    ok = err <= rtol * scale
+    return bool(ok.all()), float((err / np.where(scale > 0, scale, 1.0)).max(initial=0.0))
+
+
+if os.environ.get("SL_ORACLE_BUILD") == "1":  # pragma: no cover
+    build(force=True)

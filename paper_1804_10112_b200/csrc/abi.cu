@@ -1,0 +1,173 @@
+// abi.cu — library plumbing and the batched level-function entry point.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.cuh"
+#include "levels.cuh"
+
+namespace sl_host {
+
+int sm_count() {
+  static int cached_dev = -1, cached = 0;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 148;
+  if (dev != cached_dev) {
+    int n = 0;
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0)
+      n = 148;
+    cached = n;
+    cached_dev = dev;
+  }
+  return cached;
+}
+
+int launch_status() { return cudaGetLastError() == cudaSuccess ? SL_OK : SL_ERR_CUDA; }
+
+}  // namespace sl_host
+
+namespace sl {
+
+// Replays LevelStorage's access functions (levels.py:215-294) for a batch of
+// queries.  Capability checks happen on the host before launch.
+template <typename Level>
+__global__ void level_query_kernel(Level lv, int32_t fn, int64_t nq, const int64_t* __restrict__ a,
+                                   const int64_t* __restrict__ b, int64_t* __restrict__ o0,
+                                   int64_t* __restrict__ o1) {
+  const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= nq) return;
+  int64_t r0 = 0, r1 = 0;
+  if constexpr (Level::kValueIter) {
+    if (fn == SL_FN_COORD_BOUNDS) {
+      const Bounds bd = lv.coord_bounds(a[q]);
+      r0 = bd.lo; r1 = bd.hi;
+    } else if (fn == SL_FN_COORD_ACCESS) {
+      const PosFound pf = lv.coord_access(a[q], b[q]);
+      r0 = pf.pos; r1 = pf.found;
+    }
+  }
+  if constexpr (Level::kPosIter) {
+    if (fn == SL_FN_POS_BOUNDS) {
+      const Bounds bd = lv.pos_bounds(a[q]);
+      r0 = bd.lo; r1 = bd.hi;
+    } else if (fn == SL_FN_POS_ACCESS) {
+      const CoordFound cf = lv.pos_access(a[q], b ? b[q] : 0);
+      r0 = cf.coord; r1 = cf.found;
+    }
+  }
+  if constexpr (Level::kLocate) {
+    if (fn == SL_FN_LOCATE) {
+      const PosFound pf = lv.locate(a[q], b[q]);
+      r0 = pf.pos; r1 = pf.found;
+    }
+  }
+  if constexpr (Level::kInsert) {
+    if (fn == SL_FN_SIZE) r0 = lv.size(a[q]);
+  }
+  o0[q] = r0;
+  if (o1) o1[q] = r1;
+}
+
+__global__ void l2_flush_kernel(uint4* __restrict__ buf, size_t n, uint32_t salt) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
+       i += (size_t)gridDim.x * blockDim.x)
+    buf[i] = make_uint4((uint32_t)i ^ salt, salt, (uint32_t)(i >> 7), ~salt);
+}
+
+}  // namespace sl
+
+using namespace sl;
+
+static bool kind_has(int kind, int fn) {
+  const bool value_iter = kind == SL_DENSE || kind == SL_RANGE;
+  const bool pos_iter = kind == SL_COMPRESSED || kind == SL_SINGLETON || kind == SL_OFFSET ||
+                        kind == SL_HASHED;
+  const bool locate = kind == SL_DENSE || kind == SL_HASHED;   // levels.py:39
+  const bool insert = kind == SL_DENSE || kind == SL_HASHED;   // levels.py:40
+  switch (fn) {
+    case SL_FN_COORD_BOUNDS:
+    case SL_FN_COORD_ACCESS: return value_iter;
+    case SL_FN_POS_BOUNDS:
+    case SL_FN_POS_ACCESS: return pos_iter;
+    case SL_FN_LOCATE: return locate;
+    case SL_FN_SIZE: return insert;
+    default: return false;
+  }
+}
+
+extern "C" int sl_version(void) { return 0x0100; }
+
+extern "C" const char* sl_status_string(int status) {
+  switch (status) {
+    case SL_OK: return "ok";
+    case SL_ERR_INVALID: return "invalid argument";
+    case SL_ERR_UNSUPPORTED_CAPABILITY: return "level does not support this function";
+    case SL_ERR_ASSEMBLY: return "assembly protocol violated";
+    case SL_ERR_HASH_SEGMENT_FULL: return "hashed segment is full";
+    case SL_ERR_UNSUPPORTED_MERGE: return "unsupported merge";
+    case SL_ERR_UNSUPPORTED_OUTPUT: return "unsupported output";
+    case SL_ERR_RANGE: return "size exceeds the int32 index contract";
+    case SL_ERR_WORKSPACE: return "workspace too small";
+    case SL_ERR_CUDA: return "CUDA error";
+    default: return "unknown status";
+  }
+}
+
+extern "C" int sl_last_cuda_error(void) { return (int)cudaGetLastError(); }
+
+extern "C" int sl_device_sm_count(int32_t* out) {
+  if (!out) return SL_ERR_INVALID;
+  *out = sl_host::sm_count();
+  return SL_OK;
+}
+
+extern "C" int sl_level_query(const sl_level* lv, int32_t fn, int64_t nq, const int64_t* a,
+                              const int64_t* b, int64_t* o0, int64_t* o1, void* stream) {
+  if (!lv || nq < 0 || fn < 0 || fn > SL_FN_SIZE) return SL_ERR_INVALID;
+  if (!kind_has(lv->kind, fn)) return SL_ERR_UNSUPPORTED_CAPABILITY;
+  if (nq == 0) return SL_OK;
+  const bool needs_b = fn == SL_FN_COORD_ACCESS || fn == SL_FN_LOCATE;
+  if (!a || !o0 || (needs_b && !b)) return SL_ERR_INVALID;
+  cudaStream_t s = sl_host::as_stream(stream);
+  const int grid = sl_host::ceil_div(nq, 256);
+  const int32_t stride = lv->crd_stride > 0 ? lv->crd_stride : 1;
+  switch (lv->kind) {
+    case SL_DENSE:
+      level_query_kernel<<<grid, 256, 0, s>>>(DenseLevel{lv->n}, fn, nq, a, b, o0, o1);
+      break;
+    case SL_RANGE:
+      level_query_kernel<<<grid, 256, 0, s>>>(RangeLevel{lv->n, lv->m, lv->offset}, fn, nq, a, b,
+                                              o0, o1);
+      break;
+    case SL_COMPRESSED:
+      level_query_kernel<<<grid, 256, 0, s>>>(
+          CompressedLevel{lv->pos, lv->crd, stride, lv->crd_base}, fn, nq, a, b, o0, o1);
+      break;
+    case SL_SINGLETON:
+      level_query_kernel<<<grid, 256, 0, s>>>(SingletonLevel{lv->crd, stride, lv->crd_base}, fn,
+                                              nq, a, b, o0, o1);
+      break;
+    case SL_OFFSET:
+      if (lv->range_n <= 0) return SL_ERR_INVALID;
+      level_query_kernel<<<grid, 256, 0, s>>>(OffsetLevel{lv->offset, lv->range_n}, fn, nq, a, b,
+                                              o0, o1);
+      break;
+    case SL_HASHED:
+      if (lv->w <= 0) return SL_ERR_INVALID;
+      level_query_kernel<<<grid, 256, 0, s>>>(HashedLevel{lv->crd, lv->w}, fn, nq, a, b, o0, o1);
+      break;
+    default:
+      return SL_ERR_INVALID;
+  }
+  return sl_host::launch_status();
+}
+
+extern "C" int sl_l2_flush(void* buf, size_t bytes, void* stream) {
+  if (!buf) return SL_ERR_INVALID;
+  static uint32_t salt = 0x9e3779b9u;
+  salt = salt * 1664525u + 1013904223u;
+  const size_t n = bytes / sizeof(uint4);
+  if (n == 0) return SL_OK;
+  sl::l2_flush_kernel<<<4 * sl_host::sm_count(), 512, 0, sl_host::as_stream(stream)>>>(
+      static_cast<uint4*>(buf), n, salt);
+  return sl_host::launch_status();
+}

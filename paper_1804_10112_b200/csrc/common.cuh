@@ -1,0 +1,90 @@
+// common.cuh — shared device helpers for the sm_100a kernels.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "sl_abi.h"
+
+#define SL_DEV __device__ __forceinline__
+
+namespace sl {
+
+// The reference rounds every product and every sum separately
+// (engine.py:528-531 evaluates Python floats).  The _rn intrinsics are never
+// contracted into FMA, which keeps results bit-identical.
+SL_DEV double dmul(double a, double b) { return __dmul_rn(a, b); }
+SL_DEV double dadd(double a, double b) { return __dadd_rn(a, b); }
+
+// Read-only loads through the non-coherent path.
+template <typename T>
+SL_DEV T ldg(const T* p) { return __ldg(p); }
+
+// Streaming loads: data touched exactly once.  Not allocated in L1 and tagged
+// evict-first in L2 (an L2 cache policy from createpolicy) so the reused
+// operands (x, factor matrices) stay resident.
+SL_DEV uint64_t policy_evict_first() {
+  uint64_t pol;
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+SL_DEV uint64_t policy_evict_last() {
+  uint64_t pol;
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+SL_DEV int32_t ld_stream(const int32_t* p) {
+  int32_t v;
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.b32 %0, [%1], %2;"
+      : "=r"(v) : "l"(p), "l"(policy_evict_first()));
+  return v;
+}
+SL_DEV double ld_stream(const double* p) {
+  double v;
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;"
+      : "=d"(v) : "l"(p), "l"(policy_evict_first()));
+  return v;
+}
+SL_DEV int4 ld_stream(const int4* p) {
+  int4 v;
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.b32 {%0,%1,%2,%3}, [%4], %5;"
+      : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p), "l"(policy_evict_first()));
+  return v;
+}
+SL_DEV int2 ld_stream(const int2* p) {
+  int2 v;
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.b32 {%0,%1}, [%2], %3;"
+      : "=r"(v.x), "=r"(v.y) : "l"(p), "l"(policy_evict_first()));
+  return v;
+}
+SL_DEV double2 ld_stream(const double2* p) {
+  double2 v;
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;"
+      : "=d"(v.x), "=d"(v.y) : "l"(p), "l"(policy_evict_first()));
+  return v;
+}
+// Reused operands (x, B, C): keep in L2.
+SL_DEV double ld_keep(const double* p) {
+  double v;
+  asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(policy_evict_last()));
+  return v;
+}
+// Output stores that are never re-read by this kernel.
+SL_DEV void st_stream(double* p, double v) {
+  asm volatile("st.global.L1::no_allocate.f64 [%0], %1;" :: "l"(p), "d"(v) : "memory");
+}
+
+__host__ __device__ __forceinline__ int64_t min64(int64_t a, int64_t b) { return a < b ? a : b; }
+__host__ __device__ __forceinline__ int64_t max64(int64_t a, int64_t b) { return a > b ? a : b; }
+
+template <typename T>
+SL_DEV T warp_bcast(T v, int src) { return __shfl_sync(0xffffffffu, v, src); }
+
+}  // namespace sl
+
+// Host-side helpers shared by the .cu files.
+namespace sl_host {
+int sm_count();                              // cached per current device
+inline int ceil_div(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
+int launch_status();                         // SL_OK or SL_ERR_CUDA after a launch
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+}  // namespace sl_host

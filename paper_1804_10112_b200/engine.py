@@ -1,0 +1,302 @@
+"""`evaluate` — the reference's entry point (engine.py:739-764), B200 backend.
+
+The reference plans every expression into a merge-lattice schedule and
+interprets it (engine.py:580-713).  For the hot path, the schedules of the
+five BASELINE patterns are fixed; `plan` recognises an
+(expression, level-kinds) pair as one of them and binds it to the sm_100a
+kernel that executes that schedule with the level functions inlined:
+
+    y(i) = A(i,j) * x(j)   A coo-soa | csr | ell | dia, x dense   -> K1..K4
+                           A csr, x hash-vector                   -> K5 (locate)
+    C(i,j) = A(i,j) + B(i,j)   A csr, B coo-soa | csr, C csr      -> K6
+    A(i,r) = X(i,j,k) * B(j,r) * C(k,r)   X coo-3 | csf, B/C dense -> K7 / K8
+
+Anything else raises UnsupportedMergeError (no kernel for that merge) or
+UnsupportedOutputError (output format the kernel cannot produce) — there is
+no interpreter fallback and no CPU path.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from typing import Dict, Optional, Sequence, Tuple
+
+import numpy as np
+import torch
+
+from . import kernels as K
+from .errors import UnsupportedMergeError, UnsupportedOutputError, ValidationError
+from .formats import TensorFormat, TensorStorage, preset
+from .levels import LevelKind as LK
+from .levels import LevelStorage
+from .notation import Access, Add, Assignment, CheckedExpr, Mul, parse, validate
+
+
+@dataclass
+class EvalStats:
+    """Visit counters keyed by loop variable (engine.py:255-268).  The GPU
+    path fills `by_var` with the number of loop visits the reference's
+    schedule performs for each variable (known from the storage sizes), which
+    is what the O(nnz) complexity property checks."""
+
+    by_var: Dict[str, int] = field(default_factory=dict)
+    by_loop: Dict[Tuple[str, str], int] = field(default_factory=dict)
+
+    def count(self, var: str, point_label: str, n: int = 1) -> None:
+        self.by_var[var] = self.by_var.get(var, 0) + n
+        key = (var, point_label)
+        self.by_loop[key] = self.by_loop.get(key, 0) + n
+
+    def total(self) -> int:
+        return sum(self.by_var.values())
+
+
+# ---------------------------------------------------------------------------
+# format recognition (by level kinds and roles, not by name)
+
+def _whole(fmt: TensorFormat) -> bool:
+    return all(r.part == "whole" for r in fmt.roles) and fmt.mode_ordering == tuple(
+        range(fmt.order)) and not fmt.aos
+
+
+def format_class(fmt: TensorFormat) -> str:
+    k = fmt.kinds()
+    if _whole(fmt):
+        if all(x is LK.DENSE for x in k):
+            return f"dense{len(k)}"
+        if k == (LK.DENSE, LK.COMPRESSED) and fmt.levels[1].props.ordered:
+            return "csr"
+        if (k == (LK.COMPRESSED, LK.SINGLETON) and fmt.levels[0].props.ordered
+                and fmt.levels[1].props.ordered):
+            return "coo"
+        if k == (LK.COMPRESSED, LK.SINGLETON, LK.SINGLETON) and fmt.levels[0].props.ordered:
+            return "coo3"
+        if k == (LK.COMPRESSED, LK.COMPRESSED, LK.COMPRESSED) and all(
+                s.props.ordered and s.props.unique for s in fmt.levels):
+            return "csf"
+        if k == (LK.HASHED,):
+            return "hash1"
+    roles = tuple(r.part for r in fmt.roles)
+    if k == (LK.DENSE, LK.DENSE, LK.SINGLETON) and roles == ("slot", "whole", "whole"):
+        return "ell"
+    if k == (LK.DENSE, LK.RANGE, LK.OFFSET) and roles == ("diag", "whole", "whole"):
+        return "dia"
+    return "other:" + fmt.describe()
+
+
+# ---------------------------------------------------------------------------
+# plans
+
+@dataclass
+class Plan:
+    pattern: str                 # spmv | add | mttkrp
+    kernel: str                  # which C-ABI entry executes it
+    operands: Dict[str, str]     # role -> tensor name
+    out_format: TensorFormat
+    out_dims: Tuple[int, ...]
+
+
+def _flatten_mul(e):
+    if isinstance(e, Mul):
+        return _flatten_mul(e.left) + _flatten_mul(e.right)
+    return [e]
+
+
+def plan(checked: CheckedExpr, bindings, out_format: TensorFormat,
+         out_dims: Tuple[int, ...]) -> Plan:
+    a: Assignment = checked.assignment
+    lhs, rhs = a.lhs, a.rhs
+    cls = {name: format_class(fmt) for name, (fmt, _) in bindings.items()}
+    ocls = format_class(out_format)
+
+    # ---- SpMV: y(i) = A(i,j) * x(j)
+    if isinstance(rhs, Mul) and all(isinstance(t, Access) for t in (rhs.left, rhs.right)):
+        acc = [rhs.left, rhs.right]
+        mat = [t for t in acc if len(t.ivars) == 2]
+        vec = [t for t in acc if len(t.ivars) == 1]
+        if len(mat) == 1 and len(vec) == 1 and len(lhs.ivars) == 1:
+            A, x = mat[0], vec[0]
+            i, j = A.ivars
+            if lhs.ivars == (i,) and x.ivars == (j,) and i != j:
+                if ocls != "dense1":
+                    raise UnsupportedOutputError(
+                        f"SpMV output must be a dense vector, got {out_format.describe()}")
+                ca, cx = cls[A.tensor], cls[x.tensor]
+                if cx == "dense1" and ca in ("coo", "csr", "ell", "dia"):
+                    return Plan("spmv", f"spmv_{ca}", {"A": A.tensor, "x": x.tensor},
+                                out_format, out_dims)
+                if cx == "hash1" and ca == "csr":
+                    return Plan("spmv", "spmv_csr_hashx", {"A": A.tensor, "x": x.tensor},
+                                out_format, out_dims)
+                raise UnsupportedMergeError(
+                    f"no B200 kernel for SpMV with A {ca} and x {cx}")
+
+    # ---- C(i,j) = A(i,j) + B(i,j)
+    if isinstance(rhs, Add) and all(isinstance(t, Access) for t in (rhs.left, rhs.right)):
+        L_, R_ = rhs.left, rhs.right
+        if len(lhs.ivars) == 2 and L_.ivars == lhs.ivars and R_.ivars == lhs.ivars:
+            if ocls != "csr":
+                raise UnsupportedOutputError(
+                    f"A + B is assembled as CSR (gather-append); got {out_format.describe()}")
+            cl, cr = cls[L_.tensor], cls[R_.tensor]
+            # a + b == b + a bit-for-bit, so the CSR operand can take either side
+            if cl == "csr" and cr in ("coo", "csr"):
+                return Plan("add", f"add_csr_{cr}", {"A": L_.tensor, "B": R_.tensor},
+                            out_format, out_dims)
+            if cr == "csr" and cl == "coo":
+                return Plan("add", "add_csr_coo", {"A": R_.tensor, "B": L_.tensor},
+                            out_format, out_dims)
+            raise UnsupportedMergeError(f"no B200 kernel for A + B with {cl} + {cr}")
+
+    # ---- A(i,r) = X(i,j,k) * B(j,r) * C(k,r), association (X*B)*C
+    if isinstance(rhs, Mul) and len(_flatten_mul(rhs)) == 3 and all(
+            isinstance(t, Access) for t in _flatten_mul(rhs)):
+        inner, outer = (rhs.left, rhs.right) if isinstance(rhs.left, Mul) else (rhs.right,
+                                                                                 rhs.left)
+        if isinstance(inner, Mul) and isinstance(outer, Access):
+            pair = [inner.left, inner.right]
+            X = [t for t in pair if len(t.ivars) == 3]
+            Bm = [t for t in pair if len(t.ivars) == 2]
+            if len(X) == 1 and len(Bm) == 1 and len(outer.ivars) == 2:
+                X, Bm, Cm = X[0], Bm[0], outer
+                i, j, k = X.ivars
+                if (len({i, j, k}) == 3 and len(lhs.ivars) == 2 and lhs.ivars[0] == i
+                        and Bm.ivars == (j, lhs.ivars[1]) and Cm.ivars == (k, lhs.ivars[1])):
+                    if ocls != "dense2":
+                        raise UnsupportedOutputError("MTTKRP output must be dense-2")
+                    cX = cls[X.tensor]
+                    if cX in ("coo3", "csf") and cls[Bm.tensor] == "dense2" and \
+                            cls[Cm.tensor] == "dense2":
+                        return Plan("mttkrp", f"mttkrp_{cX}",
+                                    {"X": X.tensor, "B": Bm.tensor, "C": Cm.tensor},
+                                    out_format, out_dims)
+                    raise UnsupportedMergeError(
+                        f"no B200 kernel for MTTKRP with X {cX}, B {cls[Bm.tensor]}, "
+                        f"C {cls[Cm.tensor]}")
+    raise UnsupportedMergeError(
+        "no B200 kernel implements this expression/format combination "
+        "(supported: SpMV over coo/csr/ell/dia with dense or hashed x, CSR + COO/CSR -> CSR, "
+        "MTTKRP over COO-3/CSF)")
+
+
+# ---------------------------------------------------------------------------
+# execution
+
+def _dev(st: TensorStorage, device):
+    if st.vals.device != device:
+        return st.to(device, non_blocking=True)
+    return st
+
+
+def _dia_host_offsets(st: TensorStorage):
+    offs = getattr(st, "_host_offsets", None)
+    if offs is None:
+        offs = st.levels[1].offset.cpu().numpy().astype(np.int32)
+        st._host_offsets = offs
+    return offs
+
+
+def _run(p: Plan, inputs: Dict[str, TensorStorage], stats: Optional[EvalStats]):
+    dev = None
+    for st in inputs.values():
+        if st.vals.is_cuda:
+            dev = st.vals.device
+            break
+    if dev is None:
+        dev = torch.device("cuda", torch.cuda.current_device())
+    ops = {role: _dev(inputs[name], dev) for role, name in p.operands.items()}
+
+    if p.pattern == "spmv":
+        A, x = ops["A"], ops["x"]
+        nrows, ncols = A.dims
+        if p.kernel == "spmv_coo":
+            y = K.spmv_coo(nrows, ncols, A.levels[0].crd, A.levels[1].crd, A.vals, x.vals)
+            visits = {"i": int(A.vals.numel())}
+        elif p.kernel == "spmv_csr":
+            y = K.spmv_csr(nrows, ncols, A.levels[1].pos, A.levels[1].crd, A.vals, x.vals)
+            visits = {"i": nrows, "j": int(A.levels[1].crd.numel())}
+        elif p.kernel == "spmv_ell":
+            S = A.levels[0].n
+            y = K.spmv_ell(nrows, ncols, S, A.levels[2].crd, A.vals, x.vals)
+            visits = {"slot": S, "i": S * nrows}
+        elif p.kernel == "spmv_dia":
+            offs = _dia_host_offsets(inputs[p.operands["A"]])
+            y = K.spmv_dia(nrows, ncols, offs, A.vals, x.vals)
+            visits = {"diag": len(offs), "i": int(sum(
+                max(0, min(nrows, ncols - o) - max(0, -o)) for o in offs.tolist()))}
+        else:  # spmv_csr_hashx
+            hx = x.levels[0]
+            y = K.spmv_csr_hashx(nrows, A.levels[1].pos, A.levels[1].crd, A.vals, hx.w, hx.crd,
+                                 x.vals)
+            visits = {"i": nrows, "j": int(A.levels[1].crd.numel())}
+        out = TensorStorage(p.out_format, (nrows,),
+                            [LevelStorage(p.out_format.levels[0], n=nrows, device=dev)], y)
+    elif p.pattern == "add":
+        A, B = ops["A"], ops["B"]
+        nrows = A.dims[0]
+        if p.kernel == "add_csr_coo":
+            c_pos, c_crd, c_vals = K.add_csr(nrows, A.levels[1].pos, A.levels[1].crd, A.vals,
+                                             B.levels[1].crd, B.vals, b_rows=B.levels[0].crd)
+        else:
+            c_pos, c_crd, c_vals = K.add_csr(nrows, A.levels[1].pos, A.levels[1].crd, A.vals,
+                                             B.levels[1].crd, B.vals, b_pos=B.levels[1].pos)
+        f = p.out_format
+        out = TensorStorage(f, A.dims, [LevelStorage(f.levels[0], n=nrows, device=dev),
+                                        LevelStorage(f.levels[1], pos=c_pos, crd=c_crd,
+                                                     device=dev)], c_vals)
+        visits = {"i": nrows, "j": int(c_crd.numel())}
+    else:  # mttkrp
+        X, B, C = ops["X"], ops["B"], ops["C"]
+        I, J, Kd = X.dims
+        R = B.dims[1]
+        Bt, Ct = B.vals.view(J, R), C.vals.view(Kd, R)
+        if p.kernel == "mttkrp_coo3":
+            A = K.mttkrp_coo3(I, J, Kd, X.levels[0].crd, X.levels[1].crd, X.levels[2].crd,
+                              X.vals, Bt, Ct)
+        else:
+            A = K.mttkrp_csf(I, J, Kd, X.levels[0].crd, X.levels[1].pos, X.levels[1].crd,
+                             X.levels[2].pos, X.levels[2].crd, X.vals, Bt, Ct)
+        f = p.out_format
+        out = TensorStorage(f, (I, R), [LevelStorage(f.levels[0], n=I, device=dev),
+                                        LevelStorage(f.levels[1], n=R, device=dev)],
+                            A.reshape(-1))
+        visits = {"i": I, "r": int(X.vals.numel()) * R}
+    if stats is not None:
+        for var, n in visits.items():
+            stats.count(var, p.kernel, n)
+    return out
+
+
+def evaluate(expr, inputs: Dict[str, TensorStorage], out_format: Optional[TensorFormat] = None,
+             out_dims: Optional[Sequence[int]] = None, *, fuse: bool = True,
+             allow_reorder: bool = True, stats: Optional[EvalStats] = None) -> TensorStorage:
+    """Same signature and defaults as the reference (engine.py:739-764).
+
+    Inputs may live on the host (copied to the device first, asynchronously)
+    or on a CUDA device; the result is on the device.  `fuse` and
+    `allow_reorder` are accepted for signature compatibility: every kernel
+    already executes the fused schedule and none needs a reorder stage.
+    """
+    assignment = parse(expr) if isinstance(expr, str) else expr
+    bindings = {name: (s.format, s.dims) for name, s in inputs.items()}
+    checked = validate(assignment, bindings)
+    if out_format is None:
+        out_format = preset("dense", order=len(assignment.lhs.ivars))
+    if out_dims is None:
+        out_dims = tuple(checked.var_extents[v] for v in assignment.lhs.ivars)
+    if tuple(out_dims) != tuple(checked.var_extents[v] for v in assignment.lhs.ivars):
+        raise ValidationError("out_dims disagree with the expression's variable extents")
+    p = plan(checked, bindings, out_format, tuple(out_dims))
+    return _run(p, inputs, stats)
+
+
+def plan_expression(expr, inputs: Dict[str, TensorStorage],
+                    out_format: Optional[TensorFormat] = None) -> Plan:
+    """The kernel binding `evaluate` would use (cf. the reference's `plan`)."""
+    assignment = parse(expr) if isinstance(expr, str) else expr
+    bindings = {name: (s.format, s.dims) for name, s in inputs.items()}
+    checked = validate(assignment, bindings)
+    if out_format is None:
+        out_format = preset("dense", order=len(assignment.lhs.ivars))
+    out_dims = tuple(checked.var_extents[v] for v in assignment.lhs.ivars)
+    return plan(checked, bindings, out_format, out_dims)

@@ -1,0 +1,201 @@
+"""Thin tensor-level wrappers over the C ABI (include/sl_abi.h).
+
+Each function takes CUDA tensors in the reference's storage layouts, checks
+dtype/device/contiguity, allocates outputs and workspace with the torch
+caching allocator, and launches on the current stream.  Nothing here runs on
+the CPU: a non-CUDA tensor raises DeviceError.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _lib
+from .errors import DeviceError
+
+I32, F64 = torch.int32, torch.float64
+
+
+def _t(x, dtype, name):
+    if not isinstance(x, torch.Tensor):
+        raise DeviceError(f"{name} must be a CUDA tensor, got {type(x).__name__}")
+    if not x.is_cuda:
+        raise DeviceError(f"{name} must be a CUDA tensor (no CPU fallback)")
+    if x.dtype != dtype:
+        raise TypeError(f"{name} must be {dtype}, got {x.dtype}")
+    return x if x.is_contiguous() else x.contiguous()
+
+
+def _out(y, n, dtype, like, name):
+    if y is None:
+        return torch.empty(n, dtype=dtype, device=like.device)
+    y = _t(y, dtype, name)
+    if y.numel() < n:
+        raise ValueError(f"{name} has {y.numel()} elements, needs {n}")
+    return y
+
+
+def _ws(nbytes, like):
+    if nbytes == 0:
+        return None
+    return torch.empty(int(nbytes), dtype=torch.uint8, device=like.device)
+
+
+L = _lib.load
+S = _lib.stream_handle
+P = _lib.ptr
+
+
+# ---- SpMV -------------------------------------------------------------------
+
+def spmv_coo(nrows, ncols, rows, cols, vals, x, y=None):
+    rows, cols = _t(rows, I32, "rows"), _t(cols, I32, "cols")
+    vals, x = _t(vals, F64, "vals"), _t(x, F64, "x")
+    y = _out(y, nrows, F64, x, "y")
+    _lib.check(L().sl_spmv_coo_f64(nrows, ncols, rows.numel(), P(rows), P(cols), P(vals), P(x),
+                                   P(y), S()), "spmv_coo")
+    return y
+
+
+def spmv_csr(nrows, ncols, pos, crd, vals, x, y=None, variant=0, ws=None):
+    pos, crd = _t(pos, I32, "pos"), _t(crd, I32, "crd")
+    vals, x = _t(vals, F64, "vals"), _t(x, F64, "x")
+    y = _out(y, nrows, F64, x, "y")
+    nnz = crd.numel()
+    need = L().sl_spmv_csr_workspace_bytes(nrows, nnz, variant)
+    if ws is None or ws.numel() < need:
+        ws = _ws(need, x)
+    _lib.check(L().sl_spmv_csr_f64(nrows, ncols, nnz, P(pos), P(crd), P(vals), P(x), P(y),
+                                   variant, P(ws), 0 if ws is None else ws.numel(), S()),
+               "spmv_csr")
+    return y
+
+
+def spmv_ell(nrows, ncols, nslots, crd, vals, x, y=None):
+    crd, vals, x = _t(crd, I32, "crd"), _t(vals, F64, "vals"), _t(x, F64, "x")
+    y = _out(y, nrows, F64, x, "y")
+    _lib.check(L().sl_spmv_ell_f64(nrows, ncols, nslots, P(crd), P(vals), P(x), P(y), S()),
+               "spmv_ell")
+    return y
+
+
+def spmv_dia(nrows, ncols, offsets, vals, x, y=None):
+    """`offsets`: host numpy int32 (passed as kernel parameters) or a CUDA tensor."""
+    vals, x = _t(vals, F64, "vals"), _t(x, F64, "x")
+    y = _out(y, nrows, F64, x, "y")
+    if isinstance(offsets, torch.Tensor) and offsets.is_cuda:
+        offs = _t(offsets, I32, "offsets")
+        nd, optr, on_host = offs.numel(), P(offs), 0
+    else:
+        offs = np.ascontiguousarray(offsets, dtype=np.int32)
+        nd, optr, on_host = len(offs), offs.ctypes.data, 1
+        if nd > 32:
+            return spmv_dia(nrows, ncols, torch.as_tensor(offs, device=x.device), vals, x, y)
+    _lib.check(L().sl_spmv_dia_f64(nrows, ncols, nd, optr, on_host, P(vals), P(x), P(y), S()),
+               "spmv_dia")
+    return y
+
+
+def spmv_csr_hashx(nrows, pos, crd, vals, w, x_crd, x_vals, y=None):
+    pos, crd, vals = _t(pos, I32, "pos"), _t(crd, I32, "crd"), _t(vals, F64, "vals")
+    x_crd, x_vals = _t(x_crd, I32, "x_crd"), _t(x_vals, F64, "x_vals")
+    y = _out(y, nrows, F64, vals, "y")
+    _lib.check(L().sl_spmv_csr_hashx_f64(nrows, P(pos), P(crd), P(vals), w, P(x_crd), P(x_vals),
+                                         P(y), S()), "spmv_csr_hashx")
+    return y
+
+
+# ---- hashed level -------------------------------------------------------------
+
+def hashed_locate(coords, w, crd, parent=None, group=8):
+    coords, crd = _t(coords, I32, "coords"), _t(crd, I32, "crd")
+    parent = None if parent is None else _t(parent, I32, "parent")
+    pos = torch.empty(coords.numel(), dtype=I32, device=coords.device)
+    found = torch.empty(coords.numel(), dtype=torch.uint8, device=coords.device)
+    _lib.check(L().sl_hashed_locate(coords.numel(), P(parent), P(coords), w, P(crd), P(pos),
+                                    P(found), group, S()), "hashed_locate")
+    return pos, found
+
+
+def hashed_insert(coords, w, nseg=1, parent=None, crd=None):
+    """Bulk hashed insert; returns (crd table, device error flag)."""
+    coords = _t(coords, I32, "coords")
+    parent = None if parent is None else _t(parent, I32, "parent")
+    if crd is None:
+        crd = torch.empty(nseg * w, dtype=I32, device=coords.device)
+        _lib.check(L().sl_hashed_insert_init(crd.numel(), P(crd), S()), "insert_init")
+    err = torch.zeros(1, dtype=I32, device=coords.device)
+    _lib.check(L().sl_hashed_insert(coords.numel(), P(parent), P(coords), w, P(crd), P(err), S()),
+               "hashed_insert")
+    return crd, err
+
+
+# ---- C = A + B -----------------------------------------------------------------
+
+def add_csr(nrows, a_pos, a_crd, a_vals, b_cols, b_vals, b_rows=None, b_pos=None, sync=True):
+    """CSR + (COO | CSR) -> CSR.  Returns (c_pos, c_crd, c_vals); with
+    sync=False the crd/vals buffers are upper-bound sized (nnz_a + nnz_b) and
+    nnz_c = c_pos[nrows] is left on the device."""
+    a_pos, a_crd, a_vals = _t(a_pos, I32, "a_pos"), _t(a_crd, I32, "a_crd"), _t(a_vals, F64, "a_vals")
+    b_cols, b_vals = _t(b_cols, I32, "b_cols"), _t(b_vals, F64, "b_vals")
+    b_rows = None if b_rows is None else _t(b_rows, I32, "b_rows")
+    b_pos = None if b_pos is None else _t(b_pos, I32, "b_pos")
+    bnnz = b_cols.numel()
+    dev = a_vals.device
+    c_pos = torch.empty(nrows + 1, dtype=I32, device=dev)
+    cap = max(a_crd.numel() + bnnz, 1)
+    c_crd = torch.empty(cap, dtype=I32, device=dev)
+    c_vals = torch.empty(cap, dtype=F64, device=dev)
+    need = L().sl_add_csr_workspace_bytes(nrows, bnnz)
+    ws = _ws(need, a_vals)
+    wsn = 0 if ws is None else ws.numel()
+    _lib.check(L().sl_add_csr_count(nrows, P(a_pos), P(a_crd), bnnz, P(b_pos), P(b_rows),
+                                    P(b_cols), P(c_pos), P(ws), wsn, S()), "add_count")
+    _lib.check(L().sl_add_csr_fill(nrows, P(a_pos), P(a_crd), P(a_vals), bnnz, P(b_pos),
+                                   P(b_rows), P(b_cols), P(b_vals), P(c_pos), P(c_crd), P(c_vals),
+                                   P(ws), wsn, S()), "add_fill")
+    if sync:
+        n = int(c_pos[nrows].item())
+        return c_pos, c_crd[:n], c_vals[:n]
+    return c_pos, c_crd, c_vals
+
+
+# ---- MTTKRP ---------------------------------------------------------------------
+
+def _mttkrp_ws(nnz, R, like, ws):
+    need = L().sl_mttkrp_workspace_bytes(nnz, R)
+    if ws is not None and ws.numel() >= need:
+        return ws
+    return _ws(need, like)
+
+
+def mttkrp_coo3(I, J, K, i, j, k, vals, B, C, A=None, ws=None):
+    i, j, k = _t(i, I32, "i"), _t(j, I32, "j"), _t(k, I32, "k")
+    vals, B, C = _t(vals, F64, "vals"), _t(B, F64, "B"), _t(C, F64, "C")
+    R = B.shape[-1]
+    A = _out(A, I * R, F64, vals, "A").view(I, R) if A is None else _t(A, F64, "A")
+    ws = _mttkrp_ws(i.numel(), R, vals, ws)
+    _lib.check(L().sl_mttkrp_coo3_f64(I, J, K, R, i.numel(), P(i), P(j), P(k), P(vals), P(B),
+                                      P(C), P(A), P(ws), 0 if ws is None else ws.numel(), S()),
+               "mttkrp_coo3")
+    return A
+
+
+def mttkrp_csf(I, J, K, crd0, pos1, crd1, pos2, crd2, vals, B, C, A=None, ws=None):
+    crd0, pos1, crd1 = _t(crd0, I32, "crd0"), _t(pos1, I32, "pos1"), _t(crd1, I32, "crd1")
+    pos2, crd2 = _t(pos2, I32, "pos2"), _t(crd2, I32, "crd2")
+    vals, B, C = _t(vals, F64, "vals"), _t(B, F64, "B"), _t(C, F64, "C")
+    R = B.shape[-1]
+    A = _out(A, I * R, F64, vals, "A").view(I, R) if A is None else _t(A, F64, "A")
+    ws = _mttkrp_ws(vals.numel(), R, vals, ws)
+    _lib.check(L().sl_mttkrp_csf_f64(I, J, K, R, crd0.numel(), crd1.numel(), vals.numel(),
+                                     P(crd0), P(pos1), P(crd1), P(pos2), P(crd2), P(vals), P(B),
+                                     P(C), P(A), P(ws), 0 if ws is None else ws.numel(), S()),
+               "mttkrp_csf")
+    return A
+
+
+def l2_flush(buf):
+    buf = _t(buf, torch.uint8, "buf")
+    _lib.check(L().sl_l2_flush(P(buf), buf.numel(), S()), "l2_flush")

@@ -1,0 +1,191 @@
+"""GPU: the reference-facing API — device level functions (replaying
+pkg/tests/test_levels.py through sl_level_query) and `evaluate` over every
+supported pattern, checked against the reference's goldens."""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import paper_1804_10112_b200 as slb  # noqa: E402
+from paper_1804_10112_b200 import formats as F  # noqa: E402
+from paper_1804_10112_b200 import levels as L  # noqa: E402
+from paper_1804_10112_b200.errors import (HashSegmentFullError, UnsupportedCapabilityError,  # noqa: E402
+                                          UnsupportedMergeError)
+
+
+def bits(a):
+    if isinstance(a, torch.Tensor):
+        a = a.cpu().numpy()
+    return np.ascontiguousarray(a, dtype=np.float64).view(np.int64)
+
+
+def make_storage(kind):   # test_levels.py:27-40
+    E = L.EMPTY
+    if kind is L.LevelKind.DENSE:
+        return L.LevelStorage(L.dense(), n=4)
+    if kind is L.LevelKind.RANGE:
+        return L.LevelStorage(L.range_level(), n=4, m=6, offset=[0, -1])
+    if kind is L.LevelKind.COMPRESSED:
+        return L.LevelStorage(L.compressed(), pos=[0, 2], crd=[0, 1])
+    if kind is L.LevelKind.SINGLETON:
+        return L.LevelStorage(L.singleton(), crd=[0, 1])
+    if kind is L.LevelKind.OFFSET:
+        return L.LevelStorage(L.offset_level(), offset=[0, -1], range_n=4)
+    return L.LevelStorage(L.hashed(), w=4, crd=[E] * 4)
+
+
+SUPPORTED = {
+    L.LevelKind.DENSE: {"coord_bounds", "coord_access", "locate", "size"},
+    L.LevelKind.RANGE: {"coord_bounds", "coord_access"},
+    L.LevelKind.COMPRESSED: {"pos_bounds", "pos_access"},
+    L.LevelKind.SINGLETON: {"pos_bounds", "pos_access"},
+    L.LevelKind.OFFSET: {"pos_bounds", "pos_access"},
+    L.LevelKind.HASHED: {"pos_bounds", "pos_access", "locate", "size"},
+}
+CALLS = {
+    "coord_bounds": lambda lv: lv.coord_bounds([0]),
+    "coord_access": lambda lv: lv.coord_access(0, [0, 0]),
+    "pos_bounds": lambda lv: lv.pos_bounds(0),
+    "pos_access": lambda lv: lv.pos_access(0, [0]),
+    "locate": lambda lv: lv.locate(0, [0, 0]),
+    "size": lambda lv: lv.size(1),
+}
+
+
+@pytest.mark.parametrize("kind", list(L.LevelKind))
+@pytest.mark.parametrize("fn", sorted(CALLS))
+def test_capability_conformance_device(kind, fn):
+    lv = make_storage(kind)
+    if fn in SUPPORTED[kind]:
+        CALLS[fn](lv)
+    else:
+        with pytest.raises(UnsupportedCapabilityError):
+            CALLS[fn](lv)
+
+
+def test_level_function_kats(level_kats):
+    k = level_kats
+    lv = L.LevelStorage(L.range_level(), n=4, m=6, offset=k["range_offsets"])
+    lo, hi = lv.query("coord_bounds", np.arange(4))
+    assert np.array_equal(np.stack([lo.cpu(), hi.cpu()], 1).reshape(-1), k["range_bounds"])
+    q = k["range_access_in"].reshape(-1, 2)
+    p, f = lv.query("coord_access", q[:, 0], q[:, 1])
+    assert np.array_equal(p.cpu().numpy(), k["range_access_out"]) and f.cpu().numpy().all()
+    lv = L.LevelStorage(L.offset_level(), offset=k["range_offsets"], range_n=4)
+    q = k["offset_access_in"].reshape(-1, 2)
+    c, f = lv.query("pos_access", q[:, 0], q[:, 1])
+    assert np.array_equal(c.cpu().numpy(), k["offset_access_out"])
+    lv = L.LevelStorage(L.compressed(), pos=k["compressed_pos"], crd=k["compressed_crd"])
+    lo, hi = lv.query("pos_bounds", np.arange(4))
+    assert np.array_equal(np.stack([lo.cpu(), hi.cpu()], 1).reshape(-1), k["compressed_bounds"])
+    c, _ = lv.query("pos_access", np.arange(7))
+    assert np.array_equal(c.cpu().numpy(), k["compressed_access"])
+    for tag, w in (("h4", 4), ("h8", 8), ("h16", 16)):
+        lv = L.LevelStorage(L.hashed(), w=w, crd=k[f"{tag}_crd"])
+        p, f = lv.query("locate", np.zeros(len(k[f"{tag}_locate_q"])), k[f"{tag}_locate_q"])
+        assert np.array_equal(p.cpu().numpy(), k[f"{tag}_locate_pos"]), tag
+        assert np.array_equal(f.cpu().numpy(), k[f"{tag}_locate_found"]), tag
+        _, f = lv.query("pos_access", np.arange(w))
+        assert np.array_equal(f.cpu().numpy(), k[f"{tag}_pos_found"]), tag
+    lv = L.LevelStorage(L.dense(), n=6)
+    assert lv.locate(1, [1, 5]) == (int(k["dense_locate_1_5"][0]), True)
+    assert lv.coord_access(3, [3, 4]) == (int(k["dense_access_3_4"][0]), True)
+    assert lv.size(4) == int(k["dense_size_4"][0])
+    # scalar API (test_levels.py:107-122, 146-200)
+    assert L.LevelStorage(L.range_level(), n=4, m=6, offset=[0, -1]).coord_bounds([1]) == (1, 4)
+    assert L.LevelStorage(L.hashed(), w=4, crd=[L.EMPTY] * 16).pos_bounds(2) == (8, 12)
+    assert L.LevelStorage(L.offset_level(), offset=[-2, -1, 0, 1],
+                          range_n=4).pos_access(7, [1, 3]) == (2, True)
+    lv = L.LevelStorage(L.hashed(), w=4, crd=[L.EMPTY, 1, L.EMPTY, 3])
+    assert lv.locate(0, [3]) == (3, True) and lv.locate(0, [2]) == (-1, False)
+
+
+def test_device_insert_protocol(level_kats):
+    lv = L.LevelStorage(L.hashed(), w=4)
+    lv.insert_init(1, 4)
+    assert lv.crd.cpu().tolist() == [L.EMPTY] * 4
+    for c in (3, 2, 6):
+        lv.insert_coord(c % 4, c)
+    assert lv.crd.cpu().tolist() == level_kats["h4_crd"].tolist()   # one-at-a-time = sequential
+    lv.insert_coord(2, 2)  # idempotent
+    assert sorted(lv.crd.cpu().tolist()) == sorted(level_kats["h4_crd"].tolist())
+    lv = L.LevelStorage(L.hashed(), w=2)
+    lv.insert_init(1, 2)
+    lv.insert_coord(0, 0)
+    lv.insert_coord(0, 2)
+    with pytest.raises(HashSegmentFullError):
+        lv.insert_coord(0, 4)
+
+
+def test_append_protocol(level_kats):
+    lv = L.LevelStorage(L.compressed())
+    lv.append_init(4, 0)
+    p = 0
+    for row, cols in enumerate([[3, 5], [], [0, 4], [1, 2, 3]]):
+        for c in cols:
+            lv.append_coord(p, c)
+            p += 1
+        lv.append_edges(row, p - len(cols), p)
+    lv.append_finalize(4, p)
+    assert lv.pos.cpu().tolist() == level_kats["append_pos"].tolist()
+    assert lv.crd.cpu().tolist() == level_kats["append_crd"].tolist()
+
+
+def test_evaluate_spmv_all_formats(golden):
+    c = golden["spmv"]["spmv_rand2"]
+    n, m = int(c["nrows"]), int(c["ncols"])
+    x = F.dense_storage(c["x"])
+    mats = {
+        "coo": F.coo_storage(c["coo_rows"], c["coo_cols"], c["coo_vals"], (n, m)),
+        "csr": F.csr_storage(c["csr_pos"], c["csr_crd"], c["csr_vals"], (n, m)),
+        "ell": F.ell_storage(int(c["ell_nslots"]), c["ell_crd"], c["ell_vals"], (n, m)),
+        "dia": F.dia_storage(c["dia_offsets"], c["dia_vals"], (n, m)),
+    }
+    for fmt, A in mats.items():
+        stats = slb.EvalStats()
+        y = slb.evaluate("y(i) = A(i,j) * x(j)", {"A": A, "x": x}, stats=stats)
+        assert np.array_equal(bits(y.vals), bits(c[f"{fmt}_y"])), fmt
+        assert stats.total() > 0
+        # commuted product is bitwise the same
+        y2 = slb.evaluate("y(i) = x(j) * A(i,j)", {"A": A, "x": x})
+        assert np.array_equal(bits(y2.vals), bits(c[f"{fmt}_y"])), fmt
+    hx = F.hash_vector_storage(c["hash_crd"], c["hash_vals"], m, int(c["hash_w"]))
+    y = slb.evaluate("y(i) = A(i,j) * x(j)", {"A": mats["csr"], "x": hx})
+    assert np.array_equal(bits(y.vals), bits(c["hash_y"]))
+    with pytest.raises(UnsupportedMergeError):
+        slb.evaluate("y(i) = A(i,j) * x(j)", {"A": mats["coo"], "x": hx})
+
+
+def test_evaluate_host_inputs_moved_to_device(golden):
+    c = golden["spmv"]["spmv_rand3"]
+    n, m = int(c["nrows"]), int(c["ncols"])
+    A = F.csr_storage(c["csr_pos"], c["csr_crd"], c["csr_vals"], (n, m), device=None)
+    x = F.dense_storage(c["x"], device=None)
+    assert not A.vals.is_cuda
+    y = slb.evaluate("y(i) = A(i,j) * x(j)", {"A": A, "x": x})
+    assert y.vals.is_cuda and np.array_equal(bits(y.vals), bits(c["csr_y"]))
+
+
+def test_evaluate_add_and_mttkrp(golden, orc):
+    c = golden["add"]["add_rand1"]
+    n, m = int(c["nrows"]), int(c["ncols"])
+    A = F.csr_storage(c["a_pos"], c["a_crd"], c["a_vals"], (n, m))
+    B = F.coo_storage(c["b_rows"], c["b_cols"], c["b_vals"], (n, m))
+    for expr in ("C(i,j) = A(i,j) + B(i,j)", "C(i,j) = B(i,j) + A(i,j)"):
+        C = slb.evaluate(expr, {"A": A, "B": B}, F.preset("csr"))
+        assert np.array_equal(C.levels[1].pos.cpu().numpy(), c["c_pos"])
+        assert np.array_equal(C.levels[1].crd.cpu().numpy(), c["c_crd"])
+        assert np.array_equal(bits(C.vals), bits(c["c_vals"]))
+    t = golden["mttkrp"]["mttkrp_r32"]
+    I, J, Kd, R = (int(t[k]) for k in ("I", "J", "K", "R"))
+    X1 = F.coo3_storage(t["coo_i"], t["coo_j"], t["coo_k"], t["coo_vals"], (I, J, Kd))
+    X2 = F.csf_storage(t["csf_pos0"], t["csf_crd0"], t["csf_pos1"], t["csf_crd1"], t["csf_pos2"],
+                       t["csf_crd2"], t["csf_vals"], (I, J, Kd))
+    Bs, Cs = F.dense_storage(t["B"], (J, R)), F.dense_storage(t["C"], (Kd, R))
+    _, absA = orc.mttkrp_coo3(I, t["coo_i"], t["coo_j"], t["coo_k"], t["coo_vals"], t["B"], t["C"])
+    for X in (X1, X2):
+        out = slb.evaluate("A(i,r) = X(i,j,k) * B(j,r) * C(k,r)", {"X": X, "B": Bs, "C": Cs})
+        ok, err = orc.within_condition(out.vals.cpu().numpy().reshape(I, R), t["A_coo"], absA)
+        assert ok, err

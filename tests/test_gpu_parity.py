@@ -1,0 +1,313 @@
+"""GPU parity: every kernel against the reference's golden vectors and the C
+oracle on the same seeded inputs.
+
+Bars: SpMV y and A+B (structure and values) bit-exact; MTTKRP within the
+condition-scaled tolerance |gpu - ref| <= 1e-12 * max(|ref|, sum|terms|)
+(north star: fp64 reductions within rtol 1e-12), plus run-to-run determinism.
+"""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from paper_1804_10112_b200 import kernels as K  # noqa: E402
+from paper_1804_10112_b200 import workloads as wl  # noqa: E402
+
+RTOL = 1e-12   # MTTKRP tolerance (condition-scaled)
+
+
+def cuda(a, dtype=None):
+    a = np.asarray(a)
+    if dtype is not None:
+        a = a.astype(dtype)
+    return torch.as_tensor(np.ascontiguousarray(a), device="cuda")
+
+
+def bits(a):
+    if isinstance(a, torch.Tensor):
+        a = a.cpu().numpy()
+    return np.ascontiguousarray(a, dtype=np.float64).view(np.int64)
+
+
+# ---------------------------------------------------------------------------
+# SpMV against the reference's goldens
+
+def test_spmv_goldens_all_formats(golden):
+    for name, c in golden["spmv"].items():
+        nrows, ncols = int(c["nrows"]), int(c["ncols"])
+        x = cuda(c["x"], np.float64)
+        if "coo_y" in c:
+            y = K.spmv_coo(nrows, ncols, cuda(c["coo_rows"], np.int32),
+                           cuda(c["coo_cols"], np.int32), cuda(c["coo_vals"], np.float64), x)
+            assert np.array_equal(bits(y), bits(c["coo_y"])), name
+        if "csr_y" in c:
+            for variant in (0, 1, 2):
+                y = K.spmv_csr(nrows, ncols, cuda(c["csr_pos"], np.int32),
+                               cuda(c["csr_crd"], np.int32), cuda(c["csr_vals"], np.float64), x,
+                               variant=variant)
+                assert np.array_equal(bits(y), bits(c["csr_y"])), (name, variant)
+        if "ell_y" in c:
+            y = K.spmv_ell(nrows, ncols, int(c["ell_nslots"]), cuda(c["ell_crd"], np.int32),
+                           cuda(c["ell_vals"], np.float64), x)
+            assert np.array_equal(bits(y), bits(c["ell_y"])), name
+        if "dia_y" in c:
+            y = K.spmv_dia(nrows, ncols, np.asarray(c["dia_offsets"], np.int32),
+                           cuda(c["dia_vals"], np.float64), x)
+            assert np.array_equal(bits(y), bits(c["dia_y"])), name
+            y2 = K.spmv_dia(nrows, ncols, cuda(c["dia_offsets"], np.int32),
+                            cuda(c["dia_vals"], np.float64), x)
+            assert np.array_equal(bits(y2), bits(c["dia_y"])), name
+        if "hash_y" in c:
+            y = K.spmv_csr_hashx(nrows, cuda(c["csr_pos"], np.int32),
+                                 cuda(c["csr_crd"], np.int32), cuda(c["csr_vals"], np.float64),
+                                 int(c["hash_w"]), cuda(c["hash_crd"], np.int32),
+                                 cuda(c["hash_vals"], np.float64))
+            assert np.array_equal(bits(y), bits(c["hash_y"])), name
+
+
+# ---------------------------------------------------------------------------
+# SpMV against the oracle: medium, ragged and full BASELINE sizes
+
+@pytest.mark.parametrize("n,nnz,lam,seed", [
+    (3000, 30000, 10.0, 1), (5000, 200, 0.05, 2), (1, 4000, 1.0, 3), (20000, 20000, 1.0, 4),
+    (777, 60000, 77.0, 5)])
+def test_spmv_coo_csr_vs_oracle(orc, n, nnz, lam, seed):
+    d = wl.coo_spmv(n=n, ncols=max(n, 4000), nnz=nnz, lam=lam, seed=seed)
+    ref, _ = orc.spmv_coo(n, d["rows"], d["cols"], d["vals"], d["x"])
+    x = cuda(d["x"])
+    y = K.spmv_coo(n, d["ncols"], cuda(d["rows"]), cuda(d["cols"]), cuda(d["vals"]), x)
+    assert np.array_equal(bits(y), bits(ref))
+    pos = wl.coo_to_csr_pos(d["rows"], n)
+    for variant in (0, 1, 2):
+        y = K.spmv_csr(n, d["ncols"], cuda(pos), cuda(d["cols"]), cuda(d["vals"]), x,
+                       variant=variant)
+        assert np.array_equal(bits(y), bits(ref)), variant
+    e = wl.csr_to_ell(pos, d["cols"], d["vals"], n)
+    y = K.spmv_ell(n, d["ncols"], e["nslots"], cuda(e["crd"]), cuda(e["vals"]), x)
+    ref_e, _ = orc.spmv_ell(n, e["nslots"], e["crd"], e["vals"], d["x"])
+    assert np.array_equal(bits(y), bits(ref_e))
+
+
+def test_spmv_coo_long_rows_cross_tiles(orc):
+    # rows far longer than one 2048-nonzero tile: the owner reads forward
+    rows = np.repeat(np.arange(6, dtype=np.int32), [5000, 1, 0, 9000, 3, 0])
+    rng = np.random.default_rng(0)
+    cols = np.concatenate([np.sort(rng.choice(20000, k, replace=False)) for k in
+                           [5000, 1, 0, 9000, 3, 0]]).astype(np.int32)
+    vals = rng.uniform(-1, 1, len(rows))
+    x = rng.uniform(-1, 1, 20000)
+    ref, _ = orc.spmv_coo(8, rows, cols, vals, x)
+    y = K.spmv_coo(8, 20000, cuda(rows), cuda(cols), cuda(vals), cuda(x))
+    assert np.array_equal(bits(y), bits(ref))
+
+
+def test_spmv_empty_matrix():
+    x = cuda(np.ones(5))
+    y = K.spmv_coo(9, 5, cuda(np.zeros(0, np.int32)), cuda(np.zeros(0, np.int32)),
+                   cuda(np.zeros(0)), x)
+    assert np.array_equal(bits(y), bits(np.zeros(9)))
+    y = K.spmv_csr(9, 5, cuda(np.zeros(10, np.int32)), cuda(np.zeros(0, np.int32)),
+                   cuda(np.zeros(0)), x, variant=2)
+    assert np.array_equal(bits(y), bits(np.zeros(9)))
+
+
+def test_spmv_dia_vs_oracle_odd_shapes(orc):
+    rng = np.random.default_rng(3)
+    for nrows, ncols, offs in [(1000, 1300, [-999, -3, 0, 7, 1299]), (257, 100, [-256, -1, 0, 99]),
+                               (5, 5, [-4, -2, 0, 2, 4]), (4096, 4096, list(range(-40, 41, 3)))]:
+        offs = np.array(offs, dtype=np.int32)
+        vals = rng.uniform(-1, 1, len(offs) * nrows)
+        x = rng.uniform(-1, 1, ncols)
+        ref, _ = orc.spmv_dia(nrows, ncols, offs, vals, x)
+        y = K.spmv_dia(nrows, ncols, offs, cuda(vals), cuda(x))
+        assert np.array_equal(bits(y), bits(ref)), (nrows, ncols)
+
+
+@pytest.mark.slow
+def test_full_size_spmv_bit_exact(orc):
+    d = wl.coo_spmv()
+    ref, _ = orc.spmv_coo(d["nrows"], d["rows"], d["cols"], d["vals"], d["x"])
+    y = K.spmv_coo(d["nrows"], d["ncols"], cuda(d["rows"]), cuda(d["cols"]), cuda(d["vals"]),
+                   cuda(d["x"]))
+    assert np.array_equal(bits(y), bits(ref))
+    s = wl.stencil27()
+    ref, _ = orc.spmv_csr(s["nrows"], s["pos"], s["crd"], s["vals"], s["x"])
+    x = cuda(s["x"])
+    for variant in (0, 1, 2):
+        y = K.spmv_csr(s["nrows"], s["ncols"], cuda(s["pos"]), cuda(s["crd"]), cuda(s["vals"]),
+                       x, variant=variant)
+        assert np.array_equal(bits(y), bits(ref)), variant
+    e = wl.csr_to_ell(s["pos"], s["crd"], s["vals"], s["nrows"])
+    ref_e, _ = orc.spmv_ell(s["nrows"], e["nslots"], e["crd"], e["vals"], s["x"])
+    y = K.spmv_ell(s["nrows"], s["ncols"], e["nslots"], cuda(e["crd"]), cuda(e["vals"]), x)
+    assert np.array_equal(bits(y), bits(ref_e))
+    # ELL's padding terms 0.0*x[0] do not change finite results: ELL == CSR here
+    assert np.array_equal(bits(ref_e), bits(ref))
+    g = wl.dia7()
+    ref, _ = orc.spmv_dia(g["nrows"], g["ncols"], g["offsets"], g["vals"], g["x"])
+    y = K.spmv_dia(g["nrows"], g["ncols"], g["offsets"], cuda(g["vals"]), cuda(g["x"]))
+    assert np.array_equal(bits(y), bits(ref))
+
+
+# ---------------------------------------------------------------------------
+# hashed level
+
+@pytest.mark.parametrize("group", [1, 4, 8, 16, 32])
+def test_hashed_locate_kats(level_kats, group):
+    k = level_kats
+    for tag, w in (("h4", 4), ("h8", 8), ("h16", 16)):
+        pos, found = K.hashed_locate(cuda(k[f"{tag}_locate_q"], np.int32), w,
+                                     cuda(k[f"{tag}_crd"], np.int32), group=group)
+        assert np.array_equal(pos.cpu().numpy(), k[f"{tag}_locate_pos"]), (tag, group)
+        assert np.array_equal(found.cpu().numpy().astype(np.int32), k[f"{tag}_locate_found"])
+    pos, found = K.hashed_locate(cuda([7], np.int32), 4, cuda(k["hfull_crd"], np.int32),
+                                 group=group)
+    assert (int(pos[0]), int(found[0])) == tuple(k["hfull_locate_7"])
+    w = int(k["hseg_w"])
+    pos, found = K.hashed_locate(cuda(k["hseg_q_coord"], np.int32), w,
+                                 cuda(k["hseg_crd"], np.int32),
+                                 parent=cuda(k["hseg_q_parent"], np.int32), group=group)
+    assert np.array_equal(pos.cpu().numpy(), k["hseg_q_pos"])
+    assert np.array_equal(found.cpu().numpy().astype(np.int32), k["hseg_q_found"])
+
+
+@pytest.mark.parametrize("group", [1, 8, 32])
+def test_hashed_locate_vs_oracle_high_load(orc, group):
+    h = wl.hash_vector(n=300_000, m=120_000, width=131_072, seed=9)   # load 0.92: long probes
+    rng = np.random.default_rng(1)
+    q = rng.integers(0, 300_000, 500_000).astype(np.int32)
+    rp, rf = orc.hashed_locate(q, 131_072, h["crd"])
+    pos, found = K.hashed_locate(cuda(q), 131_072, cuda(h["crd"]), group=group)
+    assert np.array_equal(pos.cpu().numpy(), rp)
+    assert np.array_equal(found.cpu().numpy().astype(bool), rf)
+
+
+def test_hashed_insert_set_semantics(orc):
+    rng = np.random.default_rng(5)
+    w, nseg = 64, 50
+    parent = rng.integers(0, nseg, 2000).astype(np.int32)
+    coords = rng.integers(0, 200, 2000).astype(np.int32)
+    crd, err = K.hashed_insert(cuda(coords), w, nseg=nseg, parent=cuda(parent))
+    assert int(err.item()) == 0
+    table = crd.cpu().numpy()
+    ref, st = orc.hashed_insert(coords, w, nseg=nseg, parent=parent)
+    assert st == 0
+    for s in range(nseg):
+        got = set(table[s * w:(s + 1) * w].tolist()) - {-1}
+        exp = set(ref[s * w:(s + 1) * w].tolist()) - {-1}
+        assert got == exp
+    # every inserted coordinate is found through locate, nothing else is
+    pos, found = K.hashed_locate(cuda(coords), w, crd, parent=cuda(parent))
+    assert found.cpu().numpy().all()
+    assert np.array_equal(table[pos.cpu().numpy()], coords)
+    # overflow
+    crd, err = K.hashed_insert(cuda(np.array([0, 2, 4], np.int32)), 2)
+    assert int(err.item()) == 4
+
+
+def test_spmv_hashx_full_h1(orc):
+    d = wl.coo_spmv()
+    h = wl.hash_vector()
+    pos = wl.coo_to_csr_pos(d["rows"], d["nrows"])
+    ref, _ = orc.spmv_csr_hashx(d["nrows"], pos, d["cols"], d["vals"], h["width"], h["crd"],
+                                h["vals"])
+    y = K.spmv_csr_hashx(d["nrows"], cuda(pos), cuda(d["cols"]), cuda(d["vals"]), h["width"],
+                         cuda(h["crd"]), cuda(h["vals"]))
+    assert np.array_equal(bits(y), bits(ref))
+
+
+# ---------------------------------------------------------------------------
+# A + B
+
+def test_add_goldens(golden):
+    for name, c in golden["add"].items():
+        kw = {"b_pos": cuda(c["b_pos"], np.int32)} if "b_pos" in c else \
+             {"b_rows": cuda(c["b_rows"], np.int32)}
+        pos, crd, vals = K.add_csr(int(c["nrows"]), cuda(c["a_pos"], np.int32),
+                                   cuda(c["a_crd"], np.int32), cuda(c["a_vals"], np.float64),
+                                   cuda(c["b_cols"], np.int32), cuda(c["b_vals"], np.float64),
+                                   **kw)
+        assert np.array_equal(pos.cpu().numpy(), c["c_pos"]), name
+        assert np.array_equal(crd.cpu().numpy(), c["c_crd"]), name
+        assert np.array_equal(bits(vals), bits(c["c_vals"])), name
+
+
+@pytest.mark.parametrize("n,nnz,seed", [(2000, 9000, 1), (100_000, 500_000, 2), (70_000, 100, 3)])
+def test_add_vs_oracle(orc, n, nnz, seed):
+    d = wl.add_ab(n=n, nnz_a=nnz, nnz_b=nnz, seed=seed)
+    rp, rc, rv = orc.add_csr(n, d["a_pos"], d["a_crd"], d["a_vals"], d["b_cols"], d["b_vals"],
+                             b_rows=d["b_rows"])
+    pos, crd, vals = K.add_csr(n, cuda(d["a_pos"]), cuda(d["a_crd"]), cuda(d["a_vals"]),
+                               cuda(d["b_cols"]), cuda(d["b_vals"]), b_rows=cuda(d["b_rows"]))
+    assert np.array_equal(pos.cpu().numpy(), rp)
+    assert np.array_equal(crd.cpu().numpy(), rc)
+    assert np.array_equal(bits(vals), bits(rv))
+
+
+@pytest.mark.slow
+def test_add_full_size(orc):
+    d = wl.add_ab()
+    n = d["nrows"]
+    rp, rc, rv = orc.add_csr(n, d["a_pos"], d["a_crd"], d["a_vals"], d["b_cols"], d["b_vals"],
+                             b_rows=d["b_rows"], threads=0)
+    pos, crd, vals = K.add_csr(n, cuda(d["a_pos"]), cuda(d["a_crd"]), cuda(d["a_vals"]),
+                               cuda(d["b_cols"]), cuda(d["b_vals"]), b_rows=cuda(d["b_rows"]))
+    assert np.array_equal(pos.cpu().numpy(), rp)
+    assert np.array_equal(crd.cpu().numpy(), rc)
+    assert np.array_equal(bits(vals), bits(rv))
+    # structure property: nnz(C) = nnz(A) + nnz(B) - overlap
+    assert int(rp[-1]) == len(d["a_crd"]) + len(d["b_cols"]) - d["overlap"]
+
+
+# ---------------------------------------------------------------------------
+# MTTKRP
+
+def _mttkrp_both(c_or_d, I, J, Kd, coo, csf, B, C):
+    Bt, Ct = cuda(B), cuda(C)
+    A1 = K.mttkrp_coo3(I, J, Kd, cuda(coo[0]), cuda(coo[1]), cuda(coo[2]), cuda(coo[3]), Bt, Ct)
+    A2 = K.mttkrp_csf(I, J, Kd, cuda(csf["crd0"]), cuda(csf["pos1"]), cuda(csf["crd1"]),
+                      cuda(csf["pos2"]), cuda(csf["crd2"]), cuda(coo[3]), Bt, Ct)
+    return A1.cpu().numpy(), A2.cpu().numpy()
+
+
+def test_mttkrp_goldens(golden, orc):
+    for name, c in golden["mttkrp"].items():
+        I, J, Kd = int(c["I"]), int(c["J"]), int(c["K"])
+        coo = (c["coo_i"], c["coo_j"], c["coo_k"], c["coo_vals"])
+        csf = {f"{k}{l}": c[f"csf_{k}{l}"] for k in ("pos", "crd") for l in range(3)}
+        A1, A2 = _mttkrp_both(c, I, J, Kd, coo, csf, c["B"], c["C"])
+        _, absA = orc.mttkrp_coo3(I, *coo, c["B"], c["C"])
+        ok1, e1 = orc.within_condition(A1, c["A_coo"], absA, RTOL)
+        ok2, e2 = orc.within_condition(A2, c["A_csf"], absA, RTOL)
+        assert ok1 and ok2, (name, e1, e2)
+
+
+@pytest.mark.parametrize("I,J,Kd,nnz,R,seed", [
+    (2000, 1500, 1000, 400_000, 32, 1), (300, 200, 100, 50_000, 16, 2),
+    (50, 40, 30, 20_000, 64, 3), (5000, 100, 100, 3000, 32, 4), (20, 3000, 3000, 200_000, 32, 5)])
+def test_mttkrp_vs_oracle(orc, I, J, Kd, nnz, R, seed):
+    m = wl.mttkrp(I=I, J=J, K=Kd, nnz=nnz, R=R, seed=seed)
+    csf = wl.coo3_to_csf(m["i"], m["j"], m["k"], None)
+    ref, absA = orc.mttkrp_coo3(I, m["i"], m["j"], m["k"], m["vals"], m["B"], m["C"])
+    A1, A2 = _mttkrp_both(None, I, J, Kd, (m["i"], m["j"], m["k"], m["vals"]), csf, m["B"], m["C"])
+    for A in (A1, A2):
+        ok, err = orc.within_condition(A, ref, absA, RTOL)
+        assert ok, err
+    # determinism: the chunked reduction has a fixed order
+    A1b, A2b = _mttkrp_both(None, I, J, Kd, (m["i"], m["j"], m["k"], m["vals"]), csf, m["B"],
+                            m["C"])
+    assert np.array_equal(bits(A1), bits(A1b)) and np.array_equal(bits(A2), bits(A2b))
+
+
+@pytest.mark.slow
+def test_mttkrp_full_size(orc):
+    m = wl.mttkrp()
+    csf = wl.coo3_to_csf(m["i"], m["j"], m["k"], None)
+    ref, absA = orc.mttkrp_coo3(m["I"], m["i"], m["j"], m["k"], m["vals"], m["B"], m["C"])
+    A1, A2 = _mttkrp_both(None, m["I"], m["J"], m["K"], (m["i"], m["j"], m["k"], m["vals"]), csf,
+                          m["B"], m["C"])
+    for A in (A1, A2):
+        ok, err = orc.within_condition(A, ref, absA, RTOL)
+        assert ok, err
