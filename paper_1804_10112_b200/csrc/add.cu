@@ -218,7 +218,7 @@ extern "C" int sl_add_csr_count(int64_t nrows, const int32_t* a_pos, const int32
                                 void* stream) {
   if (nrows < 0 || b_nnz < 0) return SL_ERR_INVALID;
   if (nrows > INT32_MAX || b_nnz > INT32_MAX) return SL_ERR_RANGE;
-  if (!c_pos || !a_pos || (!b_pos && !b_rows)) return SL_ERR_INVALID;
+  if (!c_pos || !a_pos || (!b_pos && !b_rows && b_nnz > 0)) return SL_ERR_INVALID;
   if (!ws || ws_bytes < sl_add_csr_workspace_bytes(nrows, b_nnz)) return SL_ERR_WORKSPACE;
   cudaStream_t s = as_stream(stream);
   if (nrows == 0) {
@@ -242,7 +242,8 @@ extern "C" int sl_add_csr_fill(int64_t nrows, const int32_t* a_pos, const int32_
   if (nrows < 0 || b_nnz < 0) return SL_ERR_INVALID;
   if (nrows > INT32_MAX || b_nnz > INT32_MAX) return SL_ERR_RANGE;
   if (nrows == 0) return SL_OK;
-  if (!c_pos || !a_pos || (!b_pos && !b_rows) || !c_crd || !c_vals) return SL_ERR_INVALID;
+  if (!c_pos || !a_pos || (!b_pos && !b_rows && b_nnz > 0)) return SL_ERR_INVALID;
+  if ((!c_crd || !c_vals) && b_nnz > 0) return SL_ERR_INVALID;
   if (!b_pos && (!ws || ws_bytes < sl_add_csr_workspace_bytes(nrows, b_nnz)))
     return SL_ERR_WORKSPACE;
   cudaStream_t s = as_stream(stream);

@@ -34,31 +34,31 @@ SL_DEV uint64_t policy_evict_last() {
 }
 SL_DEV int32_t ld_stream(const int32_t* p) {
   int32_t v;
-  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.b32 %0, [%1], %2;"
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.b32 %0, [%1], %2;"
       : "=r"(v) : "l"(p), "l"(policy_evict_first()));
   return v;
 }
 SL_DEV double ld_stream(const double* p) {
   double v;
-  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;"
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;"
       : "=d"(v) : "l"(p), "l"(policy_evict_first()));
   return v;
 }
 SL_DEV int4 ld_stream(const int4* p) {
   int4 v;
-  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.b32 {%0,%1,%2,%3}, [%4], %5;"
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.b32 {%0,%1,%2,%3}, [%4], %5;"
       : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p), "l"(policy_evict_first()));
   return v;
 }
 SL_DEV int2 ld_stream(const int2* p) {
   int2 v;
-  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.b32 {%0,%1}, [%2], %3;"
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.b32 {%0,%1}, [%2], %3;"
       : "=r"(v.x), "=r"(v.y) : "l"(p), "l"(policy_evict_first()));
   return v;
 }
 SL_DEV double2 ld_stream(const double2* p) {
   double2 v;
-  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;"
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;"
       : "=d"(v.x), "=d"(v.y) : "l"(p), "l"(policy_evict_first()));
   return v;
 }
@@ -81,8 +81,23 @@ SL_DEV T warp_bcast(T v, int src) { return __shfl_sync(0xffffffffu, v, src); }
 
 }  // namespace sl
 
+namespace sl {
+constexpr int kDiaMaxParam = 32;
+struct DiaOffsets { int32_t v[kDiaMaxParam]; };   // DIA offsets passed by value (constant bank)
+}  // namespace sl
+
 // Host-side helpers shared by the .cu files.
 namespace sl_host {
+constexpr int kEllPipeMaxSlots = 32;   // ELL pipeline: slots per staged tile
+inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+int launch_ell_pipe(int64_t nrows, int32_t nslots, const int32_t* crd, const double* vals,
+                    const double* x, double* y, cudaStream_t s);
+int launch_dia_pipe(int64_t nrows, int64_t ncols, int32_t ndiag, const sl::DiaOffsets& offs,
+                    const double* vals, const double* x, double* y, cudaStream_t s);
+int launch_coo_pipe(int64_t nrows, int64_t nnz, const int32_t* rows, const int32_t* cols,
+                    const double* vals, const double* x, double* y, cudaStream_t s);
+int launch_csr_pipe(int64_t nrows, const int32_t* pos, const int32_t* crd, const double* vals,
+                    const double* x, double* y, cudaStream_t s);
 int sm_count();                              // cached per current device
 inline int ceil_div(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
 int launch_status();                         // SL_OK or SL_ERR_CUDA after a launch

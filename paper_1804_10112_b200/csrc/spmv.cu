@@ -11,9 +11,11 @@
 // the kernels are HBM-bound on the streamed index/value arrays.
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "common.cuh"
 #include "levels.cuh"
+#include "tma.cuh"
 
 namespace sl {
 
@@ -43,23 +45,25 @@ constexpr int kCooThreads = 256;
 constexpr int kCooVec = 4;                       // elements per vector load
 constexpr int kCooVecPerThread = 2;
 constexpr int kCooIpt = kCooVec * kCooVecPerThread;  // 8 items per thread
-constexpr int kCooTile = kCooThreads * kCooIpt;      // 2048 nonzeros per tile
+constexpr int kCooTile = kCooThreads * kCooIpt;      // 2048 nonzeros owned per tile
+constexpr int kCooHalo = kCooThreads;                // + 256 staged past the tile end
 
-__global__ void __launch_bounds__(kCooThreads)
+__global__ void __launch_bounds__(kCooThreads, 7)
 spmv_coo_kernel(int64_t nrows, int64_t nnz, const int32_t* __restrict__ rows,
                 const int32_t* __restrict__ cols, const double* __restrict__ vals,
                 const double* __restrict__ x, double* __restrict__ y, bool vec_ok) {
-  __shared__ __align__(16) int32_t s_row[kCooTile + 4];   // s_row[4 + q] = row of item q
-  __shared__ __align__(16) double s_prod[kCooTile];
-  __shared__ int32_t s_start[kCooTile];
-  __shared__ int32_t s_warp[kCooThreads / 32];
-  __shared__ int32_t s_nstart;
+  // s_row[4 + q] = row of staged item q; s_row[3] = row of the item before the tile
+  __shared__ __align__(16) int32_t s_row[kCooTile + kCooHalo + 4];
+  __shared__ __align__(16) double s_prod[kCooTile + kCooHalo];
+  __shared__ uint16_t s_start[kCooTile];          // row-start items (< kCooTile + kCooHalo)
+  __shared__ int32_t s_wcnt[kCooThreads / 32];
 
   const int tid = threadIdx.x;
   const int64_t e0 = (int64_t)blockIdx.x * kCooTile;
-  const int n_in = (int)min64(kCooTile, nnz - e0);
+  const int n_in = (int)min64(kCooTile, nnz - e0);               // owned row starts
+  const int n_st = (int)min64(kCooTile + kCooHalo, nnz - e0);    // staged items
 
-  // ---- stage: rows + products (coalesced, vectorised on full tiles)
+  // ---- stage rows + products: all loads of a thread are issued before use
   if (vec_ok && n_in == kCooTile) {
     int4 r4[kCooVecPerThread], c4[kCooVecPerThread];
     double2 va[kCooVecPerThread], vb[kCooVecPerThread];
@@ -71,92 +75,100 @@ spmv_coo_kernel(int64_t nrows, int64_t nnz, const int32_t* __restrict__ rows,
       va[k] = ld_stream(reinterpret_cast<const double2*>(vals + g));
       vb[k] = ld_stream(reinterpret_cast<const double2*>(vals + g + 2));
     }
+    const int qh = kCooTile + tid;                 // halo item of this thread
+    int32_t rh = 0, ch = 0;
+    double vh = 0.0;
+    if (qh < n_st) {
+      rh = ldg(rows + e0 + qh);
+      ch = ldg(cols + e0 + qh);
+      vh = ldg(vals + e0 + qh);
+    }
+    double xg[kCooVecPerThread][4];
 #pragma unroll
     for (int k = 0; k < kCooVecPerThread; ++k) {
-      const double x0 = ldg(x + c4[k].x), x1 = ldg(x + c4[k].y);
-      const double x2 = ldg(x + c4[k].z), x3 = ldg(x + c4[k].w);
+      xg[k][0] = ldg(x + c4[k].x);
+      xg[k][1] = ldg(x + c4[k].y);
+      xg[k][2] = ldg(x + c4[k].z);
+      xg[k][3] = ldg(x + c4[k].w);
+    }
+    const double xh = qh < n_st ? ldg(x + ch) : 0.0;
+#pragma unroll
+    for (int k = 0; k < kCooVecPerThread; ++k) {
       const int q = (k * kCooThreads + tid) * kCooVec;
       *reinterpret_cast<int4*>(s_row + 4 + q) = r4[k];
-      *reinterpret_cast<double2*>(s_prod + q) = make_double2(dmul(va[k].x, x0), dmul(va[k].y, x1));
-      *reinterpret_cast<double2*>(s_prod + q + 2) = make_double2(dmul(vb[k].x, x2), dmul(vb[k].y, x3));
+      *reinterpret_cast<double2*>(s_prod + q) =
+          make_double2(dmul(va[k].x, xg[k][0]), dmul(va[k].y, xg[k][1]));
+      *reinterpret_cast<double2*>(s_prod + q + 2) =
+          make_double2(dmul(vb[k].x, xg[k][2]), dmul(vb[k].y, xg[k][3]));
+    }
+    if (qh < n_st) {
+      s_row[4 + qh] = rh;
+      s_prod[qh] = dmul(vh, xh);
     }
   } else {
-#pragma unroll 4
-    for (int q = tid; q < n_in; q += kCooThreads) {
+    for (int q = tid; q < n_st; q += kCooThreads) {
       const int64_t g = e0 + q;
-      s_row[4 + q] = ld_stream(rows + g);
-      s_prod[q] = dmul(ld_stream(vals + g), ldg(x + ld_stream(cols + g)));
+      s_row[4 + q] = ldg(rows + g);
+      s_prod[q] = dmul(ldg(vals + g), ldg(x + ldg(cols + g)));
     }
   }
-  if (tid == 0) s_row[3] = e0 == 0 ? -1 : rows[e0 - 1];
+  if (tid == 0) s_row[3] = e0 == 0 ? -1 : ldg(rows + e0 - 1);
   __syncthreads();
 
-  // ---- compact row starts (q is a start iff row[q] != row[q-1])
-  int flags = 0, cnt = 0;
-  {
-    const int q0 = tid * kCooIpt;
-    int prev = s_row[3 + q0];
-#pragma unroll
-    for (int t = 0; t < kCooIpt; ++t) {
-      const int q = q0 + t;
-      if (q < n_in) {
-        const int r = s_row[4 + q];
-        if (r != prev) { flags |= 1 << t; ++cnt; }
-        prev = r;
-      }
-    }
-  }
+  // ---- compact the row starts of the owned range with warp ballots
   const int lane = tid & 31, warp = tid >> 5;
-  int incl = cnt;
+  constexpr int kPerWarp = kCooTile / (kCooThreads / 32);   // 256 items per warp
+  unsigned masks[kPerWarp / 32];
+  int cnt = 0;
 #pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int v = __shfl_up_sync(0xffffffffu, incl, o);
-    if (lane >= o) incl += v;
+  for (int b = 0; b < kPerWarp / 32; ++b) {
+    const int q = warp * kPerWarp + b * 32 + lane;
+    const bool f = q < n_in && s_row[4 + q] != s_row[3 + q];
+    masks[b] = __ballot_sync(0xffffffffu, f);
+    cnt += __popc(masks[b]);
   }
-  if (lane == 31) s_warp[warp] = incl;
+  if (lane == 0) s_wcnt[warp] = cnt;
   __syncthreads();
-  if (warp == 0) {
-    int v = lane < kCooThreads / 32 ? s_warp[lane] : 0;
-    int sc = v;
+  int base = 0, nstart = 0;
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int u = __shfl_up_sync(0xffffffffu, sc, o);
-      if (lane >= o) sc += u;
-    }
-    if (lane < kCooThreads / 32) s_warp[lane] = sc - v;   // exclusive warp offsets
-    if (lane == kCooThreads / 32 - 1) s_nstart = sc;
+  for (int w = 0; w < kCooThreads / 32; ++w) {
+    const int c = s_wcnt[w];
+    base += w < warp ? c : 0;
+    nstart += c;
   }
-  __syncthreads();
-  {
-    int o = s_warp[warp] + incl - cnt;
 #pragma unroll
-    for (int t = 0; t < kCooIpt; ++t)
-      if (flags & (1 << t)) s_start[o++] = tid * kCooIpt + t;
+  for (int b = 0; b < kPerWarp / 32; ++b) {
+    const unsigned m = masks[b];
+    if (m & (1u << lane))
+      s_start[base + __popc(m & ((1u << lane) - 1u))] = (uint16_t)(warp * kPerWarp + b * 32 + lane);
+    base += __popc(m);
   }
   __syncthreads();
 
-  // ---- owners: sum each row in storage order, zero the gap before it
-  const int nstart = s_nstart;
-  const bool last_tile = e0 + n_in == nnz;
-  for (int s = tid; s < nstart; s += kCooThreads) {
-    const int q = s_start[s];
-    const int r = s_row[4 + q];
-    const int rp = s_row[3 + q];
-    const int qe = s + 1 < nstart ? s_start[s + 1] : n_in;
+  // ---- thread per row, lockstep: rows summed in storage order from +0.0
+  for (int si = tid; si < nstart; si += kCooThreads) {
+    const int q = s_start[si];
+    const int32_t r = s_row[4 + q];
+    const int32_t rp = s_row[3 + q];
     double acc = 0.0;
-    for (int u = q; u < qe; ++u) acc = dadd(acc, s_prod[u]);
-    bool reached_end = last_tile && s + 1 == nstart;
-    if (s + 1 == nstart && !last_tile) {
-      // the row may continue into later tiles: finish it from global memory
-      int64_t g = e0 + n_in;
-      for (; g < nnz && ldg(rows + g) == r; ++g)
-        acc = dadd(acc, dmul(ldg(vals + g), ldg(x + ldg(cols + g))));
-      reached_end = g == nnz;
+    int64_t g;
+    if (si + 1 < nstart) {
+      const int qe = s_start[si + 1];
+      for (int u = q; u < qe; ++u) acc = dadd(acc, s_prod[u]);
+      g = e0 + qe;
+    } else {
+      // last row starting in this tile: runs into the halo (and beyond)
+      int u = q;
+      for (; u < n_st && s_row[4 + u] == r; ++u) acc = dadd(acc, s_prod[u]);
+      g = e0 + u;
+      if (u == n_st)
+        for (; g < nnz && ldg(rows + g) == r; ++g)
+          acc = dadd(acc, dmul(ldg(vals + g), ldg(x + ldg(cols + g))));
     }
     y[r] = acc;
-    for (int rr = rp + 1; rr < r; ++rr) y[rr] = 0.0;
-    if (reached_end)  // the matrix's last stored row: zero the empty rows after it
-      for (int64_t rr = (int64_t)r + 1; rr < nrows; ++rr) y[rr] = 0.0;
+    for (int32_t q2 = rp + 1; q2 < r; ++q2) y[q2] = 0.0;          // empty rows before r
+    if (g == nnz)                                                   // the matrix's last row
+      for (int64_t q2 = (int64_t)r + 1; q2 < nrows; ++q2) y[q2] = 0.0;
   }
 }
 
@@ -168,7 +180,8 @@ spmv_coo_kernel(int64_t nrows, int64_t nnz, const int32_t* __restrict__ rows,
 
 constexpr int kCsrThreads = 256;
 constexpr int kCsrRows = kCsrThreads;
-constexpr int kCsrChunk = 2048;
+constexpr int kCsrIpt = 8;
+constexpr int kCsrChunk = kCsrThreads * kCsrIpt;   // 2048 products per staging round
 
 template <bool kHashX>
 struct XOperand;
@@ -191,8 +204,105 @@ struct XOperand<true> {             // hashed x: probe (levels.py:270-280), miss
   }
 };
 
+// Stage products of elements [cs, cs + n) into s_prod with every load of a
+// thread issued before its first use (crd/vals stream, then the x gathers).
+template <int kThreads, int kIpt>
+SL_DEV void stage_products(const int32_t* __restrict__ crd, const double* __restrict__ vals,
+                           int64_t cs, int n, XOperand<false> xop, double* s_prod) {
+  const int tid = threadIdx.x;
+  int32_t c[kIpt];
+  double v[kIpt], xv[kIpt];
+  if (n == kThreads * kIpt) {   // full chunk: unpredicated batches
+#pragma unroll
+    for (int k = 0; k < kIpt; ++k) c[k] = ld_stream(crd + cs + tid + k * kThreads);
+#pragma unroll
+    for (int k = 0; k < kIpt; ++k) v[k] = ld_stream(vals + cs + tid + k * kThreads);
+#pragma unroll
+    for (int k = 0; k < kIpt; ++k) xv[k] = ldg(xop.x + c[k]);
+#pragma unroll
+    for (int k = 0; k < kIpt; ++k) s_prod[tid + k * kThreads] = dmul(v[k], xv[k]);
+    return;
+  }
+#pragma unroll
+  for (int k = 0; k < kIpt; ++k) {
+    const int q = tid + k * kThreads;
+    c[k] = q < n ? ld_stream(crd + cs + q) : 0;
+    v[k] = q < n ? ld_stream(vals + cs + q) : 0.0;
+  }
+#pragma unroll
+  for (int k = 0; k < kIpt; ++k) xv[k] = tid + k * kThreads < n ? ldg(xop.x + c[k]) : 0.0;
+#pragma unroll
+  for (int k = 0; k < kIpt; ++k) {
+    const int q = tid + k * kThreads;
+    if (q < n) s_prod[q] = dmul(v[k], xv[k]);
+  }
+}
+
+// Hashed x: hybrid probing.  Each lane first probes its own element for
+// kHashSolo steps (the whole answer for short probe sequences); elements still
+// unresolved are then finished one at a time by the whole warp, 32
+// consecutive probe steps per round (one coalesced 128-byte load), taking the
+// first match-or-empty in probe order — the sequential answer.
+constexpr int kHashSolo = 4;
+
+template <int kThreads, int kIpt>
+SL_DEV void stage_products(const int32_t* __restrict__ crd, const double* __restrict__ vals,
+                           int64_t cs, int n, XOperand<true> xop, double* s_prod) {
+  const int tid = threadIdx.x, lane = tid & 31;
+  const HashedLevel& lv = xop.lv;
+  const int64_t w = lv.w;
+#pragma unroll 1
+  for (int k = 0; k < kIpt; ++k) {
+    const int q = tid + k * kThreads;
+    const bool valid = q < n;
+    const int32_t c = valid ? ld_stream(crd + cs + q) : 0;
+    const double a = valid ? ld_stream(vals + cs + q) : 0.0;
+    int64_t slot = -1;
+    bool done = !valid;
+    const int64_t home = c % w;
+    int64_t step = 0;
+    for (; step < kHashSolo && step < w && !done; ++step) {
+      int64_t sidx = home + step;
+      if (sidx >= w) sidx -= w;
+      const int32_t v = ldg(lv.crd + sidx);
+      if (v == c) { slot = sidx; done = true; }
+      else if (v == kEmpty) done = true;
+    }
+    if (step >= w) done = true;   // whole (tiny) segment scanned
+    unsigned pending = __ballot_sync(0xffffffffu, !done);
+    while (pending) {
+      const int src = __ffs(pending) - 1;
+      pending &= pending - 1;
+      const int32_t cc = __shfl_sync(0xffffffffu, c, src);
+      const int64_t hh = cc % w;
+      int64_t found = -1;
+      bool stop = false;
+      for (int64_t s0 = kHashSolo; s0 < w && !stop; s0 += 32) {
+        const int64_t st = s0 + lane;
+        int32_t v = 0;
+        int64_t p = -1;
+        if (st < w) {
+          p = hh + st;
+          if (p >= w) p -= w;
+          v = ldg(lv.crd + p);
+        }
+        const unsigned hit = __ballot_sync(0xffffffffu, st < w && (v == cc || v == kEmpty));
+        if (hit) {
+          const int f = __ffs(hit) - 1;
+          const int64_t pf = __shfl_sync(0xffffffffu, p, f);
+          const int32_t vf = __shfl_sync(0xffffffffu, v, f);
+          found = vf == cc ? pf : -1;
+          stop = true;
+        }
+      }
+      if (lane == src) slot = found;
+    }
+    if (valid) s_prod[q] = slot >= 0 ? dmul(a, ldg(xop.xv + slot)) : 0.0;
+  }
+}
+
 template <bool kHashX>
-__global__ void __launch_bounds__(kCsrThreads)
+__global__ void __launch_bounds__(kCsrThreads, 8)
 spmv_csr_rowblock_kernel(int64_t nrows, const int32_t* __restrict__ pos,
                          const int32_t* __restrict__ crd, const double* __restrict__ vals,
                          XOperand<kHashX> xop, double* __restrict__ y) {
@@ -209,9 +319,7 @@ spmv_csr_rowblock_kernel(int64_t nrows, const int32_t* __restrict__ pos,
   double acc = 0.0;
   for (int32_t cs = eb; cs < ee; cs += kCsrChunk) {
     const int n_in = min(kCsrChunk, ee - cs);
-#pragma unroll 8
-    for (int q = tid; q < n_in; q += kCsrThreads)
-      s_prod[q] = xop.term(ld_stream(vals + cs + q), ld_stream(crd + cs + q));
+    stage_products<kCsrThreads, kCsrIpt>(crd, vals, cs, n_in, xop, s_prod);
     __syncthreads();
     const int lo = max(rb, cs) - cs, hi = min(re, cs + n_in) - cs;
     for (int u = lo; u < hi; ++u) acc = dadd(acc, s_prod[u]);
@@ -288,9 +396,7 @@ spmv_csr_merge_kernel(int64_t nrows, const int32_t* __restrict__ pos,
   const int64_t eb = ldg(pos + rb), ee = ldg(pos + re);
   for (int64_t cs = eb; cs < ee; cs += kMpItems) {
     const int n_in = (int)min64(kMpItems, ee - cs);
-#pragma unroll 8
-    for (int q = tid; q < n_in; q += kMpThreads)
-      s_prod[q] = xop.term(ld_stream(vals + cs + q), ld_stream(crd + cs + q));
+    stage_products<kMpThreads, kMpItems / kMpThreads>(crd, vals, cs, n_in, xop, s_prod);
     __syncthreads();
     // rows are few per tile (<= kMpItems) — thread-per-row over the chunk
     for (int64_t r = rb + tid; r < re; r += kMpThreads) {
@@ -309,36 +415,33 @@ spmv_csr_merge_kernel(int64_t nrows, const int32_t* __restrict__ pos,
 // contiguous, so every load is coalesced; slots are added in slot order
 // (= the row's column order, padding last: formats.py:322-335, 443-455).
 
-template <int kRowsPerThread>
-__global__ void __launch_bounds__(256)
+constexpr int kEllBatch = 9;   // slots loaded per batch (27 = 3 batches for the stencil)
+
+__global__ void __launch_bounds__(256, 8)
 spmv_ell_kernel(int64_t nrows, int32_t nslots, const int32_t* __restrict__ crd,
                 const double* __restrict__ vals, const double* __restrict__ x,
                 double* __restrict__ y) {
-  const int64_t i0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * kRowsPerThread;
-  if (i0 >= nrows) return;
-  if (kRowsPerThread == 2 && i0 + 1 < nrows) {
-    double a0 = 0.0, a1 = 0.0;
-#pragma unroll 9
-    for (int32_t s = 0; s < nslots; ++s) {
-      const int64_t p = (int64_t)s * nrows + i0;
-      const int2 c = ld_stream(reinterpret_cast<const int2*>(crd + p));  // 8B aligned: nrows, i0 even
-      const double2 v = ld_stream(reinterpret_cast<const double2*>(vals + p));
-      a0 = dadd(a0, dmul(v.x, ldg(x + c.x)));
-      a1 = dadd(a1, dmul(v.y, ldg(x + c.y)));
-    }
-    y[i0] = a0;
-    y[i0 + 1] = a1;
-  } else {
-    for (int64_t i = i0; i < i0 + kRowsPerThread && i < nrows; ++i) {
-      double a = 0.0;
-#pragma unroll 9
-      for (int32_t s = 0; s < nslots; ++s) {
-        const int64_t p = (int64_t)s * nrows + i;
-        a = dadd(a, dmul(ld_stream(vals + p), ldg(x + ld_stream(crd + p))));
-      }
-      y[i] = a;
-    }
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nrows) return;
+  double a = 0.0;
+  int32_t s0 = 0;
+  for (; s0 + kEllBatch <= nslots; s0 += kEllBatch) {   // full batches: no predicates
+    int32_t c[kEllBatch];
+    double v[kEllBatch], xv[kEllBatch];
+#pragma unroll
+    for (int b = 0; b < kEllBatch; ++b) c[b] = ld_stream(crd + (int64_t)(s0 + b) * nrows + i);
+#pragma unroll
+    for (int b = 0; b < kEllBatch; ++b) v[b] = ld_stream(vals + (int64_t)(s0 + b) * nrows + i);
+#pragma unroll
+    for (int b = 0; b < kEllBatch; ++b) xv[b] = ldg(x + c[b]);
+#pragma unroll
+    for (int b = 0; b < kEllBatch; ++b) a = dadd(a, dmul(v[b], xv[b]));
   }
+  for (; s0 < nslots; ++s0) {
+    const int64_t p = (int64_t)s0 * nrows + i;
+    a = dadd(a, dmul(ld_stream(vals + p), ldg(x + ld_stream(crd + p))));
+  }
+  y[i] = a;
 }
 
 // ---------------------------------------------------------------------------
@@ -347,29 +450,42 @@ spmv_ell_kernel(int64_t nrows, int32_t nslots, const int32_t* __restrict__ crd,
 // range level's bounds (levels.py:220-222): out-of-range slots are never read.
 // Offsets travel as a kernel parameter (constant bank) when ndiag <= 32.
 
-constexpr int kDiaMaxParam = 32;
-struct DiaOffsets { int32_t v[kDiaMaxParam]; };
-
-__global__ void __launch_bounds__(256)
+// Offsets in the constant bank (kernel parameter); all of a row's in-range
+// value and x loads are issued before the in-order add chain.
+template <int kMaxD>
+__global__ void __launch_bounds__(256, 8)
 spmv_dia_kernel(int64_t nrows, int64_t ncols, int32_t ndiag, DiaOffsets offs,
-                const int32_t* __restrict__ doffs, const double* __restrict__ vals,
-                const double* __restrict__ x, double* __restrict__ y) {
+                const double* __restrict__ vals, const double* __restrict__ x,
+                double* __restrict__ y) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nrows) return;
+  double v[kMaxD], xv[kMaxD];
+  bool in[kMaxD];
+#pragma unroll
+  for (int d = 0; d < kMaxD; ++d) {
+    const int64_t j = i + offs.v[d];
+    in[d] = d < ndiag && j >= 0 && j < ncols;
+    v[d] = in[d] ? ld_stream(vals + (int64_t)d * nrows + i) : 0.0;
+    xv[d] = in[d] ? ldg(x + j) : 0.0;
+  }
+  double a = 0.0;
+#pragma unroll
+  for (int d = 0; d < kMaxD; ++d)
+    if (in[d]) a = dadd(a, dmul(v[d], xv[d]));
+  y[i] = a;
+}
+
+// Device-resident offsets (any number of diagonals).
+__global__ void __launch_bounds__(256)
+spmv_dia_dev_kernel(int64_t nrows, int64_t ncols, int32_t ndiag, const int32_t* __restrict__ doffs,
+                    const double* __restrict__ vals, const double* __restrict__ x,
+                    double* __restrict__ y) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= nrows) return;
   double a = 0.0;
-  if (doffs == nullptr) {
-#pragma unroll
-    for (int d = 0; d < kDiaMaxParam; ++d) {
-      if (d < ndiag) {
-        const int64_t j = i + offs.v[d];
-        if (j >= 0 && j < ncols) a = dadd(a, dmul(ld_stream(vals + (int64_t)d * nrows + i), ldg(x + j)));
-      }
-    }
-  } else {
-    for (int d = 0; d < ndiag; ++d) {
-      const int64_t j = i + ldg(doffs + d);
-      if (j >= 0 && j < ncols) a = dadd(a, dmul(ld_stream(vals + (int64_t)d * nrows + i), ldg(x + j)));
-    }
+  for (int d = 0; d < ndiag; ++d) {
+    const int64_t j = i + ldg(doffs + d);
+    if (j >= 0 && j < ncols) a = dadd(a, dmul(ld_stream(vals + (int64_t)d * nrows + i), ldg(x + j)));
   }
   y[i] = a;
 }
@@ -382,8 +498,16 @@ spmv_dia_kernel(int64_t nrows, int64_t ncols, int32_t ndiag, DiaOffsets offs,
 using namespace sl;
 using sl_host::as_stream;
 using sl_host::ceil_div;
+using sl_host::aligned16;
 
-static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+// SL_SPMV_PATH=pipe selects the persistent TMA pipelines (pipe.cu) instead of
+// the LDG kernels (A/B knob; the LDG kernels measured faster on every BASELINE
+// config), =ldg forces LDG.
+static int spmv_path() {
+  const char* e = getenv("SL_SPMV_PATH");
+  return !e ? 0 : (e[0] == 'l' ? 1 : (e[0] == 'p' ? 2 : 0));
+}
+
 
 extern "C" int sl_spmv_coo_f64(int64_t nrows, int64_t ncols, int64_t nnz, const int32_t* rows,
                                const int32_t* cols, const double* vals, const double* x,
@@ -398,6 +522,7 @@ extern "C" int sl_spmv_coo_f64(int64_t nrows, int64_t ncols, int64_t nnz, const 
     return sl_host::launch_status();
   }
   const bool vec_ok = aligned16(rows) && aligned16(cols) && aligned16(vals);
+  if (vec_ok && spmv_path() == 2) return sl_host::launch_coo_pipe(nrows, nnz, rows, cols, vals, x, y, s);
   spmv_coo_kernel<<<ceil_div(nnz, kCooTile), kCooThreads, 0, s>>>(nrows, nnz, rows, cols, vals,
                                                                    x, y, vec_ok);
   return sl_host::launch_status();
@@ -413,7 +538,10 @@ template <bool kHashX>
 static int launch_csr(int64_t nrows, const int32_t* pos, const int32_t* crd, const double* vals,
                       XOperand<kHashX> xop, double* y, int32_t variant, void* ws,
                       size_t ws_bytes, cudaStream_t s) {
-  if (variant == 0) {
+  if (variant == 0 && !kHashX && aligned16(crd) && aligned16(vals) && spmv_path() == 2) {
+    const double* xd = reinterpret_cast<const XOperand<false>&>(xop).x;
+    return sl_host::launch_csr_pipe(nrows, pos, crd, vals, xd, y, s);
+  } else if (variant == 0) {
     spmv_csr_rowblock_kernel<kHashX><<<ceil_div(nrows, kCsrRows), kCsrThreads, 0, s>>>(
         nrows, pos, crd, vals, xop, y);
   } else if (variant == 1) {
@@ -470,13 +598,12 @@ extern "C" int sl_spmv_ell_f64(int64_t nrows, int64_t ncols, int32_t nslots, con
   if (nrows == 0) return SL_OK;
   if (!y || (nslots > 0 && (!crd || !vals || !x))) return SL_ERR_INVALID;
   cudaStream_t s = as_stream(stream);
-  const bool pair = (nrows % 2 == 0) && aligned16(vals) &&
-                    (reinterpret_cast<uintptr_t>(crd) & 7u) == 0;
-  if (pair)
-    spmv_ell_kernel<2><<<ceil_div(ceil_div(nrows, 2), 256), 256, 0, s>>>(nrows, nslots, crd, vals,
-                                                                          x, y);
-  else
-    spmv_ell_kernel<1><<<ceil_div(nrows, 256), 256, 0, s>>>(nrows, nslots, crd, vals, x, y);
+  if (nslots > 0 && nslots <= sl_host::kEllPipeMaxSlots && nrows % 4 == 0 && aligned16(crd) && aligned16(vals) &&
+      spmv_path() == 2) {
+    return sl_host::launch_ell_pipe(nrows, nslots, crd, vals, x, y, s);
+  } else {
+    spmv_ell_kernel<<<ceil_div(nrows, 256), 256, 0, s>>>(nrows, nslots, crd, vals, x, y);
+  }
   return sl_host::launch_status();
 }
 
@@ -497,6 +624,12 @@ extern "C" int sl_spmv_dia_f64(int64_t nrows, int64_t ncols, int32_t ndiag, cons
   } else {
     doffs = offsets;
   }
-  spmv_dia_kernel<<<ceil_div(nrows, 256), 256, 0, s>>>(nrows, ncols, ndiag, p, doffs, vals, x, y);
+  const int grid = ceil_div(nrows, 256);
+  if (!doffs && aligned16(vals) && aligned16(x) && ndiag > 0 && spmv_path() == 2) {
+    return sl_host::launch_dia_pipe(nrows, ncols, ndiag, p, vals, x, y, s);
+  } else if (doffs) spmv_dia_dev_kernel<<<grid, 256, 0, s>>>(nrows, ncols, ndiag, doffs, vals, x, y);
+  else if (ndiag <= 8) spmv_dia_kernel<8><<<grid, 256, 0, s>>>(nrows, ncols, ndiag, p, vals, x, y);
+  else if (ndiag <= 16) spmv_dia_kernel<16><<<grid, 256, 0, s>>>(nrows, ncols, ndiag, p, vals, x, y);
+  else spmv_dia_kernel<32><<<grid, 256, 0, s>>>(nrows, ncols, ndiag, p, vals, x, y);
   return sl_host::launch_status();
 }

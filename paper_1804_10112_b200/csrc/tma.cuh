@@ -1,0 +1,122 @@
+// tma.cuh — 1D bulk async copies (cp.async.bulk, the TMA's linear mode) and
+// mbarrier helpers for sm_100a.  The streaming kernels move their index and
+// value arrays global -> shared with these: one elected thread issues a few
+// large copies, the copy engine keeps them in flight (no registers held), and
+// the consumer threads wait on an mbarrier's transaction count.
+#pragma once
+#include <stdint.h>
+
+#include "common.cuh"
+
+namespace sl {
+
+SL_DEV uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+SL_DEV void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+               : "memory");
+}
+
+// Make mbarrier.init visible to the async (TMA) proxy.
+SL_DEV void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+
+// Order this thread's generic-proxy shared-memory accesses before later
+// async-proxy (bulk copy) writes into the same buffer.
+SL_DEV void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+SL_DEV void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+SL_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+SL_DEV void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// Named barrier over `nthreads` threads (a consumer warp-group), id >= 1.
+SL_DEV void group_sync(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+// Bulk copy `bytes` (multiple of 16, both addresses 16-byte aligned) from
+// global to shared; completion is signalled on `bar` as transaction bytes.
+// Tagged L2 evict-first: streamed operands are read once.
+SL_DEV void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+      "[%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy_evict_first())
+      : "memory");
+}
+
+// Same, default L2 policy (for reused operands such as x windows).
+SL_DEV void bulk_g2s_keep(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes "
+      "[%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// Copy the element range [lo, hi) of a global array into smem so that element
+// e lands at smem_base[e - lo0], where lo0 = lo rounded down to 16 bytes.
+// Bulk copies cover the 16-byte-aligned interior; the (< 16-byte) head and
+// tail are loaded by `lane` threads with plain loads (the caller syncs).
+// Returns the bulk transaction bytes issued (0 if the range is tiny).
+// `elected` must be true for exactly one thread.
+template <typename T>
+struct BulkRange {
+  int64_t lo0;        // first element staged at smem index 0
+  uint32_t tx_bytes;  // bytes the mbarrier must expect
+  int64_t blo, bhi;   // bulk-copied element range
+};
+
+template <typename T>
+SL_DEV BulkRange<T> plan_range(const T* g, int64_t lo, int64_t hi) {
+  constexpr int64_t per16 = 16 / sizeof(T);
+  const uintptr_t base = reinterpret_cast<uintptr_t>(g);
+  // element index whose address is 16-byte aligned at or after lo / before hi
+  const int64_t mis = (int64_t)((base / sizeof(T)) % per16);   // base misalignment in elements
+  auto align_up = [&](int64_t e) { return ((e + mis + per16 - 1) / per16) * per16 - mis; };
+  auto align_dn = [&](int64_t e) { return ((e + mis) / per16) * per16 - mis; };
+  BulkRange<T> r;
+  r.lo0 = align_dn(lo);
+  r.blo = align_up(lo);
+  r.bhi = align_dn(hi);
+  if (r.bhi < r.blo) r.bhi = r.blo;
+  r.tx_bytes = (uint32_t)((r.bhi - r.blo) * sizeof(T));
+  return r;
+}
+
+template <typename T>
+SL_DEV void issue_range(const T* g, const BulkRange<T>& r, T* s, uint64_t* bar) {
+  if (r.tx_bytes) bulk_g2s(s + (r.blo - r.lo0), g + r.blo, r.tx_bytes, bar);
+}
+
+// plain loads of the unaligned head [lo, blo) and tail [bhi, hi)
+template <typename T>
+SL_DEV void edge_loads(const T* g, const BulkRange<T>& r, int64_t lo, int64_t hi, T* s, int tid,
+                       int nthreads) {
+  const int64_t nh = r.blo - lo < hi - lo ? r.blo - lo : hi - lo;
+  for (int64_t e = tid; e < nh; e += nthreads) s[lo + e - r.lo0] = g[lo + e];
+  const int64_t t0 = r.bhi > lo ? r.bhi : lo;
+  for (int64_t e = t0 + tid; e < hi; e += nthreads)
+    if (e >= r.blo) s[e - r.lo0] = g[e];
+}
+
+}  // namespace sl

@@ -311,3 +311,39 @@ def test_mttkrp_full_size(orc):
     for A in (A1, A2):
         ok, err = orc.within_condition(A, ref, absA, RTOL)
         assert ok, err
+
+
+# ---------------------------------------------------------------------------
+# the persistent TMA pipelines (SL_SPMV_PATH=pipe) must agree bit for bit
+
+@pytest.fixture
+def pipe_path(monkeypatch):
+    monkeypatch.setenv("SL_SPMV_PATH", "pipe")
+    yield
+
+
+def test_pipe_path_goldens(golden, pipe_path):
+    test_spmv_goldens_all_formats(golden)
+
+
+@pytest.mark.parametrize("n,nnz,lam,seed", [(3000, 30000, 10.0, 1), (5000, 200, 0.05, 2),
+                                            (777, 60000, 77.0, 5)])
+def test_pipe_path_vs_oracle(orc, pipe_path, n, nnz, lam, seed):
+    test_spmv_coo_csr_vs_oracle(orc, n, nnz, lam, seed)
+
+
+def test_pipe_path_full_size(orc, pipe_path):
+    test_spmv_dia_vs_oracle_odd_shapes(orc)
+    s = wl.stencil27()
+    ref, _ = orc.spmv_csr(s["nrows"], s["pos"], s["crd"], s["vals"], s["x"])
+    x = cuda(s["x"])
+    y = K.spmv_csr(s["nrows"], s["ncols"], cuda(s["pos"]), cuda(s["crd"]), cuda(s["vals"]), x)
+    assert np.array_equal(bits(y), bits(ref))
+    e = wl.csr_to_ell(s["pos"], s["crd"], s["vals"], s["nrows"])
+    y = K.spmv_ell(s["nrows"], s["ncols"], e["nslots"], cuda(e["crd"]), cuda(e["vals"]), x)
+    assert np.array_equal(bits(y), bits(ref))
+    d = wl.coo_spmv()
+    ref, _ = orc.spmv_coo(d["nrows"], d["rows"], d["cols"], d["vals"], d["x"])
+    y = K.spmv_coo(d["nrows"], d["ncols"], cuda(d["rows"]), cuda(d["cols"]), cuda(d["vals"]),
+                   cuda(d["x"]))
+    assert np.array_equal(bits(y), bits(ref))
