@@ -199,6 +199,16 @@ int sl_add_csr_fill(int64_t nrows,
                     const int32_t* c_pos, int32_t* c_crd, double* c_vals,
                     void* ws, size_t ws_bytes, void* stream);
 
+/* Fused single pass: count, decoupled look-back scan and fill in one launch
+ * over the operands (each read once).  c_crd / c_vals must hold nnz_a + nnz_b
+ * entries (the union's upper bound); c_pos is final on completion. */
+int sl_add_csr_f64(int64_t nrows,
+                   const int32_t* a_pos, const int32_t* a_crd, const double* a_vals,
+                   int64_t b_nnz, const int32_t* b_pos, const int32_t* b_rows,
+                   const int32_t* b_cols, const double* b_vals,
+                   int32_t* c_pos, int32_t* c_crd, double* c_vals,
+                   void* ws, size_t ws_bytes, void* stream);
+
 /* ---- MTTKRP  A(i,r) = X(i,j,k) * B(j,r) * C(k,r) ----------------------------
  * B [J x R], C [K x R], A [I x R] row-major dense (dense-2 layout).
  * COO-3 (formats.py:138-140): i, j, k = L0/L1/L2 crd, lexicographically sorted.

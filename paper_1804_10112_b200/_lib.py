@@ -64,6 +64,8 @@ SIGNATURES = {
     "sl_add_csr_count": ([_i64, _p, _p, _i64, _p, _p, _p, _p, _p, _sz, _p], ctypes.c_int),
     "sl_add_csr_fill": ([_i64, _p, _p, _p, _i64, _p, _p, _p, _p, _p, _p, _p, _p, _sz, _p],
                         ctypes.c_int),
+    "sl_add_csr_f64": ([_i64, _p, _p, _p, _i64, _p, _p, _p, _p, _p, _p, _p, _p, _sz, _p],
+                       ctypes.c_int),
     "sl_mttkrp_workspace_bytes": ([_i64, _i32], _sz),
     "sl_mttkrp_coo3_f64": ([_i64, _i64, _i64, _i32, _i64, _p, _p, _p, _p, _p, _p, _p, _p, _sz,
                             _p], ctypes.c_int),

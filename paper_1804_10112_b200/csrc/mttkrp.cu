@@ -22,6 +22,7 @@
 // coordinates stream past.
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include <type_traits>
 
@@ -178,6 +179,254 @@ mttkrp_coo3_kernel(int64_t I, int R, int64_t nnz, int64_t nchunks, const int32_t
   if (e1 == nnz) zero_rows(A, (int64_t)cur + 1, I, lane, R);
 }
 
+// ---- K7 (vectorised): COO-3, R in {16, 32, 64} --------------------------------------
+// kLpn = R/4 lanes per nonzero, each lane owning 4 consecutive rank columns
+// read with one 256-bit load from B and one from C; 32/kLpn nonzeros per warp
+// step.  Each lane group ("sub") keeps a partial sum of the current output row
+// over the nonzeros it handled; when the row ends the subs' partials are
+// combined with a fixed xor-shuffle tree (deterministic).  ~3x fewer
+// instructions per nonzero than the lane-per-column kernel (ncu: that one is
+// issue-bound at ~50 warp-instructions per nonzero).
+SL_DEV double4 ld4(const double* p) {
+  double4 v;
+  asm("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w)
+      : "l"(p));
+  return v;
+}
+
+SL_DEV double4 shfl_xor4(double4 a, int m) {
+  return make_double4(__shfl_xor_sync(0xffffffffu, a.x, m), __shfl_xor_sync(0xffffffffu, a.y, m),
+                      __shfl_xor_sync(0xffffffffu, a.z, m), __shfl_xor_sync(0xffffffffu, a.w, m));
+}
+
+SL_DEV double4 add4(double4 a, double4 b) {
+  return make_double4(dadd(a.x, b.x), dadd(a.y, b.y), dadd(a.z, b.z), dadd(a.w, b.w));
+}
+
+template <int kLpn>
+SL_DEV double4 combine_subs(double4 a) {
+  // fixed tree over the 32/kLpn subs: xor kLpn, 2kLpn, ...
+#pragma unroll
+  for (int m = kLpn; m < 32; m <<= 1) a = add4(a, shfl_xor4(a, m));
+  return a;
+}
+
+SL_DEV void store4(double* dst, double4 v) {
+  *reinterpret_cast<double4*>(dst) = v;
+}
+
+// destination of a finished row: head carry, tail carry or A itself
+SL_DEV double* row_dst(int32_t row, bool is_first, bool is_last, bool head_partial, bool tail_cont,
+                       int64_t c, CarryWs cw, double* A, int R, int lane) {
+  if (is_first && head_partial) {
+    if (lane == 0) cw.head_row[c] = row;
+    return cw.head + c * R;
+  }
+  if (is_last && tail_cont) {
+    if (lane == 0) cw.tail_row[c] = row;
+    return cw.tail + c * R;
+  }
+  return A + (int64_t)row * R;
+}
+
+// Per-batch sources of (i, j, k, x) for the 32 nonzeros [base, base + 32),
+// lane l holding nonzero base + l.  The next batch's loads are issued before
+// the current batch is consumed (double-buffered in registers).
+struct CooSrc {
+  const int32_t* ii;
+  const int32_t* jj;
+  const int32_t* kk;
+  const double* vals;
+  int64_t e1;
+  int32_t ni, nj, nk;
+  double nv;
+  SL_DEV void prefetch(int64_t base, int lane) {
+    if (base + lane < e1) {
+      ni = ld_stream(ii + base + lane);
+      nj = ld_stream(jj + base + lane);
+      nk = ld_stream(kk + base + lane);
+      nv = ld_stream(vals + base + lane);
+    }
+  }
+  SL_DEV void start(int64_t e0, int lane) { prefetch(e0, lane); }
+  SL_DEV void next(int64_t base, int lane, int32_t& li, int32_t& lj, int32_t& lk, double& lv) {
+    li = ni; lj = nj; lk = nk; lv = nv;
+    prefetch(base + 32, lane);
+  }
+};
+
+// CSF: the batch's fibers and slices come from 32-wide windows of pos2/crd1
+// and pos1/crd0; each lane finds its nonzero's fiber (slice) by a 5-step
+// shuffle binary search over the window of fiber (slice) ends.
+SL_DEV int window_count_le(int32_t w, int32_t key) {
+  // number of window entries <= key (entries sorted across lanes; <= 31)
+  int d = 0;
+#pragma unroll
+  for (int step = 16; step >= 1; step >>= 1) {
+    const int32_t v = __shfl_sync(0xffffffffu, w, d + step - 1);
+    if (v <= key) d += step;
+  }
+  return d;
+}
+
+struct CsfSrc {
+  const int32_t* crd0;
+  const int32_t* pos1;
+  const int32_t* crd1;
+  const int32_t* pos2;
+  const int32_t* crd2;
+  const double* vals;
+  int64_t nslices, nfibers, e1;
+  int64_t f, s;        // fiber / slice of the batch's first nonzero (warp-uniform)
+  int32_t nk;
+  double nv;
+  SL_DEV void prefetch(int64_t base, int lane) {
+    if (base + lane < e1) {
+      nk = ld_stream(crd2 + base + lane);
+      nv = ld_stream(vals + base + lane);
+    }
+  }
+  SL_DEV void start(int64_t e0, int lane) { prefetch(e0, lane); }
+  SL_DEV void next(int64_t base, int lane, int32_t& li, int32_t& lj, int32_t& lk, double& lv) {
+    const int32_t fe = f + 1 + lane <= nfibers ? ldg(pos2 + f + 1 + lane) : INT32_MAX;
+    const int32_t jw = f + lane < nfibers ? ldg(crd1 + f + lane) : 0;
+    const int32_t se = s + 1 + lane <= nslices ? ldg(pos1 + s + 1 + lane) : INT32_MAX;
+    const int32_t iw = s + lane < nslices ? ldg(crd0 + s + lane) : 0;
+    const int32_t e = (int32_t)(base + lane);
+    const int df = window_count_le(fe, e);
+    lj = __shfl_sync(0xffffffffu, jw, df);
+    const int32_t fib = (int32_t)(f + df);
+    const int ds = window_count_le(se, fib);
+    li = __shfl_sync(0xffffffffu, iw, ds);
+    lk = nk;
+    lv = nv;
+    // advance to the next batch's first nonzero
+    f += __popc(__ballot_sync(0xffffffffu, fe <= (int32_t)(base + 32)));
+    s += __popc(__ballot_sync(0xffffffffu, se <= (int32_t)f));
+    prefetch(base + 32, lane);
+  }
+};
+
+template <int kR, class Src>
+SL_DEV void mttkrp_vec_body(int64_t I, int64_t e0, int64_t e1, int32_t row_first, int32_t prev_row,
+                            bool head_partial, bool tail_cont, int64_t c,
+                            const double* __restrict__ B, const double* __restrict__ C,
+                            double* __restrict__ A, CarryWs cw, Src& src) {
+  constexpr int kLpn = kR / 4, kNps = 32 / kLpn;   // lanes per nonzero, nonzeros per step
+  constexpr int kSteps = 4;                        // steps whose loads are issued together
+  const int lane = threadIdx.x & 31, sub = lane / kLpn, q = lane % kLpn;
+  if (lane == 0) {
+    cw.first_row[c] = row_first;
+    cw.head_row[c] = -1;
+    cw.tail_row[c] = -1;
+  }
+  if (!head_partial) zero_rows(A, prev_row + 1, row_first, lane, kR);
+  double4 acc = make_double4(0.0, 0.0, 0.0, 0.0);
+  int32_t cur = row_first;
+  bool first = true;
+  auto flush = [&](bool is_last) {
+    const double4 tot = combine_subs<kLpn>(acc);
+    double* dst = row_dst(cur, first, is_last, head_partial, tail_cont, c, cw, A, kR, lane);
+    if (sub == 0) store4(dst + 4 * q, tot);
+  };
+  src.start(e0, lane);
+  for (int64_t base = e0; base < e1; base += 32) {
+    const int n = (int)min64(32, e1 - base);
+    int32_t li, lj, lk;
+    double lv;
+    src.next(base, lane, li, lj, lk, lv);
+    for (int u0 = 0; u0 < n; u0 += kSteps * kNps) {
+      double4 t[kSteps];
+#pragma unroll
+      for (int st = 0; st < kSteps; ++st) {
+        const int u = u0 + st * kNps + sub;
+        const int us = u < n ? u : n - 1;
+        const int32_t j = __shfl_sync(0xffffffffu, lj, us);
+        const int32_t k = __shfl_sync(0xffffffffu, lk, us);
+        const double v = __shfl_sync(0xffffffffu, lv, us);
+        const double4 b = ld4(B + (int64_t)j * kR + 4 * q);
+        const double4 cc = ld4(C + (int64_t)k * kR + 4 * q);
+        t[st] = make_double4(dmul(dmul(v, b.x), cc.x), dmul(dmul(v, b.y), cc.y),
+                             dmul(dmul(v, b.z), cc.z), dmul(dmul(v, b.w), cc.w));
+      }
+      // fast path: rows are sorted, so if the round's last nonzero is still in
+      // the current row, all of them are; every sub adds its terms in the
+      // same per-sub order as the general path below
+      const int ulast = min(u0 + kSteps * kNps, n) - 1;
+      if (__shfl_sync(0xffffffffu, li, ulast) == cur) {
+#pragma unroll
+        for (int st = 0; st < kSteps; ++st)
+          if (u0 + st * kNps + sub < n) acc = add4(acc, t[st]);
+        continue;
+      }
+#pragma unroll
+      for (int st = 0; st < kSteps; ++st) {
+#pragma unroll
+        for (int s2 = 0; s2 < kNps; ++s2) {
+          const int u = u0 + st * kNps + s2;      // warp-uniform element index
+          if (u >= n) break;
+          const int32_t r = __shfl_sync(0xffffffffu, li, u);
+          if (r != cur) {
+            flush(false);
+            zero_rows(A, (int64_t)cur + 1, r, lane, kR);
+            acc = make_double4(0.0, 0.0, 0.0, 0.0);
+            cur = r;
+            first = false;
+          }
+          if (sub == s2) acc = add4(acc, t[st]);
+        }
+      }
+    }
+  }
+  flush(true);
+  (void)I;
+}
+
+template <int kR>
+__global__ void __launch_bounds__(kMtThreads, 2)
+mttkrp_coo3_vec_kernel(int64_t I, int64_t nnz, int64_t nchunks, const int32_t* __restrict__ ii,
+                       const int32_t* __restrict__ jj, const int32_t* __restrict__ kk,
+                       const double* __restrict__ vals, const double* __restrict__ B,
+                       const double* __restrict__ C, double* __restrict__ A, CarryWs cw) {
+  const int64_t c = (int64_t)blockIdx.x * kMtWarps + (threadIdx.x >> 5);
+  if (c >= nchunks) return;
+  const int64_t e0 = c * kMtChunk;
+  const int64_t e1 = min64(e0 + kMtChunk, nnz);
+  const int32_t row_first = ldg(ii + e0);
+  const int32_t prev_row = e0 > 0 ? ldg(ii + e0 - 1) : -1;
+  const bool tail_cont = e1 < nnz && ldg(ii + e1) == ldg(ii + e1 - 1);
+  CooSrc src{ii, jj, kk, vals, e1, 0, 0, 0, 0.0};
+  mttkrp_vec_body<kR>(I, e0, e1, row_first, prev_row, prev_row == row_first, tail_cont, c, B, C, A,
+                      cw, src);
+  if (e1 == nnz) zero_rows(A, (int64_t)ldg(ii + nnz - 1) + 1, I, threadIdx.x & 31, kR);
+}
+
+template <int kR>
+__global__ void __launch_bounds__(kMtThreads, 2)
+mttkrp_csf_vec_kernel(int64_t I, int64_t nslices, int64_t nfibers, int64_t nnz, int64_t nchunks,
+                      const int32_t* __restrict__ crd0, const int32_t* __restrict__ pos1,
+                      const int32_t* __restrict__ crd1, const int32_t* __restrict__ pos2,
+                      const int32_t* __restrict__ crd2, const double* __restrict__ vals,
+                      const double* __restrict__ B, const double* __restrict__ C,
+                      double* __restrict__ A, CarryWs cw) {
+  const int64_t c = (int64_t)blockIdx.x * kMtWarps + (threadIdx.x >> 5);
+  if (c >= nchunks) return;
+  const int64_t e0 = c * kMtChunk;
+  const int64_t e1 = min64(e0 + kMtChunk, nnz);
+  const int64_t f = ldg(cw.fstart + c), s = ldg(cw.sstart + c);
+  const int32_t row_first = ldg(crd0 + s);
+  const bool head_partial = ldg(pos2 + ldg(pos1 + s)) < e0;
+  const int32_t prev_row = head_partial ? row_first : (s > 0 ? ldg(crd0 + s - 1) : -1);
+  bool tail_cont = false;
+  if (e1 < nnz) {
+    const int64_t sn = ldg(cw.sstart + c + 1);        // slice of nonzero e1
+    tail_cont = ldg(pos2 + ldg(pos1 + sn)) < e1;     // it started before e1
+  }
+  CsfSrc src{crd0, pos1, crd1, pos2, crd2, vals, nslices, nfibers, e1, f, s, 0, 0.0};
+  mttkrp_vec_body<kR>(I, e0, e1, row_first, prev_row, head_partial, tail_cont, c, B, C, A, cw, src);
+  if (e1 == nnz) zero_rows(A, (int64_t)ldg(crd0 + nslices - 1) + 1, I, threadIdx.x & 31, kR);
+}
+
 // ---- K8: CSF ----------------------------------------------------------------------------
 // Pre-pass: fiber f marks the chunks whose first nonzero it holds; slice s
 // marks the chunks whose first nonzero lies in its nonzero range.
@@ -302,60 +551,52 @@ mttkrp_csf_kernel(int64_t I, int R, int64_t nslices, int64_t nfibers, int64_t nn
 }
 
 // ---- fix-up: rows cut by chunk boundaries ---------------------------------------------
-// Block per chunk c that holds a tail carry: the row continues through chunks
-// c+1 .. ce (their first rows equal it and they hold head carries).  ce is
-// found by a warp-wide 32-ary search over the monotone first_row array; the
-// 8 warps sum strided subsets of the heads, combined in a fixed order.
+// Warp per chunk c (grid-stride) that holds a tail carry: the row continues
+// through chunks c+1 .. ce (their first rows equal it; they hold head carries).
+// ce is found by a galloping search over the monotone first_row array (most
+// segments end at c+1); the heads are summed 4-way interleaved and combined in
+// a fixed order, so the result is deterministic.
 template <int RPL>
 __global__ void __launch_bounds__(kMtThreads)
 mttkrp_fixup_kernel(int R, int64_t nchunks, CarryWs cw, double* __restrict__ A) {
-  const int64_t c = blockIdx.x;
-  const int32_t row = cw.tail_row[c];
-  if (row < 0) return;
-  __shared__ int64_t s_end;
-  __shared__ double s_part[kMtWarps][32 * RPL];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (warp == 0) {
-    // last chunk ce >= c with first_row[ce'] == row for all c < ce' <= ce
-    int64_t lo = c, hi = nchunks - 1;   // answer in [lo, hi]
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = (int64_t)gridDim.x * kMtWarps;
+  for (int64_t c = (int64_t)blockIdx.x * kMtWarps + (threadIdx.x >> 5); c < nchunks; c += nwarps) {
+    const int32_t row = cw.tail_row[c];
+    if (row < 0) continue;
+    // gallop: find ce = last chunk index with first_row == row (>= c + 1)
+    int64_t lo = c + 1, step = 1;                 // first_row[lo] == row
+    while (true) {
+      const int64_t probe = lo + step;
+      if (probe >= nchunks || ldg(cw.first_row + probe) != row) break;
+      lo = probe;
+      step <<= 1;
+    }
+    int64_t hi = min64(lo + step, nchunks) - 1;   // answer in [lo, hi]
     while (lo < hi) {
       const int64_t span = hi - lo;
-      const int64_t step = (span + 31) / 32;
-      const int64_t probe = lo + (int64_t)(lane + 1) * step;
-      const bool ok = probe <= hi && ldg(cw.first_row + probe) == row;
-      const unsigned m = __ballot_sync(0xffffffffu, ok);
-      // ok is monotone: true for a prefix of lanes
-      const int nok = __popc(m);
-      const int64_t new_lo = lo + (int64_t)nok * step;
-      const int64_t new_hi = min64(hi, lo + (int64_t)(nok + 1) * step - 1);
-      lo = new_lo;
-      hi = new_hi;
+      const int64_t st = (span + 31) / 32;
+      const int64_t p = lo + (int64_t)(lane + 1) * st;
+      const bool ok = p <= hi && ldg(cw.first_row + p) == row;
+      const int nok = __popc(__ballot_sync(0xffffffffu, ok));
+      const int64_t nlo = lo + (int64_t)nok * st;
+      hi = min64(hi, lo + (int64_t)(nok + 1) * st - 1);
+      lo = nlo;
     }
-    if (lane == 0) s_end = lo;
-  }
-  __syncthreads();
-  const int64_t ce = s_end;
-  RowAcc<RPL> part;
-  part.zero();
-  for (int64_t q = c + 1 + warp; q <= ce; q += kMtWarps) {
+    const int64_t ce = lo;
 #pragma unroll
     for (int p = 0; p < RPL; ++p) {
       const int r = lane + 32 * p;
-      if (r < R) part.v[p] = dadd(part.v[p], cw.head[q * R + r]);
-    }
-  }
+      if (r >= R) continue;
+      double part[4] = {0.0, 0.0, 0.0, 0.0};
+      int64_t q = c + 1;
+      for (; q + 3 <= ce; q += 4) {
 #pragma unroll
-  for (int p = 0; p < RPL; ++p) s_part[warp][lane + 32 * p] = part.v[p];
-  __syncthreads();
-  if (warp == 0) {
-#pragma unroll
-    for (int p = 0; p < RPL; ++p) {
-      const int r = lane + 32 * p;
-      if (r < R) {
-        double tot = cw.tail[c * R + r];
-        for (int w = 0; w < kMtWarps; ++w) tot = dadd(tot, s_part[w][r]);
-        A[(int64_t)row * R + r] = tot;
+        for (int u = 0; u < 4; ++u) part[u] = dadd(part[u], cw.head[(q + u) * R + r]);
       }
+      for (int u = 0; q <= ce; ++q, ++u) part[u] = dadd(part[u], cw.head[q * R + r]);
+      const double tot = dadd(cw.tail[c * R + r], dadd(dadd(part[0], part[1]), dadd(part[2], part[3])));
+      A[(int64_t)row * R + r] = tot;
     }
   }
 }
@@ -373,6 +614,12 @@ using sl_host::as_stream;
 using sl_host::ceil_div;
 
 static int64_t mt_nchunks(int64_t nnz) { return (nnz + kMtChunk - 1) / kMtChunk; }
+
+static int fixup_grid(int64_t nch) {
+  const int64_t want = (nch + kMtWarps - 1) / kMtWarps;
+  const int64_t cap = 8LL * sl_host::sm_count();
+  return (int)(want < cap ? want : cap);
+}
 
 extern "C" size_t sl_mttkrp_workspace_bytes(int64_t nnz, int32_t R) {
   return carry_bytes(mt_nchunks(nnz) + 1, R);
@@ -411,10 +658,26 @@ extern "C" int sl_mttkrp_coo3_f64(int64_t I, int64_t J, int64_t K, int32_t R, in
   const int64_t nch = mt_nchunks(nnz);
   CarryWs cw = carve(ws, nch + 1, R);
   const int grid = ceil_div(nch, kMtWarps);
+  const bool vec_ok = (reinterpret_cast<uintptr_t>(B) & 31u) == 0 &&
+                      (reinterpret_cast<uintptr_t>(C) & 31u) == 0 &&
+                      (reinterpret_cast<uintptr_t>(A) & 31u) == 0 && !getenv("SL_MTTKRP_SCALAR");
+  if (vec_ok && (R == 16 || R == 32 || R == 64)) {
+    if (R == 16)
+      mttkrp_coo3_vec_kernel<16><<<grid, kMtThreads, 0, s>>>(I, nnz, nch, i, j, k, vals, B, C, A, cw);
+    else if (R == 32)
+      mttkrp_coo3_vec_kernel<32><<<grid, kMtThreads, 0, s>>>(I, nnz, nch, i, j, k, vals, B, C, A, cw);
+    else
+      mttkrp_coo3_vec_kernel<64><<<grid, kMtThreads, 0, s>>>(I, nnz, nch, i, j, k, vals, B, C, A, cw);
+    return dispatch_rpl(R, [&](auto rpl) {
+      constexpr int RPL = decltype(rpl)::value;
+      mttkrp_fixup_kernel<RPL><<<fixup_grid(nch), kMtThreads, 0, s>>>(R, nch, cw, A);
+      return sl_host::launch_status();
+    });
+  }
   return dispatch_rpl(R, [&](auto rpl) {
     constexpr int RPL = decltype(rpl)::value;
     mttkrp_coo3_kernel<RPL><<<grid, kMtThreads, 0, s>>>(I, R, nnz, nch, i, j, k, vals, B, C, A, cw);
-    mttkrp_fixup_kernel<RPL><<<(int)nch, kMtThreads, 0, s>>>(R, nch, cw, A);
+    mttkrp_fixup_kernel<RPL><<<fixup_grid(nch), kMtThreads, 0, s>>>(R, nch, cw, A);
     return sl_host::launch_status();
   });
 }
@@ -442,11 +705,30 @@ extern "C" int sl_mttkrp_csf_f64(int64_t I, int64_t J, int64_t K, int32_t R, int
   const int64_t nt = nslices > nfibers ? nslices : nfibers;
   csf_chunk_starts_kernel<<<ceil_div(nt, 256), 256, 0, s>>>(nslices, nfibers, pos1, pos2, cw);
   const int grid = ceil_div(nch, kMtWarps);
+  const bool vec_ok = (reinterpret_cast<uintptr_t>(B) & 31u) == 0 &&
+                      (reinterpret_cast<uintptr_t>(C) & 31u) == 0 &&
+                      (reinterpret_cast<uintptr_t>(A) & 31u) == 0 && !getenv("SL_MTTKRP_SCALAR");
+  if (vec_ok && (R == 16 || R == 32 || R == 64)) {
+    if (R == 16)
+      mttkrp_csf_vec_kernel<16><<<grid, kMtThreads, 0, s>>>(I, nslices, nfibers, nnz, nch, crd0,
+                                                            pos1, crd1, pos2, crd2, vals, B, C, A, cw);
+    else if (R == 32)
+      mttkrp_csf_vec_kernel<32><<<grid, kMtThreads, 0, s>>>(I, nslices, nfibers, nnz, nch, crd0,
+                                                            pos1, crd1, pos2, crd2, vals, B, C, A, cw);
+    else
+      mttkrp_csf_vec_kernel<64><<<grid, kMtThreads, 0, s>>>(I, nslices, nfibers, nnz, nch, crd0,
+                                                            pos1, crd1, pos2, crd2, vals, B, C, A, cw);
+    return dispatch_rpl(R, [&](auto rpl) {
+      constexpr int RPL = decltype(rpl)::value;
+      mttkrp_fixup_kernel<RPL><<<fixup_grid(nch), kMtThreads, 0, s>>>(R, nch, cw, A);
+      return sl_host::launch_status();
+    });
+  }
   return dispatch_rpl(R, [&](auto rpl) {
     constexpr int RPL = decltype(rpl)::value;
     mttkrp_csf_kernel<RPL><<<grid, kMtThreads, 0, s>>>(I, R, nslices, nfibers, nnz, nch, crd0,
                                                        pos1, crd1, pos2, crd2, vals, B, C, A, cw);
-    mttkrp_fixup_kernel<RPL><<<(int)nch, kMtThreads, 0, s>>>(R, nch, cw, A);
+    mttkrp_fixup_kernel<RPL><<<fixup_grid(nch), kMtThreads, 0, s>>>(R, nch, cw, A);
     return sl_host::launch_status();
   });
 }

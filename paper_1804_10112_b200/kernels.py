@@ -133,10 +133,13 @@ def hashed_insert(coords, w, nseg=1, parent=None, crd=None):
 
 # ---- C = A + B -----------------------------------------------------------------
 
-def add_csr(nrows, a_pos, a_crd, a_vals, b_cols, b_vals, b_rows=None, b_pos=None, sync=True):
+def add_csr(nrows, a_pos, a_crd, a_vals, b_cols, b_vals, b_rows=None, b_pos=None, sync=True,
+            two_pass=False):
     """CSR + (COO | CSR) -> CSR.  Returns (c_pos, c_crd, c_vals); with
     sync=False the crd/vals buffers are upper-bound sized (nnz_a + nnz_b) and
-    nnz_c = c_pos[nrows] is left on the device."""
+    nnz_c = c_pos[nrows] is left on the device.  two_pass=True runs the
+    count -> scan -> fill pair (sl_add_csr_count / sl_add_csr_fill), the
+    default the fused single pass (sl_add_csr_f64); both are bit-identical."""
     a_pos, a_crd, a_vals = _t(a_pos, I32, "a_pos"), _t(a_crd, I32, "a_crd"), _t(a_vals, F64, "a_vals")
     b_cols, b_vals = _t(b_cols, I32, "b_cols"), _t(b_vals, F64, "b_vals")
     b_rows = None if b_rows is None else _t(b_rows, I32, "b_rows")
@@ -150,11 +153,16 @@ def add_csr(nrows, a_pos, a_crd, a_vals, b_cols, b_vals, b_rows=None, b_pos=None
     need = L().sl_add_csr_workspace_bytes(nrows, bnnz)
     ws = _ws(need, a_vals)
     wsn = 0 if ws is None else ws.numel()
-    _lib.check(L().sl_add_csr_count(nrows, P(a_pos), P(a_crd), bnnz, P(b_pos), P(b_rows),
-                                    P(b_cols), P(c_pos), P(ws), wsn, S()), "add_count")
-    _lib.check(L().sl_add_csr_fill(nrows, P(a_pos), P(a_crd), P(a_vals), bnnz, P(b_pos),
-                                   P(b_rows), P(b_cols), P(b_vals), P(c_pos), P(c_crd), P(c_vals),
-                                   P(ws), wsn, S()), "add_fill")
+    if two_pass:
+        _lib.check(L().sl_add_csr_count(nrows, P(a_pos), P(a_crd), bnnz, P(b_pos), P(b_rows),
+                                        P(b_cols), P(c_pos), P(ws), wsn, S()), "add_count")
+        _lib.check(L().sl_add_csr_fill(nrows, P(a_pos), P(a_crd), P(a_vals), bnnz, P(b_pos),
+                                       P(b_rows), P(b_cols), P(b_vals), P(c_pos), P(c_crd),
+                                       P(c_vals), P(ws), wsn, S()), "add_fill")
+    else:
+        _lib.check(L().sl_add_csr_f64(nrows, P(a_pos), P(a_crd), P(a_vals), bnnz, P(b_pos),
+                                      P(b_rows), P(b_cols), P(b_vals), P(c_pos), P(c_crd),
+                                      P(c_vals), P(ws), wsn, S()), "add_csr")
     if sync:
         n = int(c_pos[nrows].item())
         return c_pos, c_crd[:n], c_vals[:n]

@@ -221,26 +221,30 @@ def test_spmv_hashx_full_h1(orc):
 # ---------------------------------------------------------------------------
 # A + B
 
-def test_add_goldens(golden):
+@pytest.mark.parametrize("two_pass", [False, True])
+def test_add_goldens(golden, two_pass):
     for name, c in golden["add"].items():
         kw = {"b_pos": cuda(c["b_pos"], np.int32)} if "b_pos" in c else \
              {"b_rows": cuda(c["b_rows"], np.int32)}
         pos, crd, vals = K.add_csr(int(c["nrows"]), cuda(c["a_pos"], np.int32),
                                    cuda(c["a_crd"], np.int32), cuda(c["a_vals"], np.float64),
                                    cuda(c["b_cols"], np.int32), cuda(c["b_vals"], np.float64),
-                                   **kw)
+                                   two_pass=two_pass, **kw)
         assert np.array_equal(pos.cpu().numpy(), c["c_pos"]), name
         assert np.array_equal(crd.cpu().numpy(), c["c_crd"]), name
         assert np.array_equal(bits(vals), bits(c["c_vals"])), name
 
 
-@pytest.mark.parametrize("n,nnz,seed", [(2000, 9000, 1), (100_000, 500_000, 2), (70_000, 100, 3)])
-def test_add_vs_oracle(orc, n, nnz, seed):
+@pytest.mark.parametrize("two_pass", [False, True])
+@pytest.mark.parametrize("n,nnz,seed", [(2000, 9000, 1), (100_000, 500_000, 2), (70_000, 100, 3),
+                                        (3000, 300_000, 4)])
+def test_add_vs_oracle(orc, n, nnz, seed, two_pass):
     d = wl.add_ab(n=n, nnz_a=nnz, nnz_b=nnz, seed=seed)
     rp, rc, rv = orc.add_csr(n, d["a_pos"], d["a_crd"], d["a_vals"], d["b_cols"], d["b_vals"],
                              b_rows=d["b_rows"])
     pos, crd, vals = K.add_csr(n, cuda(d["a_pos"]), cuda(d["a_crd"]), cuda(d["a_vals"]),
-                               cuda(d["b_cols"]), cuda(d["b_vals"]), b_rows=cuda(d["b_rows"]))
+                               cuda(d["b_cols"]), cuda(d["b_vals"]), b_rows=cuda(d["b_rows"]),
+                               two_pass=two_pass)
     assert np.array_equal(pos.cpu().numpy(), rp)
     assert np.array_equal(crd.cpu().numpy(), rc)
     assert np.array_equal(bits(vals), bits(rv))
@@ -286,7 +290,8 @@ def test_mttkrp_goldens(golden, orc):
 
 @pytest.mark.parametrize("I,J,Kd,nnz,R,seed", [
     (2000, 1500, 1000, 400_000, 32, 1), (300, 200, 100, 50_000, 16, 2),
-    (50, 40, 30, 20_000, 64, 3), (5000, 100, 100, 3000, 32, 4), (20, 3000, 3000, 200_000, 32, 5)])
+    (50, 40, 30, 20_000, 64, 3), (5000, 100, 100, 3000, 32, 4), (20, 3000, 3000, 200_000, 32, 5),
+    (400, 300, 200, 60_000, 8, 6), (100, 90, 80, 30_000, 100, 7)])
 def test_mttkrp_vs_oracle(orc, I, J, Kd, nnz, R, seed):
     m = wl.mttkrp(I=I, J=J, K=Kd, nnz=nnz, R=R, seed=seed)
     csf = wl.coo3_to_csf(m["i"], m["j"], m["k"], None)
@@ -347,3 +352,24 @@ def test_pipe_path_full_size(orc, pipe_path):
     y = K.spmv_coo(d["nrows"], d["ncols"], cuda(d["rows"]), cuda(d["cols"]), cuda(d["vals"]),
                    cuda(d["x"]))
     assert np.array_equal(bits(y), bits(ref))
+
+
+def test_mttkrp_scalar_path_matches(orc, monkeypatch):
+    """SL_MTTKRP_SCALAR selects the lane-per-column kernels; same tolerance."""
+    monkeypatch.setenv("SL_MTTKRP_SCALAR", "1")
+    m = wl.mttkrp(I=700, J=500, K=400, nnz=150_000, R=32, seed=11)
+    csf = wl.coo3_to_csf(m["i"], m["j"], m["k"], None)
+    ref, absA = orc.mttkrp_coo3(700, m["i"], m["j"], m["k"], m["vals"], m["B"], m["C"])
+    A1, A2 = _mttkrp_both(None, 700, 500, 400, (m["i"], m["j"], m["k"], m["vals"]), csf, m["B"],
+                          m["C"])
+    for A in (A1, A2):
+        ok, err = orc.within_condition(A, ref, absA, RTOL)
+        assert ok, err
+
+
+@pytest.mark.parametrize("two_pass", [False, True])
+def test_add_element_parallel_path(golden, orc, monkeypatch, two_pass):
+    """SL_ADD_PATH=elem: element-parallel slots must equal the row merge bit for bit."""
+    monkeypatch.setenv("SL_ADD_PATH", "elem")
+    test_add_goldens(golden, two_pass)
+    test_add_vs_oracle(orc, 100_000, 500_000, 2, two_pass)
