@@ -149,6 +149,7 @@ int sl_spmv_coo_f64(int64_t nrows, int64_t ncols, int64_t nnz,
  * variant 1 = vector-per-row (a warp per row; lanes load the row's nonzeros
  *             coalesced, lane 0 sums them in order from registers via shuffles);
  * variant 2 = merge-path (nnz+rows balanced tiles; row-owner sums in order);
+ * variant 3 = warp row-block (each warp owns 32 rows, warp-private staging);
  * All variants are bit-identical.  ws may be NULL for variants 0 and 1. */
 size_t sl_spmv_csr_workspace_bytes(int64_t nrows, int64_t nnz, int32_t variant);
 int sl_spmv_csr_f64(int64_t nrows, int64_t ncols, int64_t nnz, const int32_t* pos,
@@ -170,6 +171,14 @@ int sl_spmv_ell_f64(int64_t nrows, int64_t ncols, int32_t nslots,
 int sl_spmv_dia_f64(int64_t nrows, int64_t ncols, int32_t ndiag,
                     const int32_t* offsets, int32_t offsets_on_host,
                     const double* vals, const double* x, double* y, void* stream);
+
+/* DIA row block [row0, row0 + nrows) of a larger matrix (a multi-GPU shard):
+ * vals [ndiag * nrows] hold the block's slots, y the block's rows, x the whole
+ * vector; row i of the block takes diagonal d iff 0 <= row0 + i + offset[d] <
+ * ncols.  sl_spmv_dia_f64 is row0 = 0. */
+int sl_spmv_dia_rows_f64(int64_t nrows, int64_t row0, int64_t ncols, int32_t ndiag,
+                         const int32_t* offsets, int32_t offsets_on_host,
+                         const double* vals, const double* x, double* y, void* stream);
 
 /* CSR x hash-vector: y(i) = A(i,j) * x(j) with x a hashed level of width w
  * (crd[w] with -1 empties, vals[w] by slot).  x is located per nonzero

@@ -59,6 +59,7 @@ SIGNATURES = {
     "sl_spmv_csr_f64": ([_i64, _i64, _i64, _p, _p, _p, _p, _p, _i32, _p, _sz, _p], ctypes.c_int),
     "sl_spmv_ell_f64": ([_i64, _i64, _i32, _p, _p, _p, _p, _p], ctypes.c_int),
     "sl_spmv_dia_f64": ([_i64, _i64, _i32, _p, _i32, _p, _p, _p, _p], ctypes.c_int),
+    "sl_spmv_dia_rows_f64": ([_i64, _i64, _i64, _i32, _p, _i32, _p, _p, _p, _p], ctypes.c_int),
     "sl_spmv_csr_hashx_f64": ([_i64, _p, _p, _p, _i64, _p, _p, _p, _p], ctypes.c_int),
     "sl_add_csr_workspace_bytes": ([_i64, _i64], _sz),
     "sl_add_csr_count": ([_i64, _p, _p, _i64, _p, _p, _p, _p, _p, _sz, _p], ctypes.c_int),

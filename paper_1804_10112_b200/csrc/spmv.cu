@@ -244,6 +244,7 @@ SL_DEV void stage_products(const int32_t* __restrict__ crd, const double* __rest
 // consecutive probe steps per round (one coalesced 128-byte load), taking the
 // first match-or-empty in probe order — the sequential answer.
 constexpr int kHashSolo = 4;
+constexpr int kHashPer = 8;     // probe steps per lane per cooperative round
 
 template <int kThreads, int kIpt>
 SL_DEV void stage_products(const int32_t* __restrict__ crd, const double* __restrict__ vals,
@@ -276,23 +277,42 @@ SL_DEV void stage_products(const int32_t* __restrict__ crd, const double* __rest
       const int32_t cc = __shfl_sync(0xffffffffu, c, src);
       const int64_t hh = cc % w;
       int64_t found = -1;
-      bool stop = false;
-      for (int64_t s0 = kHashSolo; s0 < w && !stop; s0 += 32) {
-        const int64_t st = s0 + lane;
-        int32_t v = 0;
-        int64_t p = -1;
-        if (st < w) {
-          p = hh + st;
-          if (p >= w) p -= w;
-          v = ldg(lv.crd + p);
+      // each round the warp probes kHashPer * 32 consecutive steps: lane l
+      // checks steps s0 + kHashPer*l + {0..kHashPer-1} (independent loads);
+      // the lowest step that matches or is empty ends the probe
+      for (int64_t s0 = kHashSolo; s0 < w; s0 += kHashPer * 32) {
+        int hit_k = kHashPer;          // first of this lane's steps that stops the probe
+        int64_t hit_p = -1;
+        bool hit_match = false;
+        int32_t v[kHashPer];
+        int64_t pp[kHashPer];
+#pragma unroll
+        for (int k = 0; k < kHashPer; ++k) {
+          const int64_t st = s0 + (int64_t)kHashPer * lane + k;
+          pp[k] = -1;
+          v[k] = 0;
+          if (st < w) {
+            int64_t p = hh + st;
+            if (p >= w) p -= w;
+            pp[k] = p;
+            v[k] = ldg(lv.crd + p);
+          }
         }
-        const unsigned hit = __ballot_sync(0xffffffffu, st < w && (v == cc || v == kEmpty));
+#pragma unroll
+        for (int k = kHashPer - 1; k >= 0; --k) {
+          if (pp[k] >= 0 && (v[k] == cc || v[k] == kEmpty)) {
+            hit_k = k;
+            hit_p = pp[k];
+            hit_match = v[k] == cc;
+          }
+        }
+        const unsigned hit = __ballot_sync(0xffffffffu, hit_k < kHashPer);
         if (hit) {
           const int f = __ffs(hit) - 1;
-          const int64_t pf = __shfl_sync(0xffffffffu, p, f);
-          const int32_t vf = __shfl_sync(0xffffffffu, v, f);
-          found = vf == cc ? pf : -1;
-          stop = true;
+          const int64_t pf = __shfl_sync(0xffffffffu, hit_p, f);
+          const bool mf = __shfl_sync(0xffffffffu, hit_match ? 1 : 0, f) != 0;
+          found = mf ? pf : -1;
+          break;
         }
       }
       if (lane == src) slot = found;
@@ -326,6 +346,57 @@ spmv_csr_rowblock_kernel(int64_t nrows, const int32_t* __restrict__ pos,
     __syncthreads();
   }
   if (mine) y[r0 + tid] = acc;
+}
+
+// K2d: CSR warp row-block.  Each warp owns 32 consecutive rows; their
+// nonzeros (contiguous) are staged in warp-private shared memory in rounds of
+// 256 products (8 coalesced loads per lane), and lane r adds the round's
+// products of its row in order.  Warps synchronise with __syncwarp only, so
+// they progress independently (the block-level barriers of K2a stall on the
+// slowest warp).
+constexpr int kCsrWarpIpt = 8;
+constexpr int kCsrWarpChunk = 32 * kCsrWarpIpt;   // 256 products per round
+
+__global__ void __launch_bounds__(256, 8)
+spmv_csr_warp_kernel(int64_t nrows, const int32_t* __restrict__ pos, const int32_t* __restrict__ crd,
+                     const double* __restrict__ vals, const double* __restrict__ x,
+                     double* __restrict__ y) {
+  __shared__ __align__(16) double s_prod[8][kCsrWarpChunk];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t w0 = ((int64_t)blockIdx.x * 8 + warp) * 32;
+  if (w0 >= nrows) return;
+  const int nr = (int)min64(32, nrows - w0);
+  const int32_t rb = lane < nr ? ldg(pos + w0 + lane) : 0;
+  const int32_t re = lane < nr ? ldg(pos + w0 + lane + 1) : 0;
+  const int32_t eb = __shfl_sync(0xffffffffu, rb, 0), ee = __shfl_sync(0xffffffffu, re, nr - 1);
+  double* sp = s_prod[warp];
+  double acc = 0.0;
+  for (int32_t cs = eb; cs < ee; cs += kCsrWarpChunk) {
+    const int n = min(kCsrWarpChunk, ee - cs);
+    int32_t c[kCsrWarpIpt];
+    double v[kCsrWarpIpt], xv[kCsrWarpIpt];
+    if (n == kCsrWarpChunk) {
+#pragma unroll
+      for (int k = 0; k < kCsrWarpIpt; ++k) c[k] = ld_stream(crd + cs + lane + 32 * k);
+#pragma unroll
+      for (int k = 0; k < kCsrWarpIpt; ++k) v[k] = ld_stream(vals + cs + lane + 32 * k);
+#pragma unroll
+      for (int k = 0; k < kCsrWarpIpt; ++k) xv[k] = ldg(x + c[k]);
+#pragma unroll
+      for (int k = 0; k < kCsrWarpIpt; ++k) sp[lane + 32 * k] = dmul(v[k], xv[k]);
+    } else {
+#pragma unroll
+      for (int k = 0; k < kCsrWarpIpt; ++k) {
+        const int q = lane + 32 * k;
+        if (q < n) sp[q] = dmul(ld_stream(vals + cs + q), ldg(x + ld_stream(crd + cs + q)));
+      }
+    }
+    __syncwarp();
+    const int lo = max(rb, cs) - cs, hi = min(re, cs + n) - cs;
+    for (int u = lo; u < hi; ++u) acc = dadd(acc, sp[u]);
+    __syncwarp();
+  }
+  if (lane < nr) y[w0 + lane] = acc;
 }
 
 // K2b: CSR vector-per-row.  One warp per row: lanes load 32 nonzeros at a time
@@ -454,7 +525,7 @@ spmv_ell_kernel(int64_t nrows, int32_t nslots, const int32_t* __restrict__ crd,
 // value and x loads are issued before the in-order add chain.
 template <int kMaxD>
 __global__ void __launch_bounds__(256, 8)
-spmv_dia_kernel(int64_t nrows, int64_t ncols, int32_t ndiag, DiaOffsets offs,
+spmv_dia_kernel(int64_t nrows, int64_t row0, int64_t ncols, int32_t ndiag, DiaOffsets offs,
                 const double* __restrict__ vals, const double* __restrict__ x,
                 double* __restrict__ y) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -463,7 +534,7 @@ spmv_dia_kernel(int64_t nrows, int64_t ncols, int32_t ndiag, DiaOffsets offs,
   bool in[kMaxD];
 #pragma unroll
   for (int d = 0; d < kMaxD; ++d) {
-    const int64_t j = i + offs.v[d];
+    const int64_t j = row0 + i + offs.v[d];
     in[d] = d < ndiag && j >= 0 && j < ncols;
     v[d] = in[d] ? ld_stream(vals + (int64_t)d * nrows + i) : 0.0;
     xv[d] = in[d] ? ldg(x + j) : 0.0;
@@ -477,14 +548,14 @@ spmv_dia_kernel(int64_t nrows, int64_t ncols, int32_t ndiag, DiaOffsets offs,
 
 // Device-resident offsets (any number of diagonals).
 __global__ void __launch_bounds__(256)
-spmv_dia_dev_kernel(int64_t nrows, int64_t ncols, int32_t ndiag, const int32_t* __restrict__ doffs,
-                    const double* __restrict__ vals, const double* __restrict__ x,
-                    double* __restrict__ y) {
+spmv_dia_dev_kernel(int64_t nrows, int64_t row0, int64_t ncols, int32_t ndiag,
+                    const int32_t* __restrict__ doffs, const double* __restrict__ vals,
+                    const double* __restrict__ x, double* __restrict__ y) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= nrows) return;
   double a = 0.0;
   for (int d = 0; d < ndiag; ++d) {
-    const int64_t j = i + ldg(doffs + d);
+    const int64_t j = row0 + i + ldg(doffs + d);
     if (j >= 0 && j < ncols) a = dadd(a, dmul(ld_stream(vals + (int64_t)d * nrows + i), ldg(x + j)));
   }
   y[i] = a;
@@ -544,6 +615,9 @@ static int launch_csr(int64_t nrows, const int32_t* pos, const int32_t* crd, con
   } else if (variant == 0) {
     spmv_csr_rowblock_kernel<kHashX><<<ceil_div(nrows, kCsrRows), kCsrThreads, 0, s>>>(
         nrows, pos, crd, vals, xop, y);
+  } else if (variant == 3 && !kHashX) {
+    const double* xd = reinterpret_cast<const XOperand<false>&>(xop).x;
+    spmv_csr_warp_kernel<<<ceil_div(nrows, 256), 256, 0, s>>>(nrows, pos, crd, vals, xd, y);
   } else if (variant == 1) {
     spmv_csr_vector_kernel<kHashX><<<ceil_div(nrows * 32, 256), 256, 0, s>>>(nrows, pos, crd,
                                                                             vals, xop, y);
@@ -607,11 +681,11 @@ extern "C" int sl_spmv_ell_f64(int64_t nrows, int64_t ncols, int32_t nslots, con
   return sl_host::launch_status();
 }
 
-extern "C" int sl_spmv_dia_f64(int64_t nrows, int64_t ncols, int32_t ndiag, const int32_t* offsets,
-                               int32_t offsets_on_host, const double* vals, const double* x,
-                               double* y, void* stream) {
-  if (nrows < 0 || ncols < 0 || ndiag < 0) return SL_ERR_INVALID;
-  if ((int64_t)ndiag * nrows > INT32_MAX || ncols > INT32_MAX) return SL_ERR_RANGE;
+extern "C" int sl_spmv_dia_rows_f64(int64_t nrows, int64_t row0, int64_t ncols, int32_t ndiag,
+                                    const int32_t* offsets, int32_t offsets_on_host,
+                                    const double* vals, const double* x, double* y, void* stream) {
+  if (nrows < 0 || row0 < 0 || ncols < 0 || ndiag < 0) return SL_ERR_INVALID;
+  if ((int64_t)ndiag * nrows > INT32_MAX || ncols > INT32_MAX || row0 > INT32_MAX) return SL_ERR_RANGE;
   if (nrows == 0) return SL_OK;
   if (!y || (ndiag > 0 && (!offsets || !vals || !x))) return SL_ERR_INVALID;
   cudaStream_t s = as_stream(stream);
@@ -625,11 +699,22 @@ extern "C" int sl_spmv_dia_f64(int64_t nrows, int64_t ncols, int32_t ndiag, cons
     doffs = offsets;
   }
   const int grid = ceil_div(nrows, 256);
-  if (!doffs && aligned16(vals) && aligned16(x) && ndiag > 0 && spmv_path() == 2) {
+  if (!doffs && row0 == 0 && aligned16(vals) && aligned16(x) && ndiag > 0 && spmv_path() == 2) {
     return sl_host::launch_dia_pipe(nrows, ncols, ndiag, p, vals, x, y, s);
-  } else if (doffs) spmv_dia_dev_kernel<<<grid, 256, 0, s>>>(nrows, ncols, ndiag, doffs, vals, x, y);
-  else if (ndiag <= 8) spmv_dia_kernel<8><<<grid, 256, 0, s>>>(nrows, ncols, ndiag, p, vals, x, y);
-  else if (ndiag <= 16) spmv_dia_kernel<16><<<grid, 256, 0, s>>>(nrows, ncols, ndiag, p, vals, x, y);
-  else spmv_dia_kernel<32><<<grid, 256, 0, s>>>(nrows, ncols, ndiag, p, vals, x, y);
+  } else if (doffs) {
+    spmv_dia_dev_kernel<<<grid, 256, 0, s>>>(nrows, row0, ncols, ndiag, doffs, vals, x, y);
+  } else if (ndiag <= 8) {
+    spmv_dia_kernel<8><<<grid, 256, 0, s>>>(nrows, row0, ncols, ndiag, p, vals, x, y);
+  } else if (ndiag <= 16) {
+    spmv_dia_kernel<16><<<grid, 256, 0, s>>>(nrows, row0, ncols, ndiag, p, vals, x, y);
+  } else {
+    spmv_dia_kernel<32><<<grid, 256, 0, s>>>(nrows, row0, ncols, ndiag, p, vals, x, y);
+  }
   return sl_host::launch_status();
+}
+
+extern "C" int sl_spmv_dia_f64(int64_t nrows, int64_t ncols, int32_t ndiag, const int32_t* offsets,
+                               int32_t offsets_on_host, const double* vals, const double* x,
+                               double* y, void* stream) {
+  return sl_spmv_dia_rows_f64(nrows, 0, ncols, ndiag, offsets, offsets_on_host, vals, x, y, stream);
 }

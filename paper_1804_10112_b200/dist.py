@@ -106,9 +106,9 @@ def gather_row_blocks(y_local, bounds: Sequence[int], group=None):
     m = max(sizes)
     pad = torch.zeros(m, dtype=y_local.dtype, device=y_local.device)
     pad[:y_local.numel()] = y_local
-    out = torch.empty(world * m, dtype=y_local.dtype, device=y_local.device)
-    dist.all_gather_into_tensor(out, pad, group=group)
-    return torch.cat([out[p * m:p * m + sizes[p]] for p in range(world)])
+    parts = [torch.empty_like(pad) for _ in range(world)]
+    dist.all_gather(parts, pad, group=group)
+    return torch.cat([parts[p][:sizes[p]] for p in range(world)])
 
 
 def replicate(t, src: int = 0, group=None):

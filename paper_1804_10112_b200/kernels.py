@@ -80,8 +80,10 @@ def spmv_ell(nrows, ncols, nslots, crd, vals, x, y=None):
     return y
 
 
-def spmv_dia(nrows, ncols, offsets, vals, x, y=None):
-    """`offsets`: host numpy int32 (passed as kernel parameters) or a CUDA tensor."""
+def spmv_dia(nrows, ncols, offsets, vals, x, y=None, row0=0):
+    """`offsets`: host numpy int32 (passed as kernel parameters) or a CUDA
+    tensor.  row0 > 0 evaluates the row block [row0, row0 + nrows) of a larger
+    matrix (vals hold the block's slots, x the whole vector)."""
     vals, x = _t(vals, F64, "vals"), _t(x, F64, "x")
     y = _out(y, nrows, F64, x, "y")
     if isinstance(offsets, torch.Tensor) and offsets.is_cuda:
@@ -91,9 +93,9 @@ def spmv_dia(nrows, ncols, offsets, vals, x, y=None):
         offs = np.ascontiguousarray(offsets, dtype=np.int32)
         nd, optr, on_host = len(offs), offs.ctypes.data, 1
         if nd > 32:
-            return spmv_dia(nrows, ncols, torch.as_tensor(offs, device=x.device), vals, x, y)
-    _lib.check(L().sl_spmv_dia_f64(nrows, ncols, nd, optr, on_host, P(vals), P(x), P(y), S()),
-               "spmv_dia")
+            return spmv_dia(nrows, ncols, torch.as_tensor(offs, device=x.device), vals, x, y, row0)
+    _lib.check(L().sl_spmv_dia_rows_f64(nrows, row0, ncols, nd, optr, on_host, P(vals), P(x),
+                                        P(y), S()), "spmv_dia")
     return y
 
 

@@ -43,7 +43,7 @@ def test_spmv_goldens_all_formats(golden):
                            cuda(c["coo_cols"], np.int32), cuda(c["coo_vals"], np.float64), x)
             assert np.array_equal(bits(y), bits(c["coo_y"])), name
         if "csr_y" in c:
-            for variant in (0, 1, 2):
+            for variant in (0, 1, 2, 3):
                 y = K.spmv_csr(nrows, ncols, cuda(c["csr_pos"], np.int32),
                                cuda(c["csr_crd"], np.int32), cuda(c["csr_vals"], np.float64), x,
                                variant=variant)
@@ -80,7 +80,7 @@ def test_spmv_coo_csr_vs_oracle(orc, n, nnz, lam, seed):
     y = K.spmv_coo(n, d["ncols"], cuda(d["rows"]), cuda(d["cols"]), cuda(d["vals"]), x)
     assert np.array_equal(bits(y), bits(ref))
     pos = wl.coo_to_csr_pos(d["rows"], n)
-    for variant in (0, 1, 2):
+    for variant in (0, 1, 2, 3):
         y = K.spmv_csr(n, d["ncols"], cuda(pos), cuda(d["cols"]), cuda(d["vals"]), x,
                        variant=variant)
         assert np.array_equal(bits(y), bits(ref)), variant
@@ -135,7 +135,7 @@ def test_full_size_spmv_bit_exact(orc):
     s = wl.stencil27()
     ref, _ = orc.spmv_csr(s["nrows"], s["pos"], s["crd"], s["vals"], s["x"])
     x = cuda(s["x"])
-    for variant in (0, 1, 2):
+    for variant in (0, 1, 2, 3):
         y = K.spmv_csr(s["nrows"], s["ncols"], cuda(s["pos"]), cuda(s["crd"]), cuda(s["vals"]),
                        x, variant=variant)
         assert np.array_equal(bits(y), bits(ref)), variant
@@ -373,3 +373,16 @@ def test_add_element_parallel_path(golden, orc, monkeypatch, two_pass):
     monkeypatch.setenv("SL_ADD_PATH", "elem")
     test_add_goldens(golden, two_pass)
     test_add_vs_oracle(orc, 100_000, 500_000, 2, two_pass)
+
+
+def test_dia_row_block_shards(orc):
+    from paper_1804_10112_b200 import dist as D
+    g = wl.dia7(g=32)
+    n = g["nrows"]
+    ref, _ = orc.spmv_dia(n, n, g["offsets"], g["vals"], g["x"])
+    x = cuda(g["x"])
+    ys = []
+    for r0, r1 in ((0, 5000), (5000, 20011), (20011, n)):
+        offs, v = D.shard_dia(g["offsets"], g["vals"], n, r0, r1)
+        ys.append(K.spmv_dia(r1 - r0, n, offs, cuda(v), x, row0=r0).cpu().numpy())
+    assert np.array_equal(bits(np.concatenate(ys)), bits(ref))

@@ -61,6 +61,7 @@ def main():
         jobs["csr"] = (bc, lambda: K.spmv_csr(n, n, p, c, v, x, y, variant=0))
         jobs["csr_vec"] = (bc, lambda: K.spmv_csr(n, n, p, c, v, x, y, variant=1))
         jobs["csr_merge"] = (bc, lambda: K.spmv_csr(n, n, p, c, v, x, y, variant=2))
+        jobs["csr_warp"] = (bc, lambda: K.spmv_csr(n, n, p, c, v, x, y, variant=3))
         jobs["ell"] = (12 * 27 * n + 16 * n, lambda: K.spmv_ell(n, n, 27, ec, ev, x, y))
 
     def d3():
@@ -96,7 +97,7 @@ def main():
 
     if want("coo") or want("hashx") or want("hashx_wdef") or want("csr_d1"):
         d1()
-    if want("csr") or want("ell") or want("csr_vec") or want("csr_merge"):
+    if want("csr") or want("ell") or want("csr_vec") or want("csr_merge") or want("csr_warp"):
         d2()
     if want("dia"):
         d3()
