@@ -311,7 +311,7 @@ template <int kR, class Src>
 SL_DEV void mttkrp_vec_body(int64_t I, int64_t e0, int64_t e1, int32_t row_first, int32_t prev_row,
                             bool head_partial, bool tail_cont, int64_t c,
                             const double* __restrict__ B, const double* __restrict__ C,
-                            double* __restrict__ A, CarryWs cw, Src& src) {
+                            double* __restrict__ A, CarryWs cw, Src& src, bool reuse_b) {
   constexpr int kLpn = kR / 4, kNps = 32 / kLpn;   // lanes per nonzero, nonzeros per step
   constexpr int kSteps = 4;                        // steps whose loads are issued together
   const int lane = threadIdx.x & 31, sub = lane / kLpn, q = lane % kLpn;
@@ -330,6 +330,12 @@ SL_DEV void mttkrp_vec_body(int64_t I, int64_t e0, int64_t e1, int32_t row_first
     if (sub == 0) store4(dst + 4 * q, tot);
   };
   src.start(e0, lane);
+  // sub s handles the kSteps CONSECUTIVE nonzeros [u0 + s*kSteps, ...) of a
+  // round, so it can keep the B row of a fiber in registers across nonzeros
+  // that share j (ncu: the kernel is L1-throughput bound; B reloads were half
+  // of the L1 traffic)
+  int32_t jprev = -1;
+  double4 b = make_double4(0.0, 0.0, 0.0, 0.0);
   for (int64_t base = e0; base < e1; base += 32) {
     const int n = (int)min64(32, e1 - base);
     int32_t li, lj, lk;
@@ -339,41 +345,44 @@ SL_DEV void mttkrp_vec_body(int64_t I, int64_t e0, int64_t e1, int32_t row_first
       double4 t[kSteps];
 #pragma unroll
       for (int st = 0; st < kSteps; ++st) {
-        const int u = u0 + st * kNps + sub;
+        const int u = u0 + sub * kSteps + st;
         const int us = u < n ? u : n - 1;
         const int32_t j = __shfl_sync(0xffffffffu, lj, us);
         const int32_t k = __shfl_sync(0xffffffffu, lk, us);
         const double v = __shfl_sync(0xffffffffu, lv, us);
-        const double4 b = ld4(B + (int64_t)j * kR + 4 * q);
+        if (j != jprev || !reuse_b) {
+          b = ld4(B + (int64_t)j * kR + 4 * q);
+          jprev = j;
+        }
         const double4 cc = ld4(C + (int64_t)k * kR + 4 * q);
         t[st] = make_double4(dmul(dmul(v, b.x), cc.x), dmul(dmul(v, b.y), cc.y),
                              dmul(dmul(v, b.z), cc.z), dmul(dmul(v, b.w), cc.w));
       }
       // fast path: rows are sorted, so if the round's last nonzero is still in
-      // the current row, all of them are; every sub adds its terms in the
-      // same per-sub order as the general path below
+      // the current row, all of them are; every sub adds its terms in order
       const int ulast = min(u0 + kSteps * kNps, n) - 1;
       if (__shfl_sync(0xffffffffu, li, ulast) == cur) {
 #pragma unroll
         for (int st = 0; st < kSteps; ++st)
-          if (u0 + st * kNps + sub < n) acc = add4(acc, t[st]);
+          if (u0 + sub * kSteps + st < n) acc = add4(acc, t[st]);
         continue;
       }
 #pragma unroll
-      for (int st = 0; st < kSteps; ++st) {
+      for (int s2 = 0; s2 < kNps; ++s2) {
 #pragma unroll
-        for (int s2 = 0; s2 < kNps; ++s2) {
-          const int u = u0 + st * kNps + s2;      // warp-uniform element index
-          if (u >= n) break;
-          const int32_t r = __shfl_sync(0xffffffffu, li, u);
-          if (r != cur) {
-            flush(false);
-            zero_rows(A, (int64_t)cur + 1, r, lane, kR);
-            acc = make_double4(0.0, 0.0, 0.0, 0.0);
-            cur = r;
-            first = false;
+        for (int st = 0; st < kSteps; ++st) {
+          const int u = u0 + s2 * kSteps + st;    // warp-uniform element index, storage order
+          if (u < n) {
+            const int32_t r = __shfl_sync(0xffffffffu, li, u);
+            if (r != cur) {
+              flush(false);
+              zero_rows(A, (int64_t)cur + 1, r, lane, kR);
+              acc = make_double4(0.0, 0.0, 0.0, 0.0);
+              cur = r;
+              first = false;
+            }
+            if (sub == s2) acc = add4(acc, t[st]);
           }
-          if (sub == s2) acc = add4(acc, t[st]);
         }
       }
     }
@@ -387,7 +396,8 @@ __global__ void __launch_bounds__(kMtThreads, 2)
 mttkrp_coo3_vec_kernel(int64_t I, int64_t nnz, int64_t nchunks, const int32_t* __restrict__ ii,
                        const int32_t* __restrict__ jj, const int32_t* __restrict__ kk,
                        const double* __restrict__ vals, const double* __restrict__ B,
-                       const double* __restrict__ C, double* __restrict__ A, CarryWs cw) {
+                       const double* __restrict__ C, double* __restrict__ A, CarryWs cw,
+                       bool reuse_b) {
   const int64_t c = (int64_t)blockIdx.x * kMtWarps + (threadIdx.x >> 5);
   if (c >= nchunks) return;
   const int64_t e0 = c * kMtChunk;
@@ -397,7 +407,7 @@ mttkrp_coo3_vec_kernel(int64_t I, int64_t nnz, int64_t nchunks, const int32_t* _
   const bool tail_cont = e1 < nnz && ldg(ii + e1) == ldg(ii + e1 - 1);
   CooSrc src{ii, jj, kk, vals, e1, 0, 0, 0, 0.0};
   mttkrp_vec_body<kR>(I, e0, e1, row_first, prev_row, prev_row == row_first, tail_cont, c, B, C, A,
-                      cw, src);
+                      cw, src, reuse_b);
   if (e1 == nnz) zero_rows(A, (int64_t)ldg(ii + nnz - 1) + 1, I, threadIdx.x & 31, kR);
 }
 
@@ -408,7 +418,7 @@ mttkrp_csf_vec_kernel(int64_t I, int64_t nslices, int64_t nfibers, int64_t nnz, 
                       const int32_t* __restrict__ crd1, const int32_t* __restrict__ pos2,
                       const int32_t* __restrict__ crd2, const double* __restrict__ vals,
                       const double* __restrict__ B, const double* __restrict__ C,
-                      double* __restrict__ A, CarryWs cw) {
+                      double* __restrict__ A, CarryWs cw, bool reuse_b) {
   const int64_t c = (int64_t)blockIdx.x * kMtWarps + (threadIdx.x >> 5);
   if (c >= nchunks) return;
   const int64_t e0 = c * kMtChunk;
@@ -423,7 +433,8 @@ mttkrp_csf_vec_kernel(int64_t I, int64_t nslices, int64_t nfibers, int64_t nnz, 
     tail_cont = ldg(pos2 + ldg(pos1 + sn)) < e1;     // it started before e1
   }
   CsfSrc src{crd0, pos1, crd1, pos2, crd2, vals, nslices, nfibers, e1, f, s, 0, 0.0};
-  mttkrp_vec_body<kR>(I, e0, e1, row_first, prev_row, head_partial, tail_cont, c, B, C, A, cw, src);
+  mttkrp_vec_body<kR>(I, e0, e1, row_first, prev_row, head_partial, tail_cont, c, B, C, A, cw, src,
+                      reuse_b);
   if (e1 == nnz) zero_rows(A, (int64_t)ldg(crd0 + nslices - 1) + 1, I, threadIdx.x & 31, kR);
 }
 
@@ -551,11 +562,45 @@ mttkrp_csf_kernel(int64_t I, int R, int64_t nslices, int64_t nfibers, int64_t nn
 }
 
 // ---- fix-up: rows cut by chunk boundaries ---------------------------------------------
-// Warp per chunk c (grid-stride) that holds a tail carry: the row continues
-// through chunks c+1 .. ce (their first rows equal it; they hold head carries).
-// ce is found by a galloping search over the monotone first_row array (most
-// segments end at c+1); the heads are summed 4-way interleaved and combined in
-// a fixed order, so the result is deterministic.
+// A row cut by chunk boundaries has a tail carry in the chunk where it starts
+// (s) and head carries in chunks s+1 .. ce.  Two levels, fixed order
+// (deterministic):
+//   1. group prefix: chunks are grouped by 32; within a group, each head is
+//      replaced by the running sum of the heads of its row from the group's
+//      start (or the row's first head in the group) up to it;
+//   2. owner: the warp of chunk s finds ce by galloping over the monotone
+//      first_row array and adds tail[s] + the group prefixes at the last
+//      chunk of the row in each group it spans (<= 1 + (ce - s) / 32 terms).
+// The heaviest D5 slice spans ~1950 chunks: one warp summing them serially
+// measured 328 us; this takes a few us.
+constexpr int kFixGroup = 32;
+
+template <int RPL>
+__global__ void __launch_bounds__(kMtThreads)
+mttkrp_group_prefix_kernel(int R, int64_t nchunks, CarryWs cw) {
+  const int lane = threadIdx.x & 31;
+  const int64_t g = (int64_t)blockIdx.x * kMtWarps + (threadIdx.x >> 5);
+  const int64_t c0 = g * kFixGroup;
+  if (c0 >= nchunks) return;
+  const int64_t c1 = min64(c0 + kFixGroup, nchunks);
+  double run[RPL];
+  int32_t prow = -1;
+  for (int64_t c = c0; c < c1; ++c) {
+    const int32_t row = cw.head_row[c];
+    if (row < 0) { prow = -1; continue; }
+#pragma unroll
+    for (int p = 0; p < RPL; ++p) {
+      const int r = lane + 32 * p;
+      if (r < R) {
+        const double h = cw.head[c * R + r];
+        run[p] = row == prow ? dadd(run[p], h) : h;
+        cw.head[c * R + r] = run[p];
+      }
+    }
+    prow = row;
+  }
+}
+
 template <int RPL>
 __global__ void __launch_bounds__(kMtThreads)
 mttkrp_fixup_kernel(int R, int64_t nchunks, CarryWs cw, double* __restrict__ A) {
@@ -588,14 +633,12 @@ mttkrp_fixup_kernel(int R, int64_t nchunks, CarryWs cw, double* __restrict__ A) 
     for (int p = 0; p < RPL; ++p) {
       const int r = lane + 32 * p;
       if (r >= R) continue;
-      double part[4] = {0.0, 0.0, 0.0, 0.0};
-      int64_t q = c + 1;
-      for (; q + 3 <= ce; q += 4) {
-#pragma unroll
-        for (int u = 0; u < 4; ++u) part[u] = dadd(part[u], cw.head[(q + u) * R + r]);
+      double tot = cw.tail[c * R + r];
+      // last chunk of the row in each group from group(c + 1) to group(ce)
+      for (int64_t gs = (c + 1) / kFixGroup; gs <= ce / kFixGroup; ++gs) {
+        const int64_t last = min64(ce, gs * kFixGroup + kFixGroup - 1);
+        tot = dadd(tot, cw.head[last * R + r]);
       }
-      for (int u = 0; q <= ce; ++q, ++u) part[u] = dadd(part[u], cw.head[q * R + r]);
-      const double tot = dadd(cw.tail[c * R + r], dadd(dadd(part[0], part[1]), dadd(part[2], part[3])));
       A[(int64_t)row * R + r] = tot;
     }
   }
@@ -615,6 +658,11 @@ using sl_host::ceil_div;
 
 static int64_t mt_nchunks(int64_t nnz) { return (nnz + kMtChunk - 1) / kMtChunk; }
 
+static int group_grid(int64_t nch) {
+  const int64_t ngroups = (nch + kFixGroup - 1) / kFixGroup;
+  return (int)((ngroups + kMtWarps - 1) / kMtWarps);
+}
+
 static int fixup_grid(int64_t nch) {
   const int64_t want = (nch + kMtWarps - 1) / kMtWarps;
   const int64_t cap = 8LL * sl_host::sm_count();
@@ -631,6 +679,24 @@ static int dispatch_rpl(int R, Launch&& launch) {
   if (R <= 64) return launch(std::integral_constant<int, 2>{});
   if (R <= 128) return launch(std::integral_constant<int, 4>{});
   return SL_ERR_RANGE;
+}
+
+// vectorised kernels: R in {16, 32, 64}, 32-byte aligned factor rows
+static bool vec_path(const double* B, const double* C, const double* A, int R) {
+  const bool aligned = (reinterpret_cast<uintptr_t>(B) & 31u) == 0 &&
+                       (reinterpret_cast<uintptr_t>(C) & 31u) == 0 &&
+                       (reinterpret_cast<uintptr_t>(A) & 31u) == 0;
+  return aligned && (R == 16 || R == 32 || R == 64) && !getenv("SL_MTTKRP_SCALAR");
+}
+
+// group prefix + owner fix-up of the rows cut by chunk boundaries
+static int launch_fixup(int R, int64_t nch, CarryWs cw, double* A, cudaStream_t s) {
+  return dispatch_rpl(R, [&](auto rpl) {
+    constexpr int RPL = decltype(rpl)::value;
+    mttkrp_group_prefix_kernel<RPL><<<group_grid(nch), kMtThreads, 0, s>>>(R, nch, cw);
+    mttkrp_fixup_kernel<RPL><<<fixup_grid(nch), kMtThreads, 0, s>>>(R, nch, cw, A);
+    return sl_host::launch_status();
+  });
 }
 
 static int mt_check(int64_t I, int64_t J, int64_t K, int32_t R, int64_t nnz) {
@@ -658,28 +724,25 @@ extern "C" int sl_mttkrp_coo3_f64(int64_t I, int64_t J, int64_t K, int32_t R, in
   const int64_t nch = mt_nchunks(nnz);
   CarryWs cw = carve(ws, nch + 1, R);
   const int grid = ceil_div(nch, kMtWarps);
-  const bool vec_ok = (reinterpret_cast<uintptr_t>(B) & 31u) == 0 &&
-                      (reinterpret_cast<uintptr_t>(C) & 31u) == 0 &&
-                      (reinterpret_cast<uintptr_t>(A) & 31u) == 0 && !getenv("SL_MTTKRP_SCALAR");
-  if (vec_ok && (R == 16 || R == 32 || R == 64)) {
+  const bool reuse_b = !getenv("SL_MTTKRP_NOREUSE");
+  if (vec_path(B, C, A, R)) {
     if (R == 16)
-      mttkrp_coo3_vec_kernel<16><<<grid, kMtThreads, 0, s>>>(I, nnz, nch, i, j, k, vals, B, C, A, cw);
+      mttkrp_coo3_vec_kernel<16><<<grid, kMtThreads, 0, s>>>(I, nnz, nch, i, j, k, vals, B, C, A,
+                                                             cw, reuse_b);
     else if (R == 32)
-      mttkrp_coo3_vec_kernel<32><<<grid, kMtThreads, 0, s>>>(I, nnz, nch, i, j, k, vals, B, C, A, cw);
+      mttkrp_coo3_vec_kernel<32><<<grid, kMtThreads, 0, s>>>(I, nnz, nch, i, j, k, vals, B, C, A,
+                                                             cw, reuse_b);
     else
-      mttkrp_coo3_vec_kernel<64><<<grid, kMtThreads, 0, s>>>(I, nnz, nch, i, j, k, vals, B, C, A, cw);
-    return dispatch_rpl(R, [&](auto rpl) {
-      constexpr int RPL = decltype(rpl)::value;
-      mttkrp_fixup_kernel<RPL><<<fixup_grid(nch), kMtThreads, 0, s>>>(R, nch, cw, A);
-      return sl_host::launch_status();
-    });
+      mttkrp_coo3_vec_kernel<64><<<grid, kMtThreads, 0, s>>>(I, nnz, nch, i, j, k, vals, B, C, A,
+                                                             cw, reuse_b);
+    return launch_fixup(R, nch, cw, A, s);
   }
-  return dispatch_rpl(R, [&](auto rpl) {
+  const int st2 = dispatch_rpl(R, [&](auto rpl) {
     constexpr int RPL = decltype(rpl)::value;
     mttkrp_coo3_kernel<RPL><<<grid, kMtThreads, 0, s>>>(I, R, nnz, nch, i, j, k, vals, B, C, A, cw);
-    mttkrp_fixup_kernel<RPL><<<fixup_grid(nch), kMtThreads, 0, s>>>(R, nch, cw, A);
-    return sl_host::launch_status();
+    return SL_OK;
   });
+  return st2 != SL_OK ? st2 : launch_fixup(R, nch, cw, A, s);
 }
 
 extern "C" int sl_mttkrp_csf_f64(int64_t I, int64_t J, int64_t K, int32_t R, int64_t nslices,
@@ -705,30 +768,27 @@ extern "C" int sl_mttkrp_csf_f64(int64_t I, int64_t J, int64_t K, int32_t R, int
   const int64_t nt = nslices > nfibers ? nslices : nfibers;
   csf_chunk_starts_kernel<<<ceil_div(nt, 256), 256, 0, s>>>(nslices, nfibers, pos1, pos2, cw);
   const int grid = ceil_div(nch, kMtWarps);
-  const bool vec_ok = (reinterpret_cast<uintptr_t>(B) & 31u) == 0 &&
-                      (reinterpret_cast<uintptr_t>(C) & 31u) == 0 &&
-                      (reinterpret_cast<uintptr_t>(A) & 31u) == 0 && !getenv("SL_MTTKRP_SCALAR");
-  if (vec_ok && (R == 16 || R == 32 || R == 64)) {
+  const bool reuse_b = !getenv("SL_MTTKRP_NOREUSE");
+  if (vec_path(B, C, A, R)) {
     if (R == 16)
       mttkrp_csf_vec_kernel<16><<<grid, kMtThreads, 0, s>>>(I, nslices, nfibers, nnz, nch, crd0,
-                                                            pos1, crd1, pos2, crd2, vals, B, C, A, cw);
+                                                            pos1, crd1, pos2, crd2, vals, B, C, A,
+                                                            cw, reuse_b);
     else if (R == 32)
       mttkrp_csf_vec_kernel<32><<<grid, kMtThreads, 0, s>>>(I, nslices, nfibers, nnz, nch, crd0,
-                                                            pos1, crd1, pos2, crd2, vals, B, C, A, cw);
+                                                            pos1, crd1, pos2, crd2, vals, B, C, A,
+                                                            cw, reuse_b);
     else
       mttkrp_csf_vec_kernel<64><<<grid, kMtThreads, 0, s>>>(I, nslices, nfibers, nnz, nch, crd0,
-                                                            pos1, crd1, pos2, crd2, vals, B, C, A, cw);
-    return dispatch_rpl(R, [&](auto rpl) {
-      constexpr int RPL = decltype(rpl)::value;
-      mttkrp_fixup_kernel<RPL><<<fixup_grid(nch), kMtThreads, 0, s>>>(R, nch, cw, A);
-      return sl_host::launch_status();
-    });
+                                                            pos1, crd1, pos2, crd2, vals, B, C, A,
+                                                            cw, reuse_b);
+    return launch_fixup(R, nch, cw, A, s);
   }
-  return dispatch_rpl(R, [&](auto rpl) {
+  const int st2 = dispatch_rpl(R, [&](auto rpl) {
     constexpr int RPL = decltype(rpl)::value;
     mttkrp_csf_kernel<RPL><<<grid, kMtThreads, 0, s>>>(I, R, nslices, nfibers, nnz, nch, crd0,
                                                        pos1, crd1, pos2, crd2, vals, B, C, A, cw);
-    mttkrp_fixup_kernel<RPL><<<fixup_grid(nch), kMtThreads, 0, s>>>(R, nch, cw, A);
-    return sl_host::launch_status();
+    return SL_OK;
   });
+  return st2 != SL_OK ? st2 : launch_fixup(R, nch, cw, A, s);
 }

@@ -244,7 +244,7 @@ SL_DEV void stage_products(const int32_t* __restrict__ crd, const double* __rest
 // consecutive probe steps per round (one coalesced 128-byte load), taking the
 // first match-or-empty in probe order — the sequential answer.
 constexpr int kHashSolo = 4;
-constexpr int kHashPer = 8;     // probe steps per lane per cooperative round
+constexpr int kHashPer = 8;     // probe steps per lane per cooperative round (256 per warp)
 
 template <int kThreads, int kIpt>
 SL_DEV void stage_products(const int32_t* __restrict__ crd, const double* __restrict__ vals,
@@ -281,36 +281,27 @@ SL_DEV void stage_products(const int32_t* __restrict__ crd, const double* __rest
       // checks steps s0 + kHashPer*l + {0..kHashPer-1} (independent loads);
       // the lowest step that matches or is empty ends the probe
       for (int64_t s0 = kHashSolo; s0 < w; s0 += kHashPer * 32) {
-        int hit_k = kHashPer;          // first of this lane's steps that stops the probe
-        int64_t hit_p = -1;
-        bool hit_match = false;
         int32_t v[kHashPer];
-        int64_t pp[kHashPer];
+        const int64_t sb = s0 + (int64_t)kHashPer * lane;   // this lane's first step
 #pragma unroll
         for (int k = 0; k < kHashPer; ++k) {
-          const int64_t st = s0 + (int64_t)kHashPer * lane + k;
-          pp[k] = -1;
-          v[k] = 0;
-          if (st < w) {
-            int64_t p = hh + st;
-            if (p >= w) p -= w;
-            pp[k] = p;
-            v[k] = ldg(lv.crd + p);
-          }
+          const int64_t st = sb + k;
+          int64_t p = hh + st;
+          while (p >= w) p -= w;
+          v[k] = st < w ? ldg(lv.crd + p) : 0;
         }
+        int hit_k = kHashPer;
 #pragma unroll
-        for (int k = kHashPer - 1; k >= 0; --k) {
-          if (pp[k] >= 0 && (v[k] == cc || v[k] == kEmpty)) {
-            hit_k = k;
-            hit_p = pp[k];
-            hit_match = v[k] == cc;
-          }
-        }
+        for (int k = kHashPer - 1; k >= 0; --k)
+          if (sb + k < w && (v[k] == cc || v[k] == kEmpty)) hit_k = k;
+        const bool hit_match = hit_k < kHashPer && v[hit_k < kHashPer ? hit_k : 0] == cc;
         const unsigned hit = __ballot_sync(0xffffffffu, hit_k < kHashPer);
         if (hit) {
           const int f = __ffs(hit) - 1;
-          const int64_t pf = __shfl_sync(0xffffffffu, hit_p, f);
+          const int hk = __shfl_sync(0xffffffffu, hit_k, f);
           const bool mf = __shfl_sync(0xffffffffu, hit_match ? 1 : 0, f) != 0;
+          int64_t pf = hh + s0 + (int64_t)kHashPer * f + hk;
+          while (pf >= w) pf -= w;
           found = mf ? pf : -1;
           break;
         }
@@ -322,7 +313,7 @@ SL_DEV void stage_products(const int32_t* __restrict__ crd, const double* __rest
 }
 
 template <bool kHashX>
-__global__ void __launch_bounds__(kCsrThreads, 8)
+__global__ void __launch_bounds__(kCsrThreads, kHashX ? 4 : 8)
 spmv_csr_rowblock_kernel(int64_t nrows, const int32_t* __restrict__ pos,
                          const int32_t* __restrict__ crd, const double* __restrict__ vals,
                          XOperand<kHashX> xop, double* __restrict__ y) {

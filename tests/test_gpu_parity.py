@@ -386,3 +386,28 @@ def test_dia_row_block_shards(orc):
         offs, v = D.shard_dia(g["offsets"], g["vals"], n, r0, r1)
         ys.append(K.spmv_dia(r1 - r0, n, offs, cuda(v), x, row0=r0).cpu().numpy())
     assert np.array_equal(bits(np.concatenate(ys)), bits(ref))
+
+
+def test_mttkrp_heavy_rows_span_many_chunks(orc, monkeypatch):
+    """Rows longer than 64 chunks (x 2048 nonzeros) exercise the group prefix."""
+    rng = np.random.default_rng(21)
+    I, J, Kd, R = 5, 1000, 600, 32
+    lens = [300_000, 1, 0, 150_000, 2049]
+    i = np.repeat(np.arange(I, dtype=np.int32), lens)
+    keys = []
+    for r, n in enumerate(lens):
+        kk = np.sort(rng.choice(J * Kd, size=n, replace=False))
+        keys.append(kk)
+    jk = np.concatenate(keys)
+    j, k = (jk // Kd).astype(np.int32), (jk % Kd).astype(np.int32)
+    vals = 1.0 - rng.random(len(i))
+    B, C = rng.uniform(-1, 1, (J, R)), rng.uniform(-1, 1, (Kd, R))
+    ref, absA = orc.mttkrp_coo3(I, i, j, k, vals, B, C)
+    csf = wl.coo3_to_csf(i, j, k, None)
+    for env in (None, "1"):
+        if env:
+            monkeypatch.setenv("SL_MTTKRP_NOREUSE", env)
+        A1, A2 = _mttkrp_both(None, I, J, Kd, (i, j, k, vals), csf, B, C)
+        for A in (A1, A2):
+            ok, err = orc.within_condition(A, ref, absA, RTOL)
+            assert ok, err
