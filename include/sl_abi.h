@@ -237,6 +237,32 @@ int sl_mttkrp_csf_f64(int64_t I, int64_t J, int64_t K, int32_t R,
                       const double* vals, const double* B, const double* C,
                       double* A, void* ws, size_t ws_bytes, void* stream);
 
+/* ---- format conversion (formats.convert, formats.py:583-587) -------------
+ * COO -> CSR exactly as the reference's identity copy: call the A+B entry
+ * points with an empty A (a_pos all zero) and the COO as B; the structural
+ * row pointer alone (row-sorted COO, unique coordinates) is: */
+int sl_convert_coo_to_csr(int64_t nrows, int64_t nnz, const int32_t* rows, int32_t* pos,
+                          void* stream);
+/* CSR -> ELL: nslots = max per-row count of nonzero values (read *out_dev
+ * after the stream); entries with value 0.0 are dropped and values stored as
+ * 0.0 + v, as the reference's reorder writer + assemble do. */
+int sl_csr_max_row_length(int64_t nrows, const int32_t* pos, const double* vals,
+                          int32_t* out_dev, void* stream);
+int sl_convert_csr_to_ell(int64_t nrows, int32_t nslots, const int32_t* pos,
+                          const int32_t* crd, const double* vals,
+                          int32_t* ell_crd, double* ell_vals, void* stream);
+/* COO (unique coordinates) -> DIA: offsets of the nonzero entries' diagonals,
+ * sorted (offsets needs nrows + ncols - 1 entries; *ndiag_dev is the count),
+ * then the values [ndiag * nrows] (0.0 where no entry). */
+size_t sl_convert_coo_to_dia_workspace_bytes(int64_t nrows, int64_t ncols);
+int sl_convert_coo_to_dia_offsets(int64_t nrows, int64_t ncols, int64_t nnz,
+                                  const int32_t* rows, const int32_t* cols, const double* vals,
+                                  int32_t* offsets, int32_t* ndiag_dev,
+                                  void* ws, size_t ws_bytes, void* stream);
+int sl_convert_coo_to_dia_values(int64_t nrows, int64_t ncols, int64_t nnz, int32_t ndiag,
+                                 const int32_t* rows, const int32_t* cols, const double* vals,
+                                 double* dia_vals, void* ws, size_t ws_bytes, void* stream);
+
 /* ---- utilities used by the benchmark ------------------------------------- */
 /* Writes `bytes` of junk into `buf` to evict L2 between timed iterations. */
 int sl_l2_flush(void* buf, size_t bytes, void* stream);

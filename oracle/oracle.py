@@ -216,6 +216,57 @@ def mttkrp_csf(I, crd0, pos1, crd1, pos2, crd2, vals, B, C, threads=None):
     return A
 
 
+# ---- format conversion (formats.convert -> engine.identity_copy,
+#      formats.py:583-587, engine.py:775-779) -------------------------------
+
+def convert_coo_to_csr(nrows, rows, cols, vals, threads=None):
+    """Identity copy COO -> CSR = gather-append writer over the COO's grouped
+    rows/columns (engine.py:330-434): the A+B restatement with A empty."""
+    a_pos = np.zeros(nrows + 1, dtype=np.int32)
+    e_i = np.zeros(0, dtype=np.int32)
+    e_f = np.zeros(0, dtype=np.float64)
+    return add_csr(nrows, a_pos, e_i, e_f, cols, vals, b_rows=rows, threads=threads)
+
+
+def convert_csr_to_ell(nrows, pos, crd, vals):
+    """Identity copy -> ELL goes through the reorder writer (cells[key] =
+    0.0 + v, engine.py:437-452) and assemble, whose canonicalize drops exact
+    zeros (formats.py:217-222); ELL layout slot-major s*N + i with padding
+    (col 0, 0.0), nslots = longest row (formats.py:322-335, 443-455)."""
+    pos = np.asarray(pos, dtype=np.int64)
+    crd = np.asarray(crd, dtype=np.int32)
+    vals = np.asarray(vals, dtype=np.float64)
+    keep = vals != 0.0
+    row = np.repeat(np.arange(nrows, dtype=np.int64), np.diff(pos))[keep]
+    kc, kv = crd[keep], 0.0 + vals[keep]
+    counts = np.bincount(row, minlength=nrows) if nrows else np.zeros(0, np.int64)
+    nslots = int(counts.max()) if len(kc) else 0
+    start = np.zeros(nrows + 1, dtype=np.int64)
+    np.cumsum(counts, out=start[1:])
+    slot = np.arange(len(kc), dtype=np.int64) - start[row]
+    ecrd = np.zeros(nslots * nrows, dtype=np.int32)
+    evals = np.zeros(nslots * nrows, dtype=np.float64)
+    ecrd[slot * nrows + row] = kc
+    evals[slot * nrows + row] = kv
+    return nslots, ecrd, evals
+
+
+def convert_coo_to_dia(nrows, ncols, rows, cols, vals):
+    """Identity copy -> DIA (unique coordinates): reorder writer + assemble;
+    offsets = sorted distinct c - r of the kept entries (formats.py:313),
+    vals[d*N + r] (formats.py:405-412), 0.0 elsewhere."""
+    rows = np.asarray(rows, dtype=np.int64)
+    cols = np.asarray(cols, dtype=np.int64)
+    vals = np.asarray(vals, dtype=np.float64)
+    keep = vals != 0.0
+    r, c, v = rows[keep], cols[keep], 0.0 + vals[keep]
+    offs = np.unique(c - r).astype(np.int32)
+    d = np.searchsorted(offs, c - r)
+    dvals = np.zeros(len(offs) * nrows, dtype=np.float64)
+    dvals[d * nrows + r] = v
+    return offs, dvals
+
+
 def bits_equal(a, b) -> bool:
     """Bit-exact equality of float64 arrays, treating +0.0 and -0.0 as different."""
     a = np.ascontiguousarray(a, dtype=np.float64)

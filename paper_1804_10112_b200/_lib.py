@@ -72,6 +72,14 @@ SIGNATURES = {
                             _p], ctypes.c_int),
     "sl_mttkrp_csf_f64": ([_i64, _i64, _i64, _i32, _i64, _i64, _i64, _p, _p, _p, _p, _p, _p, _p,
                            _p, _p, _p, _sz, _p], ctypes.c_int),
+    "sl_convert_coo_to_csr": ([_i64, _i64, _p, _p, _p], ctypes.c_int),
+    "sl_csr_max_row_length": ([_i64, _p, _p, _p, _p], ctypes.c_int),
+    "sl_convert_csr_to_ell": ([_i64, _i32, _p, _p, _p, _p, _p, _p], ctypes.c_int),
+    "sl_convert_coo_to_dia_workspace_bytes": ([_i64, _i64], _sz),
+    "sl_convert_coo_to_dia_offsets": ([_i64, _i64, _i64, _p, _p, _p, _p, _p, _p, _sz, _p],
+                                      ctypes.c_int),
+    "sl_convert_coo_to_dia_values": ([_i64, _i64, _i64, _i32, _p, _p, _p, _p, _p, _sz, _p],
+                                     ctypes.c_int),
     "sl_l2_flush": ([_p, _sz, _p], ctypes.c_int),
 }
 

@@ -46,7 +46,7 @@ constexpr int kCooVec = 4;                       // elements per vector load
 constexpr int kCooVecPerThread = 2;
 constexpr int kCooIpt = kCooVec * kCooVecPerThread;  // 8 items per thread
 constexpr int kCooTile = kCooThreads * kCooIpt;      // 2048 nonzeros owned per tile
-constexpr int kCooHalo = kCooThreads;                // + 256 staged past the tile end
+constexpr int kCooHalo = 128;                        // staged past the tile end (7 blocks/SM fit)
 
 __global__ void __launch_bounds__(kCooThreads, 7)
 spmv_coo_kernel(int64_t nrows, int64_t nnz, const int32_t* __restrict__ rows,
@@ -57,6 +57,7 @@ spmv_coo_kernel(int64_t nrows, int64_t nnz, const int32_t* __restrict__ rows,
   __shared__ __align__(16) double s_prod[kCooTile + kCooHalo];
   __shared__ uint16_t s_start[kCooTile];          // row-start items (< kCooTile + kCooHalo)
   __shared__ int32_t s_wcnt[kCooThreads / 32];
+  __shared__ unsigned s_mask[kCooThreads / 32][kCooTile / kCooThreads];
 
   const int tid = threadIdx.x;
   const int64_t e0 = (int64_t)blockIdx.x * kCooTile;
@@ -115,17 +116,21 @@ spmv_coo_kernel(int64_t nrows, int64_t nnz, const int32_t* __restrict__ rows,
   if (tid == 0) s_row[3] = e0 == 0 ? -1 : ldg(rows + e0 - 1);
   __syncthreads();
 
-  // ---- compact the row starts of the owned range with warp ballots
+  // ---- compact the row starts of the owned range with warp ballots; the
+  // predecessor's row comes from a shuffle (one shared load per item), the
+  // per-warp masks live in shared memory (no register spills)
   const int lane = tid & 31, warp = tid >> 5;
   constexpr int kPerWarp = kCooTile / (kCooThreads / 32);   // 256 items per warp
-  unsigned masks[kPerWarp / 32];
   int cnt = 0;
 #pragma unroll
   for (int b = 0; b < kPerWarp / 32; ++b) {
     const int q = warp * kPerWarp + b * 32 + lane;
-    const bool f = q < n_in && s_row[4 + q] != s_row[3 + q];
-    masks[b] = __ballot_sync(0xffffffffu, f);
-    cnt += __popc(masks[b]);
+    const int32_t r = s_row[4 + q];
+    int32_t rp = __shfl_up_sync(0xffffffffu, r, 1);
+    if (lane == 0) rp = s_row[3 + q];
+    const unsigned m = __ballot_sync(0xffffffffu, q < n_in && r != rp);
+    if (lane == 0) s_mask[warp][b] = m;
+    cnt += __popc(m);
   }
   if (lane == 0) s_wcnt[warp] = cnt;
   __syncthreads();
@@ -138,7 +143,7 @@ spmv_coo_kernel(int64_t nrows, int64_t nnz, const int32_t* __restrict__ rows,
   }
 #pragma unroll
   for (int b = 0; b < kPerWarp / 32; ++b) {
-    const unsigned m = masks[b];
+    const unsigned m = s_mask[warp][b];
     if (m & (1u << lane))
       s_start[base + __popc(m & ((1u << lane) - 1u))] = (uint16_t)(warp * kPerWarp + b * 32 + lane);
     base += __popc(m);

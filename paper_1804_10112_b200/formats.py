@@ -278,3 +278,42 @@ def csf_storage(pos0, crd0, pos1, crd1, pos2, crd2, vals, dims, device="cuda") -
           LevelStorage(fmt.levels[1], pos=pos1, crd=crd1, device=device),
           LevelStorage(fmt.levels[2], pos=pos2, crd=crd2, device=device)]
     return TensorStorage(fmt, dims, lv, _f64(vals, device))
+
+
+# ---------------------------------------------------------------------------
+# conversion
+
+def convert(src: TensorStorage, dst: TensorFormat) -> TensorStorage:
+    """Re-store `src` in format `dst` (formats.py:583-587: an identity
+    assignment `OUT(i,j) = IN(i,j)` evaluated by the engine, engine.py:775-779).
+
+    Device kernels (csrc/convert.cu, csrc/add.cu) reproduce the reference's
+    output exactly:
+      COO -> CSR : gather-append copy — duplicates summed +0.0 + v1 + ...,
+                   stored 0.0 + value, explicit zeros kept (A+B kernels, A empty)
+      CSR -> ELL : reorder writer + assemble — exact zeros dropped, 0.0 + v
+      COO -> ELL : COO -> CSR -> ELL (same values as the direct copy)
+      COO -> DIA : reorder writer + assemble (unique coordinates)
+    Other pairs raise UnsupportedOutputError (no CPU interpretation)."""
+    from . import kernels as K
+    from .engine import format_class
+    from .errors import UnsupportedOutputError
+
+    s, d = format_class(src.fmt), format_class(dst)
+    dims = tuple(src.dims)
+    if len(dims) != 2:
+        raise UnsupportedOutputError(f"no device conversion {s} -> {d}")
+    n, m = dims
+    dev = src.vals.device
+    if s == "coo" and d in ("csr", "ell"):
+        pos, crd, vals = K.coo_to_csr(n, src.levels[0].crd, src.levels[1].crd, src.vals)
+        csr = csr_storage(pos, crd, vals, dims, device=dev)
+        return csr if d == "csr" else convert(csr, dst)
+    if s == "csr" and d == "ell":
+        l1 = src.levels[1]
+        nslots, ecrd, evals = K.csr_to_ell(n, l1.pos, l1.crd, src.vals)
+        return ell_storage(nslots, ecrd, evals, dims, device=dev)
+    if s == "coo" and d == "dia":
+        offs, dvals = K.coo_to_dia(n, m, src.levels[0].crd, src.levels[1].crd, src.vals)
+        return dia_storage(offs.cpu().numpy(), dvals, dims, device=dev)
+    raise UnsupportedOutputError(f"no device conversion {s} -> {d}")

@@ -171,6 +171,62 @@ def add_csr(nrows, a_pos, a_crd, a_vals, b_cols, b_vals, b_rows=None, b_pos=None
     return c_pos, c_crd, c_vals
 
 
+# ---- format conversion (formats.convert, formats.py:583-587) -------------------
+
+def coo_to_csr(nrows, rows, cols, vals, sync=True, two_pass=True):
+    """COO-SoA -> CSR exactly as the reference's identity copy: the A+B
+    count -> scan -> fill kernels with an empty A, so duplicates are summed
+    (+0.0 + v1 + v2 ...) and values stored as 0.0 + v (explicit zeros kept)."""
+    rows = _t(rows, I32, "rows")
+    a_pos = torch.zeros(nrows + 1, dtype=I32, device=rows.device)
+    empty_i = torch.empty(0, dtype=I32, device=rows.device)
+    empty_f = torch.empty(0, dtype=F64, device=rows.device)
+    return add_csr(nrows, a_pos, empty_i, empty_f, cols, vals, b_rows=rows, sync=sync,
+                   two_pass=two_pass)
+
+
+def coo_rowptr(nrows, rows, pos=None):
+    """Structural part alone: the row pointer of a row-sorted COO."""
+    rows = _t(rows, I32, "rows")
+    pos = _out(pos, nrows + 1, I32, rows, "pos")
+    _lib.check(L().sl_convert_coo_to_csr(nrows, rows.numel(), P(rows), P(pos), S()), "coo_rowptr")
+    return pos
+
+
+def csr_to_ell(nrows, pos, crd, vals):
+    """CSR -> ELL (slot-major, padding (0, 0.0)); zeros dropped as assemble
+    does.  Returns (nslots, crd, vals); reads nslots back (one sync)."""
+    pos, crd, vals = _t(pos, I32, "pos"), _t(crd, I32, "crd"), _t(vals, F64, "vals")
+    m = torch.empty(1, dtype=I32, device=pos.device)
+    _lib.check(L().sl_csr_max_row_length(nrows, P(pos), P(vals), P(m), S()), "csr_max_row")
+    nslots = int(m.item())
+    ecrd = torch.empty(nslots * nrows, dtype=I32, device=pos.device)
+    evals = torch.empty(nslots * nrows, dtype=F64, device=pos.device)
+    _lib.check(L().sl_convert_csr_to_ell(nrows, nslots, P(pos), P(crd), P(vals), P(ecrd),
+                                         P(evals), S()), "csr_to_ell")
+    return nslots, ecrd, evals
+
+
+def coo_to_dia(nrows, ncols, rows, cols, vals):
+    """COO (unique coordinates) -> DIA.  Returns (offsets, vals); reads the
+    diagonal count back (one sync)."""
+    rows, cols, vals = _t(rows, I32, "rows"), _t(cols, I32, "cols"), _t(vals, F64, "vals")
+    dev = rows.device
+    ws = _ws(L().sl_convert_coo_to_dia_workspace_bytes(nrows, ncols), rows)
+    offs = torch.empty(nrows + ncols - 1, dtype=I32, device=dev)
+    nd = torch.empty(1, dtype=I32, device=dev)
+    nnz = rows.numel()
+    _lib.check(L().sl_convert_coo_to_dia_offsets(nrows, ncols, nnz, P(rows), P(cols), P(vals),
+                                                 P(offs), P(nd), P(ws), ws.numel(), S()),
+               "coo_to_dia_offsets")
+    ndiag = int(nd.item())
+    dvals = torch.empty(ndiag * nrows, dtype=F64, device=dev)
+    _lib.check(L().sl_convert_coo_to_dia_values(nrows, ncols, nnz, ndiag, P(rows), P(cols),
+                                                P(vals), P(dvals), P(ws), ws.numel(), S()),
+               "coo_to_dia_values")
+    return offs[:ndiag].clone(), dvals
+
+
 # ---- MTTKRP ---------------------------------------------------------------------
 
 def _mttkrp_ws(nnz, R, like, ws):

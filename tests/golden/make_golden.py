@@ -270,6 +270,70 @@ def mttkrp_cases():
 # ---------------------------------------------------------------------------
 # Level-function KATs (pkg/tests/test_levels.py), as explicit tables
 
+# ---------------------------------------------------------------------------
+# format conversion (formats.convert -> engine.identity_copy, formats.py:583,
+# engine.py:775-779)
+
+def _csr_arrays(st, prefix, out):
+    out[f"{prefix}_pos"] = i32(st.levels[1].pos)
+    out[f"{prefix}_crd"] = i32(st.levels[1].crd)
+    out[f"{prefix}_vals"] = f64(st.vals[:len(st.levels[1].crd)] if st.levels[1].crd else [])
+
+
+def convert_case(name, nrows, ncols, rows, cols, vals, dia=True):
+    """COO -> CSR, CSR -> ELL (and, for unique coordinates, COO -> DIA)
+    through the reference's own convert()."""
+    out = {"nrows": nrows, "ncols": ncols}
+    coo = sl.assemble(sl.preset("coo-soa"), (nrows, ncols),
+                      coordlist((nrows, ncols), zip(rows, cols), vals))
+    out["coo_rows"] = i32(coo.levels[0].crd)
+    out["coo_cols"] = i32(coo.levels[1].crd)
+    out["coo_vals"] = f64(coo.vals[:len(coo.levels[1].crd)] if coo.levels[1].crd else [])
+    csr = rf.convert(coo, sl.preset("csr"))
+    _csr_arrays(csr, "csr", out)
+    ell = rf.convert(csr, sl.preset("ell"))
+    out["ell_nslots"] = ell.levels[0].n
+    out["ell_crd"] = i32(ell.levels[2].crd)
+    out["ell_vals"] = f64(ell.vals[:ell.levels[0].n * nrows] if ell.levels[0].n else [])
+    if dia:
+        d = rf.convert(coo, sl.preset("dia"))
+        out["dia_offsets"] = i32(d.levels[1].offset)
+        nd = len(d.levels[1].offset)
+        out["dia_vals"] = f64(d.vals[:nd * nrows] if nd else [])
+    return name, out
+
+
+def convert_cases():
+    cases = []
+    for seed in range(4):
+        rng = np.random.default_rng(900 + seed)
+        n, m = 30 + 5 * seed, 25 + 4 * seed
+        nnz = 5 * n
+        r = rng.integers(0, n, nnz)
+        c = rng.integers(0, m, nnz)
+        v = rng.uniform(-1, 1, nnz)
+        v[rng.random(nnz) < 0.1] = 0.0          # explicit zeros
+        v[rng.random(nnz) < 0.05] = -0.0        # signed zeros
+        o = np.lexsort((c, r))
+        # duplicates kept in COO (non-unique level) -> summed by the copy
+        cases.append(convert_case(f"conv_dup{seed}", n, m, r[o], c[o], v[o], dia=False))
+        key = np.unique(r * m + c)
+        ur, uc = key // m, key % m
+        uv = rng.uniform(-1, 1, len(key))
+        uv[rng.random(len(key)) < 0.1] = 0.0
+        uv[rng.random(len(key)) < 0.05] = -0.0
+        cases.append(convert_case(f"conv_uniq{seed}", n, m, ur, uc, uv))
+    cases.append(convert_case("conv_empty", 6, 4, [], [], []))
+    cases.append(convert_case("conv_hypersparse", 20, 30, [2, 2, 11, 19], [29, 0, 7, 3],
+                              [1.5, -2.0, 0.25, 8.0]))
+    cases.append(convert_case("conv_all_zero", 4, 4, [0, 1, 3], [0, 2, 1], [0.0, -0.0, 0.0]))
+    st = wl.stencil27(g=3, seed=5)
+    rr = np.repeat(np.arange(st["nrows"]), np.diff(st["pos"]))
+    cases.append(convert_case("conv_stencil_g3", st["nrows"], st["ncols"], rr, st["crd"],
+                              st["vals"]))
+    return cases
+
+
 def level_kats():
     """Run the reference level functions on the test_levels.py fixtures."""
     E = rl.EMPTY
@@ -401,6 +465,7 @@ def main():
         "spmv": spmv_cases() + [coo_duplicates_case(), dia_case(4, 21), dia_case(5, 22)],
         "add": add_cases(),
         "mttkrp": mttkrp_cases(),
+        "convert": convert_cases(),
     }
     for group, cases in groups.items():
         flat = {}

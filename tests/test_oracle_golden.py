@@ -9,6 +9,7 @@ import numpy as np
 import pytest
 
 from paper_1804_10112_b200 import workloads as wl
+from conftest import load_cases
 
 
 def _bits(a):
@@ -147,3 +148,23 @@ def test_oracle_mt_equals_st_medium(orc, threads):
     A1, _ = orc.mttkrp_coo3(200, m["i"], m["j"], m["k"], m["vals"], m["B"], m["C"])
     A2 = orc.mttkrp_coo3(200, m["i"], m["j"], m["k"], m["vals"], m["B"], m["C"], threads=threads)
     assert np.array_equal(_bits(A1), _bits(A2))
+
+
+# ---------------------------------------------------------------------------
+# format conversion: the oracle restatement against the reference's convert()
+
+def test_oracle_convert_goldens(orc):
+    for name, c in load_cases("convert").items():
+        n, m = int(c["nrows"]), int(c["ncols"])
+        pos, crd, vals = orc.convert_coo_to_csr(n, c["coo_rows"], c["coo_cols"], c["coo_vals"])
+        assert np.array_equal(pos, c["csr_pos"]), name
+        assert np.array_equal(crd, c["csr_crd"]), name
+        assert orc.bits_equal(vals, c["csr_vals"]), name
+        ns, ecrd, evals = orc.convert_csr_to_ell(n, c["csr_pos"], c["csr_crd"], c["csr_vals"])
+        assert ns == int(c["ell_nslots"]), name
+        assert np.array_equal(ecrd, c["ell_crd"]), name
+        assert orc.bits_equal(evals, c["ell_vals"]), name
+        if "dia_offsets" in c:
+            offs, dv = orc.convert_coo_to_dia(n, m, c["coo_rows"], c["coo_cols"], c["coo_vals"])
+            assert np.array_equal(offs, c["dia_offsets"]), name
+            assert orc.bits_equal(dv, c["dia_vals"]), name
