@@ -299,7 +299,7 @@ def convert(src: TensorStorage, dst: TensorFormat) -> TensorStorage:
     from .engine import format_class
     from .errors import UnsupportedOutputError
 
-    s, d = format_class(src.fmt), format_class(dst)
+    s, d = format_class(src.format), format_class(dst)
     dims = tuple(src.dims)
     if len(dims) != 2:
         raise UnsupportedOutputError(f"no device conversion {s} -> {d}")
