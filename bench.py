@@ -340,15 +340,33 @@ def run_formats(torch, K, wl, dev, timer, peak, steps):
                     "csr_hashx": lambda: K.spmv_csr_hashx(n, pos, c, v, h["width"], hc, hv, y)},
                    steps, 3)
     b = bytes_coo(n, m, nnz)
-    t = float(np.median(tt["coo"]))
+    t = float(np.mean(tt["coo"]))
     res["coo_spmv_D1"] = {"ms": round(t, 5), "GB/s": round(b / t / 1e6, 1),
                           "frac": round(b / t / 1e6 / peak, 4), "nnz/s": round(nnz / t * 1e3, 1),
                           "bytes": b}
     bh = 4 * (n + 1) + 12 * nnz + 8 * n + 12 * h["width"]
-    t = float(np.median(tt["csr_hashx"]))
+    t = float(np.mean(tt["csr_hashx"]))
     res["csr_hashx_H1"] = {"ms": round(t, 5), "GB/s": round(bh / t / 1e6, 1),
                            "locates/s": round(nnz / t * 1e3, 1), "bytes": bh}
-    del r, c, v, x, y, pos
+    # format conversion (formats.convert): the COO -> CSR identity copy, and
+    # the structural row pointer alone; the paper's "convert, then CSR SpMV"
+    # alternative to COO SpMV costs convert + csr_spmv_D1.
+    rp = torch.empty(n + 1, dtype=torch.int32, device=dev)
+    tt = timer.run({"conv": lambda: K.coo_to_csr(n, r, c, v, sync=False),
+                    "rowptr": lambda: K.coo_rowptr(n, r, rp),
+                    "csr": lambda: K.spmv_csr(n, m, pos, c, v, x, y)}, steps, 3)
+    bc = 16 * nnz + 4 * (n + 1) + 12 * nnz
+    t = float(np.mean(tt["conv"]))
+    res["convert_coo_to_csr_D1"] = {"ms": round(t, 5), "GB/s": round(bc / t / 1e6, 1),
+                                    "frac": round(bc / t / 1e6 / peak, 4), "bytes": bc}
+    br = 4 * nnz + 4 * (n + 1)
+    t = float(np.mean(tt["rowptr"]))
+    res["coo_rowptr_D1"] = {"ms": round(t, 5), "GB/s": round(br / t / 1e6, 1), "bytes": br}
+    bs = bytes_csr(n, nnz)
+    t = float(np.mean(tt["csr"]))
+    res["csr_spmv_D1"] = {"ms": round(t, 5), "GB/s": round(bs / t / 1e6, 1),
+                          "frac": round(bs / t / 1e6 / peak, 4), "bytes": bs}
+    del r, c, v, x, y, pos, rp
 
     g = wl.dia7()
     n = g["nrows"]
@@ -356,7 +374,7 @@ def run_formats(torch, K, wl, dev, timer, peak, steps):
     y = torch.empty(n, dtype=torch.float64, device=dev)
     tt = timer.run({"dia": lambda: K.spmv_dia(n, n, g["offsets"], gv, gx, y)}, steps, 3)
     b = bytes_dia(n, n, g["offsets"].tolist())
-    t = float(np.median(tt["dia"]))
+    t = float(np.mean(tt["dia"]))
     res["dia_spmv_D3"] = {"ms": round(t, 5), "GB/s": round(b / t / 1e6, 1),
                           "frac": round(b / t / 1e6 / peak, 4), "bytes": b}
     del gv, gx, y
@@ -373,7 +391,7 @@ def run_formats(torch, K, wl, dev, timer, peak, steps):
     tt = timer.run({"add": add}, steps, 3)
     nnz_c = int(out["c"][0][n].item())
     b = 4 * (n + 1) + 12 * len(a["a_crd"]) + 16 * len(a["b_cols"]) + 4 * (n + 1) + 12 * nnz_c
-    t = float(np.median(tt["add"]))
+    t = float(np.mean(tt["add"]))
     res["add_csr_coo_D4"] = {"ms": round(t, 5), "GB/s": round(b / t / 1e6, 1),
                              "frac": round(b / t / 1e6 / peak, 4), "nnz_c": nnz_c, "bytes": b,
                              "input nnz/s": round((len(a["a_crd"]) + len(a["b_cols"])) / t * 1e3, 1)}
@@ -396,7 +414,7 @@ def run_formats(torch, K, wl, dev, timer, peak, steps):
     n1 = len(csf["crd1"])
     b_csf = 8 + 4 * len(csf["crd0"]) + 4 * (len(csf["crd0"]) + 1) + 4 * n1 + 4 * (n1 + 1) + 12 * nnz + bf
     for name, b, key in (("mttkrp_coo3_D5", b_coo, "coo3"), ("mttkrp_csf_D5", b_csf, "csf")):
-        t = float(np.median(tt[key]))
+        t = float(np.mean(tt[key]))
         res[name] = {"ms": round(t, 4), "nnz/s": round(nnz / t * 1e3, 1),
                      "nnz*R/s": round(nnz * R / t * 1e3, 1), "GB/s": round(b / t / 1e6, 1),
                      "frac": round(b / t / 1e6 / peak, 4), "GFLOP/s": round(3 * nnz * R / t / 1e6, 1),

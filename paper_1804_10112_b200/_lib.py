@@ -8,6 +8,7 @@ compute entry point raises DeviceError.
 from __future__ import annotations
 
 import ctypes
+import os
 import re
 from pathlib import Path
 
@@ -97,6 +98,8 @@ def load(path: Path = LIB_PATH):
     """Load the library (no CUDA context is created)."""
     global _LIB
     if _LIB is None:
+        # SL_LIB_PATH: load another build of the same ABI (A/B timing of two builds)
+        path = Path(os.environ.get("SL_LIB_PATH", str(path)))
         if not path.exists():
             raise E.DeviceError(
                 f"kernel library {path} is missing: run `python -m paper_1804_10112_b200.build` "

@@ -54,14 +54,16 @@ coo_rowptr_kernel(int64_t nrows, int64_t nnz, const int32_t* __restrict__ rows,
 #pragma unroll
     for (int t = 0; t < kRowptrIpt; ++t) r[t] = e0 + t < nnz ? ldg(rows + e0 + t) : (int32_t)nrows;
   }
-  int64_t prev = e0 == 0 ? -1 : (int64_t)ldg(rows + e0 - 1);
+  // positions past the end read as row nrows, so element nnz closes the
+  // trailing rows (rowptr[nrows] = nnz) and later ones write nothing
+  int32_t prev = e0 == 0 ? -1 : ldg(rows + e0 - 1);
 #pragma unroll
   for (int t = 0; t < kRowptrIpt; ++t) {
-    const int64_t e = e0 + t;
-    if (e > nnz) break;
-    const int64_t hi = e == nnz ? nrows : (int64_t)r[t];
-    for (int64_t q = prev + 1; q <= hi; ++q) rowptr[q] = (int32_t)e;
-    prev = hi;
+    const int32_t cur = r[t];
+    if (cur != prev) {
+      for (int32_t q = prev + 1; q <= cur; ++q) rowptr[q] = (int32_t)(e0 + t);
+      prev = cur;
+    }
   }
 }
 
@@ -130,19 +132,7 @@ struct FillEmit {
 //                     super_tot[tile / kSuper] += tile total
 // kMode 1: fill    (c_pos final)
 // kMode 2: fill + finalise c_pos from the tile-local counts and the tile prefix
-//
-// Optional element-parallel formulation (tiles without duplicate B coordinates): each
-// A element binary-searches its row of B (rank + match flag), an exclusive
-// scan S of the A match flags over the tile gives, per row, how many
-// intersections precede any coordinate, and every output's slot is
-//   A element a (index i in its row):   base + i + rankB(a) - (S[p] - S[row start])
-//   unmatched B element b (index j):    base + j + rankA(b) - (S[A index of rankA] - S[row start])
-// i.e. its position in the row's sorted union, with no per-row sequential
-// merge.  It measured slower than the thread-per-row merge on D4 (its
-// dependent shared-memory chains outweigh the merge's divergence), so the
-// merge is the default.  Tiles whose B row holds a repeated coordinate
-// (non-unique COO) always use the row merge, which groups duplicates exactly
-// as the reference does.
+
 constexpr int kAddRows = 128;
 constexpr int kAddCap = 768;     // staged elements per operand per tile (Poisson(5) tiles: 640 +- 25)
 constexpr int kSuper = 64;       // tiles per super-tile of the two-level prefix
@@ -194,26 +184,6 @@ SL_DEV int block_incl_scan(int v, int* s_warp, int* total) {
   return before + incl;
 }
 
-// row r of the tile holding element e: pos[r] <= e < pos[r + 1] (pos in smem, nr + 1 entries)
-SL_DEV int row_of(const int32_t* pos, int nr, int32_t e) {
-  int lo = 0, hi = nr - 1;
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (pos[mid] <= e) lo = mid; else hi = mid - 1;
-  }
-  return lo;
-}
-
-// first index in [lo, hi) whose column is >= c
-template <typename F>
-SL_DEV int32_t lower_bound_col(int32_t lo, int32_t hi, int32_t c, F&& col) {
-  while (lo < hi) {
-    const int32_t mid = (lo + hi) >> 1;
-    if (col(mid) < c) lo = mid + 1; else hi = mid;
-  }
-  return lo;
-}
-
 // exclusive prefix of all tile totals before `tile` (one warp; lane 0 result)
 SL_DEV int64_t tile_prefix(int64_t tile, const int64_t* tile_tot, const int64_t* super_tot) {
   const int lane = threadIdx.x & 31;
@@ -226,23 +196,22 @@ SL_DEV int64_t tile_prefix(int64_t tile, const int64_t* tile_tot, const int64_t*
   return acc;
 }
 
+// count: 32 registers keep 16 blocks (64 warps) resident; fill: ~90 registers
+// and the output stage allow 5 (the merge is instruction-bound, not occupancy-bound)
 template <int kMode>
-__global__ void __launch_bounds__(kAddRows)
+__global__ void __launch_bounds__(kAddRows, kMode == 0 ? 16 : 1)
 add_tile_kernel(int64_t nrows, const int32_t* __restrict__ a_pos, const int32_t* __restrict__ a_crd,
                 const double* __restrict__ a_vals, const int32_t* __restrict__ b_pos,
                 const int32_t* __restrict__ b_cols, const double* __restrict__ b_vals,
                 int32_t* __restrict__ c_pos, int32_t* __restrict__ c_crd,
                 double* __restrict__ c_vals, int64_t* __restrict__ tile_tot,
-                int64_t* __restrict__ super_tot, bool elem_path) {
+                int64_t* __restrict__ super_tot) {
   constexpr bool kValues = kMode != 0;
   __shared__ int32_t s_apos[kAddRows + 1], s_bpos[kAddRows + 1];
   __shared__ __align__(16) int32_t s_acrd[kAddCap + 8], s_bcol[kAddCap + 8];
   __shared__ __align__(16) double s_aval[kValues ? kAddCap + 4 : 2], s_bval[kValues ? kAddCap + 4 : 2];
-  __shared__ int32_t s_S[kAddCap + 1];          // exclusive scan of A match flags (tile-local)
   __shared__ int32_t s_rbase[kAddRows];         // row output offsets within the tile
-  __shared__ uint8_t s_rowA[kAddCap], s_rowB[kAddCap];   // row (within the tile) of each element
   __shared__ int s_warp[kAddRows / 32];
-  __shared__ int s_dup;
   __shared__ int64_t s_tile_out;
   __shared__ __align__(8) uint64_t bar;
   // output stage (fill modes): the tile's outputs are contiguous in C
@@ -252,7 +221,6 @@ add_tile_kernel(int64_t nrows, const int32_t* __restrict__ a_pos, const int32_t*
   if (tid == 0) {
     mbar_init(&bar, 1);
     fence_mbar_init();
-    s_dup = 0;
   }
   const int64_t tile = blockIdx.x;
   const int64_t r0 = tile * kAddRows;
@@ -297,59 +265,11 @@ add_tile_kernel(int64_t nrows, const int32_t* __restrict__ a_pos, const int32_t*
   const SmemAcc sacc{s_acrd, s_aval, s_bcol, s_bval, (int32_t)ra.lo0, (int32_t)rb.lo0,
                      (int32_t)rav.lo0, (int32_t)rbv.lo0};
   const GlobalAcc gacc{a_crd, a_vals, b_cols, b_vals};
-  auto acol = [&](int32_t p) { return sacc.acol(p); };
-  auto bcol = [&](int32_t p) { return sacc.bcol(p); };
-
-  // ---- element-parallel path (SL_ADD_PATH=elem; the row merge below measured
-  // faster on D4: 97 us vs 154 us fill): row ids, duplicate check, A match
-  // flags, their scan
-  bool fast = fits && elem_path;
-  if (fast) {
-    if (tid < nr) {
-      for (int32_t e = s_apos[tid]; e < s_apos[tid + 1]; ++e) s_rowA[e - ea0] = (uint8_t)tid;
-      for (int32_t e = s_bpos[tid]; e < s_bpos[tid + 1]; ++e) s_rowB[e - eb0] = (uint8_t)tid;
-    }
-    __syncthreads();
-    int dup = 0;
-#pragma unroll 4
-    for (int q = tid + 1; q < nb; q += kAddRows)      // a repeated B coordinate in one row?
-      dup |= (bcol(eb0 + q) == bcol(eb0 + q - 1)) & (s_rowB[q] == s_rowB[q - 1]);
-    if (dup) s_dup = 1;
-    // A match flags, scanned over contiguous per-thread chunks of the tile's A range
-    const int per = (na + kAddRows - 1) / kAddRows;
-    const int c0 = min(na, tid * per), c1 = min(na, c0 + per);
-    int local = 0;
-#pragma unroll 4
-    for (int q = c0; q < c1; ++q) {
-      const int32_t e = ea0 + q;
-      const int r = s_rowA[q];
-      const int32_t a = acol(e), bl = s_bpos[r], bh = s_bpos[r + 1];
-      const int32_t k = lower_bound_col(bl, bh, a, bcol);
-      const int m = (k < bh && bcol(k) == a) ? 1 : 0;
-      s_S[q] = m;                                     // flag for now
-      local += m;
-    }
-    int total;
-    const int incl = block_incl_scan(local, s_warp, &total);
-    int run = incl - local;
-    for (int q = c0; q < c1; ++q) {
-      const int m = s_S[q];
-      s_S[q] = run;
-      run += m;
-    }
-    if (tid == 0) s_S[na] = total;
-    __syncthreads();
-    fast = s_dup == 0;                                 // block-uniform
-  }
-
   // ---- per-row counts (count mode) / row bases (fill modes)
   if (kMode == 0) {
     int cnt = 0;
     if (mine) {
-      if (fast) {
-        const int32_t alo = s_apos[tid], ahi = s_apos[tid + 1];
-        cnt = (ahi - alo) + (s_bpos[tid + 1] - s_bpos[tid]) - (s_S[ahi - ea0] - s_S[alo - ea0]);
-      } else if (fits) {
+      if (fits) {
         cnt = merge_row<false>(s_apos[tid], s_apos[tid + 1], s_bpos[tid], s_bpos[tid + 1], sacc,
                                NoEmit{});
       } else {
@@ -392,31 +312,7 @@ add_tile_kernel(int64_t nrows, const int32_t* __restrict__ a_pos, const int32_t*
   const bool staged_out = n_out <= 2 * kAddCap;
   int32_t* oc = staged_out ? s_ccrd : c_crd + tile_out;
   double* ov = staged_out ? s_cval : c_vals + tile_out;
-  if (fast) {
-#pragma unroll 4
-    for (int q = tid; q < na; q += kAddRows) {        // A elements
-      const int32_t e = ea0 + q;
-      const int r = s_rowA[q];
-      const int32_t a = acol(e), alo = s_apos[r], bl = s_bpos[r], bh = s_bpos[r + 1];
-      const int32_t k = lower_bound_col(bl, bh, a, bcol);
-      const bool m = k < bh && bcol(k) == a;
-      const int32_t slot = s_rbase[r] + (e - alo) + (k - bl) - (s_S[q] - s_S[alo - ea0]);
-      const double v = m ? dadd(sacc.aval(e), sacc.bval(k)) : sacc.aval(e);
-      oc[slot] = a;
-      ov[slot] = dadd(0.0, v);
-    }
-#pragma unroll 4
-    for (int q = tid; q < nb; q += kAddRows) {        // B elements not matched in A
-      const int32_t e = eb0 + q;
-      const int r = s_rowB[q];
-      const int32_t b = bcol(e), alo = s_apos[r], ahi = s_apos[r + 1], bl = s_bpos[r];
-      const int32_t k = lower_bound_col(alo, ahi, b, acol);
-      if (k < ahi && acol(k) == b) continue;
-      const int32_t slot = s_rbase[r] + (e - bl) + (k - alo) - (s_S[k - ea0] - s_S[alo - ea0]);
-      oc[slot] = b;
-      ov[slot] = dadd(0.0, sacc.bval(e));
-    }
-  } else if (mine) {
+  if (mine) {
     const int32_t lo = s_rbase[tid];
     if (fits)
       merge_row<true>(s_apos[tid], s_apos[tid + 1], s_bpos[tid], s_bpos[tid + 1], sacc,
@@ -469,11 +365,6 @@ extern "C" size_t sl_add_csr_workspace_bytes(int64_t nrows, int64_t b_nnz) {
          256;
 }
 
-static bool add_elem_path() {
-  const char* e = getenv("SL_ADD_PATH");
-  return e && e[0] == 'e';
-}
-
 struct AddWs {
   int64_t* tiles;
   int64_t* supers;
@@ -486,12 +377,16 @@ static AddWs add_ws(void* ws, int64_t nrows) {
                reinterpret_cast<int32_t*>(p + add_tiles_bytes(nrows) + add_super_bytes(nrows))};
 }
 
+void sl_host::launch_coo_rowptr(int64_t nrows, int64_t nnz, const int32_t* rows,
+                                int32_t* rowptr, cudaStream_t s) {
+  coo_rowptr_kernel<<<ceil_div(ceil_div(nnz + 1, kRowptrIpt), 256), 256, 0, s>>>(nrows, nnz, rows,
+                                                                               rowptr);
+}
+
 static const int32_t* add_rowptr(int64_t nrows, int64_t b_nnz, const int32_t* b_pos,
                                  const int32_t* b_rows, const AddWs& w, bool build, cudaStream_t s) {
   if (b_pos) return b_pos;
-  if (build)
-    coo_rowptr_kernel<<<ceil_div(ceil_div(b_nnz + 1, kRowptrIpt), 256), 256, 0, s>>>(nrows, b_nnz,
-                                                                                     b_rows, w.rowptr);
+  if (build) sl_host::launch_coo_rowptr(nrows, b_nnz, b_rows, w.rowptr, s);
   return w.rowptr;
 }
 
@@ -513,7 +408,7 @@ static const int32_t* add_count_pass(int64_t nrows, const int32_t* a_pos, const 
   const int32_t* bp = add_rowptr(nrows, b_nnz, b_pos, b_rows, w, true, s);
   add_tile_kernel<0><<<(int)add_ntiles(nrows), kAddRows, 0, s>>>(
       nrows, a_pos, a_crd, nullptr, bp, b_cols, nullptr, c_pos, nullptr, nullptr, w.tiles,
-      w.supers, add_elem_path());
+      w.supers);
   return bp;
 }
 
@@ -547,7 +442,7 @@ extern "C" int sl_add_csr_fill(int64_t nrows, const int32_t* a_pos, const int32_
   const int32_t* bp = add_rowptr(nrows, b_nnz, b_pos, b_rows, w, false, s);
   add_tile_kernel<1><<<(int)add_ntiles(nrows), kAddRows, 0, s>>>(
       nrows, a_pos, a_crd, a_vals, bp, b_cols, b_vals, const_cast<int32_t*>(c_pos), c_crd, c_vals,
-      w.tiles, w.supers, add_elem_path());
+      w.tiles, w.supers);
   return sl_host::launch_status();
 }
 
@@ -564,7 +459,6 @@ extern "C" int sl_add_csr_f64(int64_t nrows, const int32_t* a_pos, const int32_t
   const AddWs w = add_ws(ws, nrows);
   const int32_t* bp = add_count_pass(nrows, a_pos, a_crd, b_nnz, b_pos, b_rows, b_cols, c_pos, w, s);
   add_tile_kernel<2><<<(int)add_ntiles(nrows), kAddRows, 0, s>>>(
-      nrows, a_pos, a_crd, a_vals, bp, b_cols, b_vals, c_pos, c_crd, c_vals, w.tiles, w.supers,
-      add_elem_path());
+      nrows, a_pos, a_crd, a_vals, bp, b_cols, b_vals, c_pos, c_crd, c_vals, w.tiles, w.supers);
   return sl_host::launch_status();
 }

@@ -98,6 +98,8 @@ int launch_coo_pipe(int64_t nrows, int64_t nnz, const int32_t* rows, const int32
                     const double* vals, const double* x, double* y, cudaStream_t s);
 int launch_csr_pipe(int64_t nrows, const int32_t* pos, const int32_t* crd, const double* vals,
                     const double* x, double* y, cudaStream_t s);
+void launch_coo_rowptr(int64_t nrows, int64_t nnz, const int32_t* rows, int32_t* rowptr,
+                       cudaStream_t s);       // add.cu: row pointer of a row-sorted COO
 int sm_count();                              // cached per current device
 inline int ceil_div(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
 int launch_status();                         // SL_OK or SL_ERR_CUDA after a launch

@@ -21,22 +21,6 @@
 
 namespace sl {
 
-__global__ void coo_rowptr_kernel2(int64_t nrows, int64_t nnz, const int32_t* __restrict__ rows,
-                                   int32_t* __restrict__ rowptr) {
-  constexpr int kIpt = 8;
-  const int64_t e0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * kIpt;
-  if (e0 > nnz) return;
-  int64_t prev = e0 == 0 ? -1 : (int64_t)ldg(rows + e0 - 1);
-#pragma unroll
-  for (int t = 0; t < kIpt; ++t) {
-    const int64_t e = e0 + t;
-    if (e > nnz) break;
-    const int64_t hi = e == nnz ? nrows : (int64_t)ldg(rows + e);
-    for (int64_t q = prev + 1; q <= hi; ++q) rowptr[q] = (int32_t)e;
-    prev = hi;
-  }
-}
-
 // row lengths' maximum (ELL slot count)
 __global__ void csr_max_row_kernel(int64_t nrows, const int32_t* __restrict__ pos,
                                    const double* __restrict__ vals, int32_t* __restrict__ out) {
@@ -149,8 +133,7 @@ extern "C" int sl_convert_coo_to_csr(int64_t nrows, int64_t nnz, const int32_t* 
   if (nrows < 0 || nnz < 0) return SL_ERR_INVALID;
   if (nrows > INT32_MAX || nnz > INT32_MAX) return SL_ERR_RANGE;
   if (!pos || (nnz > 0 && !rows)) return SL_ERR_INVALID;
-  coo_rowptr_kernel2<<<ceil_div(ceil_div(nnz + 1, 8), 256), 256, 0, as_stream(stream)>>>(
-      nrows, nnz, rows, pos);
+  sl_host::launch_coo_rowptr(nrows, nnz, rows, pos, as_stream(stream));
   return sl_host::launch_status();
 }
 

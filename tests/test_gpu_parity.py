@@ -250,6 +250,41 @@ def test_add_vs_oracle(orc, n, nnz, seed, two_pass):
     assert np.array_equal(bits(vals), bits(rv))
 
 
+@pytest.mark.parametrize("two_pass", [False, True])
+@pytest.mark.parametrize("seed", [5, 6])
+def test_add_duplicates_zeros_vs_oracle(orc, two_pass, seed):
+    """B with repeated coordinates (grouped sums), explicit and signed zeros,
+    rows of every length including ones past the stage capacity."""
+    rng = np.random.default_rng(seed)
+    n, m = 5000, 64
+    la = rng.poisson(6, n)
+    la[rng.integers(0, n, 3)] = 60                  # a few long rows
+    a_pos = np.zeros(n + 1, np.int64)
+    np.cumsum(np.minimum(la, m), out=a_pos[1:])
+    a_crd = np.concatenate([np.sort(rng.choice(m, size=k, replace=False)) for k in np.diff(a_pos)])
+    a_vals = rng.uniform(-1, 1, len(a_crd))
+    a_vals[rng.random(len(a_vals)) < 0.05] = -0.0
+    nb = 40000
+    b_rows = np.sort(rng.integers(0, n, nb))
+    b_rows[:3000] = 17                                # one row far past the capacity
+    b_rows = np.sort(b_rows)
+    b_cols = rng.integers(0, m, nb)
+    o = np.lexsort((b_cols, b_rows))
+    b_rows, b_cols = b_rows[o], b_cols[o]
+    b_vals = rng.uniform(-1, 1, nb)
+    b_vals[rng.random(nb) < 0.05] = 0.0
+    b_vals[rng.random(nb) < 0.05] = -0.0
+    a_pos = a_pos.astype(np.int32)
+    rp, rc, rv = orc.add_csr(n, a_pos, a_crd.astype(np.int32), a_vals, b_cols.astype(np.int32),
+                             b_vals, b_rows=b_rows.astype(np.int32))
+    pos, crd, vals = K.add_csr(n, cuda(a_pos), cuda(a_crd, np.int32), cuda(a_vals),
+                               cuda(b_cols, np.int32), cuda(b_vals),
+                               b_rows=cuda(b_rows, np.int32), two_pass=two_pass)
+    assert np.array_equal(pos.cpu().numpy(), rp)
+    assert np.array_equal(crd.cpu().numpy(), rc)
+    assert np.array_equal(bits(vals), bits(rv))
+
+
 @pytest.mark.slow
 def test_add_full_size(orc):
     d = wl.add_ab()
@@ -365,14 +400,6 @@ def test_mttkrp_scalar_path_matches(orc, monkeypatch):
     for A in (A1, A2):
         ok, err = orc.within_condition(A, ref, absA, RTOL)
         assert ok, err
-
-
-@pytest.mark.parametrize("two_pass", [False, True])
-def test_add_element_parallel_path(golden, orc, monkeypatch, two_pass):
-    """SL_ADD_PATH=elem: element-parallel slots must equal the row merge bit for bit."""
-    monkeypatch.setenv("SL_ADD_PATH", "elem")
-    test_add_goldens(golden, two_pass)
-    test_add_vs_oracle(orc, 100_000, 500_000, 2, two_pass)
 
 
 def test_dia_row_block_shards(orc):

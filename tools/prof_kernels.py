@@ -126,7 +126,7 @@ def main():
                 e1.record()
                 torch.cuda.synchronize()
                 ts.append(e0.elapsed_time(e1))
-            t = float(np.median(ts))
+            t = float(np.mean(ts))
             res.append(f"{t * 1e3:9.2f} us {b / t / 1e6:8.1f} GB/s")
         print(f"{name:12s} flushed: {res[0]}   L2-warm: {res[1]}", flush=True)
 
