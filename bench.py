@@ -336,8 +336,12 @@ def run_formats(torch, K, wl, dev, timer, peak, steps):
     pos = T(wl.coo_to_csr_pos(d["rows"], n))
     h = wl.hash_vector()
     hc, hv = T(h["crd"]), T(h["vals"])
+    hws = torch.empty(int(K.L().sl_spmv_csr_hashx_map_workspace_bytes(m, h["width"])),
+                      dtype=torch.uint8, device=dev)
     tt = timer.run({"coo": lambda: K.spmv_coo(n, m, r, c, v, x, y),
-                    "csr_hashx": lambda: K.spmv_csr_hashx(n, pos, c, v, h["width"], hc, hv, y)},
+                    "csr_hashx": lambda: K.spmv_csr_hashx(n, pos, c, v, h["width"], hc, hv, y),
+                    "csr_hashx_map": lambda: K.spmv_csr_hashx(n, pos, c, v, h["width"], hc, hv, y,
+                                                              n=m, ws=hws)},
                    steps, 3)
     b = bytes_coo(n, m, nnz)
     t = float(np.mean(tt["coo"]))
@@ -347,7 +351,12 @@ def run_formats(torch, K, wl, dev, timer, peak, steps):
     bh = 4 * (n + 1) + 12 * nnz + 8 * n + 12 * h["width"]
     t = float(np.mean(tt["csr_hashx"]))
     res["csr_hashx_H1"] = {"ms": round(t, 5), "GB/s": round(bh / t / 1e6, 1),
-                           "locates/s": round(nnz / t * 1e3, 1), "bytes": bh}
+                           "locates/s": round(nnz / t * 1e3, 1), "bytes": bh,
+                           "path": "per-nonzero warp-cooperative probing"}
+    t = float(np.mean(tt["csr_hashx_map"]))
+    res["csr_hashx_map_H1"] = {"ms": round(t, 5), "GB/s": round(bh / t / 1e6, 1),
+                               "locates/s": round(nnz / t * 1e3, 1), "bytes": bh,
+                               "path": "slot map (one locate per coordinate) + CSR SpMV"}
     # format conversion (formats.convert): the COO -> CSR identity copy, and
     # the structural row pointer alone; the paper's "convert, then CSR SpMV"
     # alternative to COO SpMV costs convert + csr_spmv_D1.

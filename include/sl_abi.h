@@ -131,6 +131,15 @@ int sl_hashed_insert_init(int64_t size, int32_t* crd, void* stream);
 int sl_hashed_insert(int64_t nq, const int32_t* parent_pos, const int32_t* coord,
                      int64_t w, int32_t* crd, int32_t* err_flag, void* stream);
 
+/* Slot map of a hash vector: for every coordinate c < n, the answer of
+ * locate(c) (first slot in probe order holding c with no empty slot before
+ * it), packed (probe distance << 32 | slot) in a u64 at ws[c], ~0 = absent.
+ * Exact for any table contents.  Used when queries outnumber table slots
+ * (one resolution per coordinate instead of one probe sequence per query). */
+size_t sl_hashed_slot_map_workspace_bytes(int64_t n, int64_t w);
+int sl_hashed_slot_map(int64_t n, int64_t w, const int32_t* crd, void* ws, size_t ws_bytes,
+                       void* stream);
+
 /* ---- SpMV  y(i) = A(i,j) * x(j), dense x and y --------------------------
  * COO-SoA (formats.py:132-133): rows/cols = L0/L1 crd, row-major sorted
  * (the compressed(~U) level is ordered).  Replaces run_fused over i(+)j with
@@ -195,6 +204,15 @@ int sl_spmv_csr_hashx_f64(int64_t nrows, const int32_t* pos, const int32_t* crd,
  *          in-place exclusive scan -> c_pos is the final CSR row pointer;
  *   fill:  writes c_crd/c_vals in sorted-union order.
  * nnz_c = c_pos[nrows] (read it back, or size c_crd/c_vals at nnz_a + nnz_b). */
+/* CSR x hash-vector through the slot map (x has dimension n): the same
+ * results as sl_spmv_csr_hashx_f64, one locate per coordinate instead of per
+ * nonzero.  ws: sl_spmv_csr_hashx_map_workspace_bytes(n, w). */
+size_t sl_spmv_csr_hashx_map_workspace_bytes(int64_t n, int64_t w);
+int sl_spmv_csr_hashx_map_f64(int64_t nrows, int64_t n, const int32_t* pos, const int32_t* crd,
+                              const double* vals, int64_t w, const int32_t* x_crd,
+                              const double* x_vals, double* y, void* ws, size_t ws_bytes,
+                              void* stream);
+
 size_t sl_add_csr_workspace_bytes(int64_t nrows, int64_t b_nnz);
 int sl_add_csr_count(int64_t nrows,
                      const int32_t* a_pos, const int32_t* a_crd,

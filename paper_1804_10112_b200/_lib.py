@@ -81,6 +81,11 @@ SIGNATURES = {
                                       ctypes.c_int),
     "sl_convert_coo_to_dia_values": ([_i64, _i64, _i64, _i32, _p, _p, _p, _p, _p, _sz, _p],
                                      ctypes.c_int),
+    "sl_hashed_slot_map_workspace_bytes": ([_i64, _i64], _sz),
+    "sl_hashed_slot_map": ([_i64, _i64, _p, _p, _sz, _p], ctypes.c_int),
+    "sl_spmv_csr_hashx_map_workspace_bytes": ([_i64, _i64], _sz),
+    "sl_spmv_csr_hashx_map_f64": ([_i64, _i64, _p, _p, _p, _i64, _p, _p, _p, _p, _sz, _p],
+                                  ctypes.c_int),
     "sl_l2_flush": ([_p, _sz, _p], ctypes.c_int),
 }
 

@@ -66,9 +66,133 @@ __global__ void hashed_insert_kernel(int64_t nq, const int32_t* __restrict__ par
   atomicExch(err, SL_ERR_HASH_SEGMENT_FULL);
 }
 
+// ---- slot map: the answer of locate(c) for every coordinate c < n ------------
+// For a query stream much longer than the table (CSR x hash-vector: one
+// locate per nonzero, ~10 per stored coordinate), resolving each coordinate
+// once is cheaper than probing per query.  locate(c) returns the first slot s
+// in probe order home(c), home(c)+1, ... holding c, provided no empty slot
+// comes before it; with d = (s - home(c)) mod W and L(s) = the number of
+// occupied slots immediately preceding s (cyclically), s is reachable iff
+// d <= L(s), and the answer is the reachable slot of c with the smallest d.
+// That is exact for any table contents (not only tables built by insert).
+// Map entries pack (d << 32 | s); ~0 = absent.
+constexpr int kMapChunk = 1024;
+
+// per chunk: last empty slot at or before each slot (within the chunk, -1 if
+// none) and the chunk's last empty slot
+__global__ void __launch_bounds__(kMapChunk)
+hash_runs_kernel(int64_t w, const int32_t* __restrict__ crd, int32_t* __restrict__ last_empty,
+                 int32_t* __restrict__ chunk_last) {
+  __shared__ int32_t s_warp[kMapChunk / 32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t s = (int64_t)blockIdx.x * kMapChunk + tid;
+  int32_t v = (s < w && ldg(crd + s) == kEmpty) ? (int32_t)s : -1;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int32_t u = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v = max(v, u);
+  }
+  if (lane == 31) s_warp[warp] = v;
+  __syncthreads();
+  int32_t before = -1;
+  for (int i = 0; i < warp; ++i) before = max(before, s_warp[i]);
+  v = max(v, before);
+  if (s < w) last_empty[s] = v;
+  if (tid == kMapChunk - 1) chunk_last[blockIdx.x] = v;
+}
+
+// exclusive prefix max of the chunk maxima (one block); chunk_pre[nchunks] = overall last empty
+__global__ void __launch_bounds__(1024)
+hash_chunk_scan_kernel(int64_t nchunks, const int32_t* __restrict__ chunk_last,
+                       int32_t* __restrict__ chunk_pre) {
+  __shared__ int32_t s_warp[32];
+  __shared__ int32_t s_carry;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) s_carry = -1;
+  __syncthreads();
+  for (int64_t b0 = 0; b0 < nchunks; b0 += 1024) {
+    const int64_t b = b0 + tid;
+    int32_t incl = b < nchunks ? chunk_last[b] : -1;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int32_t u = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl = max(incl, u);
+    }
+    if (lane == 31) s_warp[warp] = incl;
+    __syncthreads();
+    int32_t before = s_carry;
+    for (int i = 0; i < warp; ++i) before = max(before, s_warp[i]);
+    const int32_t up = __shfl_up_sync(0xffffffffu, incl, 1);
+    const int32_t excl = max(before, lane == 0 ? -1 : up);
+    if (b < nchunks) chunk_pre[b] = excl;
+    __syncthreads();
+    if (tid == 1023) s_carry = max(before, incl);
+    __syncthreads();
+  }
+  if (tid == 0) chunk_pre[nchunks] = s_carry;
+}
+
+__global__ void map_init_kernel(unsigned long long* __restrict__ map, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    map[i] = ~0ull;
+}
+
+__global__ void map_fill_kernel(int64_t w, int64_t n, const int32_t* __restrict__ crd,
+                                const int32_t* __restrict__ last_empty,
+                                const int32_t* __restrict__ chunk_pre,
+                                unsigned long long* __restrict__ map, int64_t nchunks) {
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < w;
+       s += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t c = ldg(crd + s);
+    if (c < 0 || c >= n) continue;
+    const int64_t b = s / kMapChunk;
+    int64_t pe = ldg(chunk_pre + b);                                  // last empty before chunk b
+    if (s > b * kMapChunk) pe = max64(pe, (int64_t)ldg(last_empty + s - 1));
+    int64_t run;                                                      // occupied slots before s
+    if (pe >= 0) {
+      run = s - 1 - pe;
+    } else {
+      const int64_t g = ldg(chunk_pre + nchunks);                     // last empty overall
+      run = g >= 0 ? s - 1 - (g - w) : w - 1;                         // wrap, or no empty slot
+    }
+    int64_t d = s - (int64_t)c % w;
+    if (d < 0) d += w;
+    if (d <= run)
+      atomicMin(map + c, ((unsigned long long)d << 32) | (unsigned long long)(uint32_t)s);
+  }
+}
+
 }  // namespace sl
 
 using namespace sl;
+
+extern "C" size_t sl_hashed_slot_map_workspace_bytes(int64_t n, int64_t w) {
+  const int64_t nchunks = (w + kMapChunk - 1) / kMapChunk;
+  return (size_t)n * 8 + (size_t)w * 4 + (size_t)(2 * nchunks + 1) * 4 + 512;
+}
+
+// Workspace layout: [map u64 x n][last_empty i32 x w][chunk_last x nchunks][chunk_pre x nchunks+1]
+extern "C" int sl_hashed_slot_map(int64_t n, int64_t w, const int32_t* crd, void* ws,
+                                  size_t ws_bytes, void* stream) {
+  if (n < 0 || w <= 0 || !crd) return SL_ERR_INVALID;
+  if (w > INT32_MAX || n > INT32_MAX) return SL_ERR_RANGE;
+  if (!ws || ws_bytes < sl_hashed_slot_map_workspace_bytes(n, w)) return SL_ERR_WORKSPACE;
+  cudaStream_t s = sl_host::as_stream(stream);
+  const int64_t nchunks = (w + kMapChunk - 1) / kMapChunk;
+  char* p = static_cast<char*>(ws);
+  unsigned long long* map = reinterpret_cast<unsigned long long*>(p);
+  int32_t* last_empty = reinterpret_cast<int32_t*>(p + (size_t)n * 8);
+  int32_t* chunk_last = last_empty + w;
+  int32_t* chunk_pre = chunk_last + nchunks;
+  const int sms = sl_host::sm_count();
+  if (n > 0) map_init_kernel<<<min(sl_host::ceil_div(n, 256), 8 * sms), 256, 0, s>>>(map, n);
+  hash_runs_kernel<<<(int)nchunks, kMapChunk, 0, s>>>(w, crd, last_empty, chunk_last);
+  hash_chunk_scan_kernel<<<1, 1024, 0, s>>>(nchunks, chunk_last, chunk_pre);
+  map_fill_kernel<<<min(sl_host::ceil_div(w, 256), 8 * sms), 256, 0, s>>>(
+      w, n, crd, last_empty, chunk_pre, map, nchunks);
+  return sl_host::launch_status();
+}
 
 extern "C" int sl_hashed_locate(int64_t nq, const int32_t* parent_pos, const int32_t* coord,
                                 int64_t w, const int32_t* crd, int32_t* out_pos,

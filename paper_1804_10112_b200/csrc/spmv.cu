@@ -188,17 +188,17 @@ constexpr int kCsrRows = kCsrThreads;
 constexpr int kCsrIpt = 8;
 constexpr int kCsrChunk = kCsrThreads * kCsrIpt;   // 2048 products per staging round
 
-template <bool kHashX>
+template <int kHashX>
 struct XOperand;
 
 template <>
-struct XOperand<false> {            // dense x: locate = parent*n + c (levels.py:268-269)
+struct XOperand<0> {            // dense x: locate = parent*n + c (levels.py:268-269)
   const double* x;
   SL_DEV double term(double a, int32_t c) const { return dmul(a, ldg(x + c)); }
 };
 
 template <>
-struct XOperand<true> {             // hashed x: probe (levels.py:270-280), miss -> no term
+struct XOperand<1> {             // hashed x: probe (levels.py:270-280), miss -> no term
   HashedLevel lv;
   const double* xv;
   // A miss contributes no term.  The row accumulator starts at +0.0 and can
@@ -209,11 +209,31 @@ struct XOperand<true> {             // hashed x: probe (levels.py:270-280), miss
   }
 };
 
+template <>
+struct XOperand<2> {                // hashed x through the slot map (hashed.cu): one
+  HashedLevel lv;                   // resolved locate per coordinate c < n, probing
+  const double* xv;                 // only for coordinates outside the map
+  const unsigned long long* map;
+  int64_t n;
+  SL_DEV int64_t slot(int32_t c) const {
+    if (c < n) {
+      const unsigned long long m = __ldg(map + c);
+      return m == ~0ull ? -1 : (int64_t)(uint32_t)m;
+    }
+    const PosFound pf = lv.locate(0, c);
+    return pf.found ? pf.pos : -1;
+  }
+  SL_DEV double term(double a, int32_t c) const {
+    const int64_t sl = slot(c);
+    return sl >= 0 ? dmul(a, ldg(xv + sl)) : 0.0;
+  }
+};
+
 // Stage products of elements [cs, cs + n) into s_prod with every load of a
 // thread issued before its first use (crd/vals stream, then the x gathers).
 template <int kThreads, int kIpt>
 SL_DEV void stage_products(const int32_t* __restrict__ crd, const double* __restrict__ vals,
-                           int64_t cs, int n, XOperand<false> xop, double* s_prod) {
+                           int64_t cs, int n, XOperand<0> xop, double* s_prod) {
   const int tid = threadIdx.x;
   int32_t c[kIpt];
   double v[kIpt], xv[kIpt];
@@ -243,6 +263,30 @@ SL_DEV void stage_products(const int32_t* __restrict__ crd, const double* __rest
   }
 }
 
+// Mapped hashed x: crd/vals, then the map entries, then x — each batch of
+// loads independent of the next batch's wait.
+template <int kThreads, int kIpt>
+SL_DEV void stage_products(const int32_t* __restrict__ crd, const double* __restrict__ vals,
+                           int64_t cs, int n, XOperand<2> xop, double* s_prod) {
+  const int tid = threadIdx.x;
+  int32_t c[kIpt];
+  double v[kIpt];
+  int64_t sl[kIpt];
+#pragma unroll
+  for (int k = 0; k < kIpt; ++k) {
+    const int q = tid + k * kThreads;
+    c[k] = q < n ? ld_stream(crd + cs + q) : 0;
+    v[k] = q < n ? ld_stream(vals + cs + q) : 0.0;
+  }
+#pragma unroll
+  for (int k = 0; k < kIpt; ++k) sl[k] = tid + k * kThreads < n ? xop.slot(c[k]) : -1;
+#pragma unroll
+  for (int k = 0; k < kIpt; ++k) {
+    const int q = tid + k * kThreads;
+    if (q < n) s_prod[q] = sl[k] >= 0 ? dmul(v[k], ldg(xop.xv + sl[k])) : 0.0;
+  }
+}
+
 // Hashed x: hybrid probing.  Each lane first probes its own element for
 // kHashSolo steps (the whole answer for short probe sequences); elements still
 // unresolved are then finished one at a time by the whole warp, 32
@@ -253,7 +297,7 @@ constexpr int kHashPer = 8;     // probe steps per lane per cooperative round (2
 
 template <int kThreads, int kIpt>
 SL_DEV void stage_products(const int32_t* __restrict__ crd, const double* __restrict__ vals,
-                           int64_t cs, int n, XOperand<true> xop, double* s_prod) {
+                           int64_t cs, int n, XOperand<1> xop, double* s_prod) {
   const int tid = threadIdx.x, lane = tid & 31;
   const HashedLevel& lv = xop.lv;
   const int64_t w = lv.w;
@@ -317,8 +361,8 @@ SL_DEV void stage_products(const int32_t* __restrict__ crd, const double* __rest
   }
 }
 
-template <bool kHashX>
-__global__ void __launch_bounds__(kCsrThreads, kHashX ? 4 : 8)
+template <int kHashX>
+__global__ void __launch_bounds__(kCsrThreads, kHashX == 1 ? 4 : 8)
 spmv_csr_rowblock_kernel(int64_t nrows, const int32_t* __restrict__ pos,
                          const int32_t* __restrict__ crd, const double* __restrict__ vals,
                          XOperand<kHashX> xop, double* __restrict__ y) {
@@ -398,7 +442,7 @@ spmv_csr_warp_kernel(int64_t nrows, const int32_t* __restrict__ pos, const int32
 // K2b: CSR vector-per-row.  One warp per row: lanes load 32 nonzeros at a time
 // coalesced, then the products are shuffled to every lane in order and added
 // sequentially (the same order as the reference).  Best for long rows.
-template <bool kHashX>
+template <int kHashX>
 __global__ void __launch_bounds__(256)
 spmv_csr_vector_kernel(int64_t nrows, const int32_t* __restrict__ pos,
                        const int32_t* __restrict__ crd, const double* __restrict__ vals,
@@ -449,7 +493,7 @@ __global__ void csr_merge_partition_kernel(const int32_t* __restrict__ pos, int6
   part[t] = row;
 }
 
-template <bool kHashX>
+template <int kHashX>
 __global__ void __launch_bounds__(kMpThreads)
 spmv_csr_merge_kernel(int64_t nrows, const int32_t* __restrict__ pos,
                       const int32_t* __restrict__ crd, const double* __restrict__ vals,
@@ -601,18 +645,18 @@ extern "C" size_t sl_spmv_csr_workspace_bytes(int64_t nrows, int64_t nnz, int32_
   return (size_t)(ntiles + 1) * sizeof(int64_t);
 }
 
-template <bool kHashX>
+template <int kHashX>
 static int launch_csr(int64_t nrows, const int32_t* pos, const int32_t* crd, const double* vals,
                       XOperand<kHashX> xop, double* y, int32_t variant, void* ws,
                       size_t ws_bytes, cudaStream_t s) {
   if (variant == 0 && !kHashX && aligned16(crd) && aligned16(vals) && spmv_path() == 2) {
-    const double* xd = reinterpret_cast<const XOperand<false>&>(xop).x;
+    const double* xd = reinterpret_cast<const XOperand<0>&>(xop).x;
     return sl_host::launch_csr_pipe(nrows, pos, crd, vals, xd, y, s);
   } else if (variant == 0) {
     spmv_csr_rowblock_kernel<kHashX><<<ceil_div(nrows, kCsrRows), kCsrThreads, 0, s>>>(
         nrows, pos, crd, vals, xop, y);
   } else if (variant == 3 && !kHashX) {
-    const double* xd = reinterpret_cast<const XOperand<false>&>(xop).x;
+    const double* xd = reinterpret_cast<const XOperand<0>&>(xop).x;
     spmv_csr_warp_kernel<<<ceil_div(nrows, 256), 256, 0, s>>>(nrows, pos, crd, vals, xd, y);
   } else if (variant == 1) {
     spmv_csr_vector_kernel<kHashX><<<ceil_div(nrows * 32, 256), 256, 0, s>>>(nrows, pos, crd,
@@ -636,18 +680,18 @@ extern "C" int sl_spmv_csr_f64(int64_t nrows, int64_t ncols, int64_t nnz, const 
   if (nrows == 0) return SL_OK;
   if (!pos || !y || !x) return SL_ERR_INVALID;
   cudaStream_t s = as_stream(stream);
-  XOperand<false> xop{x};
+  XOperand<0> xop{x};
   if (variant == 2) {
     const int64_t ntiles = (nrows + nnz + kMpItems - 1) / kMpItems;
     if (!ws || ws_bytes < sl_spmv_csr_workspace_bytes(nrows, nnz, 2)) return SL_ERR_WORKSPACE;
     int64_t* part = static_cast<int64_t*>(ws);
     csr_merge_partition_kernel<<<ceil_div(ntiles + 1, 256), 256, 0, s>>>(pos, nrows, nnz, ntiles,
                                                                        part);
-    spmv_csr_merge_kernel<false><<<(int)ntiles, kMpThreads, 0, s>>>(nrows, pos, crd, vals, xop,
+    spmv_csr_merge_kernel<0><<<(int)ntiles, kMpThreads, 0, s>>>(nrows, pos, crd, vals, xop,
                                                                    part, y);
     return sl_host::launch_status();
   }
-  return launch_csr<false>(nrows, pos, crd, vals, xop, y, variant, ws, ws_bytes, s);
+  return launch_csr<0>(nrows, pos, crd, vals, xop, y, variant, ws, ws_bytes, s);
 }
 
 extern "C" int sl_spmv_csr_hashx_f64(int64_t nrows, const int32_t* pos, const int32_t* crd,
@@ -657,8 +701,26 @@ extern "C" int sl_spmv_csr_hashx_f64(int64_t nrows, const int32_t* pos, const in
   if (nrows > INT32_MAX || w > INT32_MAX) return SL_ERR_RANGE;
   if (nrows == 0) return SL_OK;
   if (!pos || !y || !x_crd || !x_vals) return SL_ERR_INVALID;
-  XOperand<true> xop{HashedLevel{x_crd, w}, x_vals};
-  return launch_csr<true>(nrows, pos, crd, vals, xop, y, 0, nullptr, 0, as_stream(stream));
+  XOperand<1> xop{HashedLevel{x_crd, w}, x_vals};
+  return launch_csr<1>(nrows, pos, crd, vals, xop, y, 0, nullptr, 0, as_stream(stream));
+}
+
+extern "C" size_t sl_spmv_csr_hashx_map_workspace_bytes(int64_t n, int64_t w) {
+  return sl_hashed_slot_map_workspace_bytes(n, w);
+}
+
+extern "C" int sl_spmv_csr_hashx_map_f64(int64_t nrows, int64_t n, const int32_t* pos,
+                                         const int32_t* crd, const double* vals, int64_t w,
+                                         const int32_t* x_crd, const double* x_vals, double* y,
+                                         void* ws, size_t ws_bytes, void* stream) {
+  if (nrows < 0 || n < 0 || w <= 0) return SL_ERR_INVALID;
+  if (nrows > INT32_MAX || w > INT32_MAX || n > INT32_MAX) return SL_ERR_RANGE;
+  if (nrows == 0) return SL_OK;
+  if (!pos || !y || !x_crd || !x_vals) return SL_ERR_INVALID;
+  const int st = sl_hashed_slot_map(n, w, x_crd, ws, ws_bytes, stream);
+  if (st != SL_OK) return st;
+  XOperand<2> xop{HashedLevel{x_crd, w}, x_vals, static_cast<const unsigned long long*>(ws), n};
+  return launch_csr<2>(nrows, pos, crd, vals, xop, y, 0, nullptr, 0, as_stream(stream));
 }
 
 extern "C" int sl_spmv_ell_f64(int64_t nrows, int64_t ncols, int32_t nslots, const int32_t* crd,

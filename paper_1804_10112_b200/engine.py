@@ -226,8 +226,11 @@ def _run(p: Plan, inputs: Dict[str, TensorStorage], stats: Optional[EvalStats]):
                 max(0, min(nrows, ncols - o) - max(0, -o)) for o in offs.tolist()))}
         else:  # spmv_csr_hashx
             hx = x.levels[0]
+            nq = int(A.levels[1].crd.numel())
+            # queries >= table slots: resolve each coordinate once (slot map)
+            n_map = int(x.dims[0]) if nq >= hx.w else None
             y = K.spmv_csr_hashx(nrows, A.levels[1].pos, A.levels[1].crd, A.vals, hx.w, hx.crd,
-                                 x.vals)
+                                 x.vals, n=n_map)
             visits = {"i": nrows, "j": int(A.levels[1].crd.numel())}
         out = TensorStorage(p.out_format, (nrows,),
                             [LevelStorage(p.out_format.levels[0], n=nrows, device=dev)], y)

@@ -99,13 +99,34 @@ def spmv_dia(nrows, ncols, offsets, vals, x, y=None, row0=0):
     return y
 
 
-def spmv_csr_hashx(nrows, pos, crd, vals, w, x_crd, x_vals, y=None):
+def spmv_csr_hashx(nrows, pos, crd, vals, w, x_crd, x_vals, y=None, n=None, ws=None):
+    """CSR x hash-vector.  With the vector's dimension `n`, the slot-map path
+    (sl_spmv_csr_hashx_map_f64: one locate per coordinate) runs; without it,
+    every nonzero probes the table (sl_spmv_csr_hashx_f64).  Same results."""
     pos, crd, vals = _t(pos, I32, "pos"), _t(crd, I32, "crd"), _t(vals, F64, "vals")
     x_crd, x_vals = _t(x_crd, I32, "x_crd"), _t(x_vals, F64, "x_vals")
     y = _out(y, nrows, F64, vals, "y")
-    _lib.check(L().sl_spmv_csr_hashx_f64(nrows, P(pos), P(crd), P(vals), w, P(x_crd), P(x_vals),
-                                         P(y), S()), "spmv_csr_hashx")
+    if n is None:
+        _lib.check(L().sl_spmv_csr_hashx_f64(nrows, P(pos), P(crd), P(vals), w, P(x_crd),
+                                             P(x_vals), P(y), S()), "spmv_csr_hashx")
+        return y
+    need = L().sl_spmv_csr_hashx_map_workspace_bytes(n, w)
+    if ws is None or ws.numel() < need:
+        ws = _ws(need, vals)
+    _lib.check(L().sl_spmv_csr_hashx_map_f64(nrows, n, P(pos), P(crd), P(vals), w, P(x_crd),
+                                             P(x_vals), P(y), P(ws), ws.numel(), S()),
+               "spmv_csr_hashx_map")
     return y
+
+
+def hashed_slot_map(n, w, crd, ws=None):
+    """u64 per coordinate c < n: (probe distance << 32 | slot) of locate(c), ~0 absent."""
+    crd = _t(crd, I32, "crd")
+    need = L().sl_hashed_slot_map_workspace_bytes(n, w)
+    if ws is None or ws.numel() < need:
+        ws = _ws(need, crd)
+    _lib.check(L().sl_hashed_slot_map(n, w, P(crd), P(ws), ws.numel(), S()), "hashed_slot_map")
+    return ws[:8 * n].view(torch.int64)
 
 
 # ---- hashed level -------------------------------------------------------------

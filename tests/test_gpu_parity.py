@@ -65,6 +65,11 @@ def test_spmv_goldens_all_formats(golden):
                                  int(c["hash_w"]), cuda(c["hash_crd"], np.int32),
                                  cuda(c["hash_vals"], np.float64))
             assert np.array_equal(bits(y), bits(c["hash_y"])), name
+            y = K.spmv_csr_hashx(nrows, cuda(c["csr_pos"], np.int32),          # slot-map path
+                                 cuda(c["csr_crd"], np.int32), cuda(c["csr_vals"], np.float64),
+                                 int(c["hash_w"]), cuda(c["hash_crd"], np.int32),
+                                 cuda(c["hash_vals"], np.float64), n=ncols)
+            assert np.array_equal(bits(y), bits(c["hash_y"])), name
 
 
 # ---------------------------------------------------------------------------
@@ -216,6 +221,42 @@ def test_spmv_hashx_full_h1(orc):
     y = K.spmv_csr_hashx(d["nrows"], cuda(pos), cuda(d["cols"]), cuda(d["vals"]), h["width"],
                          cuda(h["crd"]), cuda(h["vals"]))
     assert np.array_equal(bits(y), bits(ref))
+    y = K.spmv_csr_hashx(d["nrows"], cuda(pos), cuda(d["cols"]), cuda(d["vals"]), h["width"],
+                         cuda(h["crd"]), cuda(h["vals"]), n=d["ncols"])
+    assert np.array_equal(bits(y), bits(ref))
+
+
+def _map_vs_oracle(orc, crd, w, n, sample=None):
+    m = K.hashed_slot_map(n, w, cuda(crd, np.int32)).cpu().numpy().view(np.uint64)
+    q = np.arange(n, dtype=np.int32)
+    if sample is not None:      # every stored coordinate plus a sample of the rest
+        crd_a = np.asarray(crd)
+        rng = np.random.default_rng(n)
+        stored = crd_a[(crd_a >= 0) & (crd_a < n)]
+        q = np.unique(np.concatenate([rng.choice(stored, min(sample, len(stored)), replace=False),
+                                      rng.integers(0, n, sample)])).astype(np.int32)
+        m = m[q]
+    rp, rf = orc.hashed_locate(q, w, np.asarray(crd, np.int32))
+    found = m != np.uint64(0xFFFFFFFFFFFFFFFF)
+    assert np.array_equal(found, rf)
+    assert np.array_equal((m[found] & np.uint64(0xFFFFFFFF)).astype(np.int64), rp[rf].astype(np.int64))
+
+
+def test_hashed_slot_map_vs_probing(orc):
+    """The slot map (one resolution per coordinate) equals per-query probing
+    for tables built by insertion and for arbitrary contents: empty slots
+    cutting probe paths, duplicates, a full table, wrap-around, one-slot tables."""
+    h = wl.hash_vector()
+    _map_vs_oracle(orc, h["crd"], h["width"], h["n"], sample=1500)
+    h = wl.hash_vector(n=300_000, m=120_000, width=131_072, seed=9)
+    _map_vs_oracle(orc, h["crd"], h["width"], h["n"], sample=1500)
+    rng = np.random.default_rng(3)
+    for w in (1, 2, 7, 1000, 5000):
+        for fill in (0.0, 0.5, 0.9, 1.0):
+            crd = np.where(rng.random(w) < fill, rng.integers(0, 3 * w + 1, w), -1).astype(np.int32)
+            _map_vs_oracle(orc, crd, w, 3 * w + 2)
+    crd = np.array([5, 5, -1, 5, 9, 1, 1, -1], np.int32)       # duplicates, gaps
+    _map_vs_oracle(orc, crd, 8, 12)
 
 
 # ---------------------------------------------------------------------------

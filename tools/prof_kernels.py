@@ -49,6 +49,11 @@ def main():
             hc, hv = T(h["crd"]), T(h["vals"])
             jobs[tag] = (4 * (n + 1) + 12 * len(d["rows"]) + 8 * n + 12 * w,
                          lambda hc=hc, hv=hv, w=w: K.spmv_csr_hashx(n, pos, c, v, w, hc, hv, y))
+            hws = torch.empty(int(K.L().sl_spmv_csr_hashx_map_workspace_bytes(m, w)),
+                              dtype=torch.uint8, device=dev)
+            jobs[tag + "_map"] = (4 * (n + 1) + 12 * len(d["rows"]) + 8 * n + 12 * w,
+                                  lambda hc=hc, hv=hv, w=w, hws=hws: K.spmv_csr_hashx(
+                                      n, pos, c, v, w, hc, hv, y, n=m, ws=hws))
 
     def d2():
         s = wl.stencil27()
@@ -95,7 +100,8 @@ def main():
         jobs["mttkrp_csf"] = (532_669_912, lambda: K.mttkrp_csf(I, J, Kd, c0, p1, c1, p2, c2, tv,
                                                                 Bt, Ct, A, ws))
 
-    if want("coo") or want("hashx") or want("hashx_wdef") or want("csr_d1"):
+    if (want("coo") or want("hashx") or want("hashx_wdef") or want("csr_d1")
+            or want("hashx_map") or want("hashx_wdef_map")):
         d1()
     if want("csr") or want("ell") or want("csr_vec") or want("csr_merge") or want("csr_warp"):
         d2()
