@@ -54,6 +54,15 @@ def measured_peak():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
+def l2_calib():
+    """Measured L2 -> SM ceilings (tools/calib_l2.py on this pool's B200)."""
+    p = ROOT / "profiles" / "l2_calib.json"
+    try:
+        return json.loads(p.read_text())
+    except Exception:
+        return {}
+
+
 def ncu_traffic():
     p = ROOT / "profiles" / "ncu_traffic.json"
     try:
@@ -345,9 +354,13 @@ def run_formats(torch, K, wl, dev, timer, peak, steps):
                    steps, 3)
     b = bytes_coo(n, m, nnz)
     t = float(np.mean(tt["coo"]))
+    g8 = l2_calib().get("gather8_G_per_s")
     res["coo_spmv_D1"] = {"ms": round(t, 5), "GB/s": round(b / t / 1e6, 1),
                           "frac": round(b / t / 1e6 / peak, 4), "nnz/s": round(nnz / t * 1e3, 1),
-                          "bytes": b}
+                          "bytes": b,
+                          "gather_ceiling": {"x_gathers": nnz, "peak_G_per_s": g8,
+                                             "floor_ms": round(nnz / g8 / 1e6, 5) if g8 else None,
+                                             "note": "random 8-B x gathers, tools/calib_l2.py"}}
     bh = 4 * (n + 1) + 12 * nnz + 8 * n + 12 * h["width"]
     t = float(np.mean(tt["csr_hashx"]))
     res["csr_hashx_H1"] = {"ms": round(t, 5), "GB/s": round(bh / t / 1e6, 1),
@@ -422,12 +435,25 @@ def run_formats(torch, K, wl, dev, timer, peak, steps):
     b_coo = 20 * nnz + bf
     n1 = len(csf["crd1"])
     b_csf = 8 + 4 * len(csf["crd0"]) + 4 * (len(csf["crd0"]) + 1) + 4 * n1 + 4 * (n1 + 1) + 12 * nnz + bf
+    # L2 -> SM bytes the loop nest must move at minimum: a C row per nonzero and
+    # a B row per (i, j) fiber (factors are L2-resident, L1 far smaller), plus
+    # the streamed tensor and the A rows — the resource that bounds MTTKRP.
+    l2c = l2_calib()
+    l2_peak = l2c.get("gather256_GBs")
+    l2_rows = 8 * R * (nnz + n1) + 8 * I * R
     for name, b, key in (("mttkrp_coo3_D5", b_coo, "coo3"), ("mttkrp_csf_D5", b_csf, "csf")):
         t = float(np.mean(tt[key]))
+        l2b = l2_rows + (b - bf)
         res[name] = {"ms": round(t, 4), "nnz/s": round(nnz / t * 1e3, 1),
                      "nnz*R/s": round(nnz * R / t * 1e3, 1), "GB/s": round(b / t / 1e6, 1),
                      "frac": round(b / t / 1e6 / peak, 4), "GFLOP/s": round(3 * nnz * R / t / 1e6, 1),
-                     "bytes": b}
+                     "bytes": b,
+                     "l2_roofline": {"bound": "l2 (factor-row gathers)", "bytes": l2b,
+                                     "achieved_GBs": round(l2b / t / 1e6, 1),
+                                     "peak_GBs": l2_peak,
+                                     "peak_source": "profiles/l2_calib.json gather256_GBs "
+                                                    "(tools/calib_l2.py, 256-B random rows)",
+                                     "frac": round(l2b / t / 1e6 / l2_peak, 4) if l2_peak else None}}
     return res
 
 
