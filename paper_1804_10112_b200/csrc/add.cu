@@ -32,7 +32,6 @@
 
 namespace sl {
 
-constexpr int kAddThreads = 256;
 
 // ---- pass 0: row pointer of a row-sorted COO level ---------------------------
 constexpr int kRowptrIpt = 8;   // elements per thread (two 16-byte loads when aligned)
