@@ -104,6 +104,7 @@ def load(path: Path = LIB_PATH):
     global _LIB
     if _LIB is None:
         # SL_LIB_PATH: load another build of the same ABI (A/B timing of two builds)
+        override = "SL_LIB_PATH" in os.environ
         path = Path(os.environ.get("SL_LIB_PATH", str(path)))
         if not path.exists():
             raise E.DeviceError(
@@ -111,7 +112,11 @@ def load(path: Path = LIB_PATH):
                 "(there is no CPU fallback)")
         L = ctypes.CDLL(str(path))
         for name, (args, res) in SIGNATURES.items():
-            fn = getattr(L, name)
+            fn = getattr(L, name, None)
+            if fn is None and override:   # an older build under A/B: bind what it has
+                continue
+            if fn is None:
+                raise E.DeviceError(f"{path} does not export {name}: rebuild the library")
             fn.argtypes = args
             fn.restype = res
         _LIB = L

@@ -113,6 +113,52 @@ SL_DEV int merge_row(int32_t alo, int32_t ahi, int32_t blo, int32_t bhi, const A
   return n;
 }
 
+// The same merge over the tile's shared-memory stage, written for SIMT: both
+// operands' next values are read unconditionally (indices stay inside the
+// stage) and selected, so the loop body has no divergent branch except the
+// rare duplicate-B group.  ac/av/bc/bv are indexed by global element number.
+template <bool kValues>
+SL_DEV int merge_row_smem(int32_t pa, int32_t ahi, int32_t pb, int32_t bhi,
+                          const int32_t* ac, const double* av, const int32_t* bc,
+                          const double* bv, int32_t* oc, double* ov) {
+  int n = 0;
+  int32_t ca = pa < ahi ? ac[pa] : INT32_MAX;
+  int32_t cb = pb < bhi ? bc[pb] : INT32_MAX;
+  while (pa < ahi || pb < bhi) {
+    const int32_t c = ca < cb ? ca : cb;
+    const bool ha = ca == c, hb = cb == c;
+    int32_t pb1 = pb + 1;
+    int32_t cb1 = pb1 < bhi ? bc[pb1] : INT32_MAX;
+    if (kValues) {
+      const double a = av[pa];
+      double b = bv[pb];
+      if (hb && cb1 == c) {           // duplicate B coordinates: Python sum over the group
+        b = dadd(0.0, b);
+        do {
+          b = dadd(b, bv[pb1]);
+          ++pb1;
+          cb1 = pb1 < bhi ? bc[pb1] : INT32_MAX;
+        } while (cb1 == c);
+      }
+      const double e = ha ? (hb ? dadd(a, b) : a) : b;
+      oc[n] = c;
+      ov[n] = dadd(0.0, e);
+    } else if (hb && cb1 == c) {
+      do {
+        ++pb1;
+        cb1 = pb1 < bhi ? bc[pb1] : INT32_MAX;
+      } while (cb1 == c);
+    }
+    pa += ha;
+    const int32_t na_ = ac[pa];
+    ca = ha ? (pa < ahi ? na_ : INT32_MAX) : ca;
+    pb = hb ? pb1 : pb;
+    cb = hb ? cb1 : cb;
+    ++n;
+  }
+  return n;
+}
+
 struct NoEmit {
   SL_DEV void operator()(int, int32_t, double) const {}
 };
@@ -251,11 +297,11 @@ add_tile_kernel(int64_t nrows, const int32_t* __restrict__ a_pos, const int32_t*
         issue_range(b_vals, rbv, s_bval, &bar);
       }
     }
-    edge_loads(a_crd, ra, ea0, ea1, s_acrd, tid, kAddRows);
-    edge_loads(b_cols, rb, eb0, eb1, s_bcol, tid, kAddRows);
+    edge_loads_small(a_crd, ra, ea0, ea1, s_acrd, tid);
+    edge_loads_small(b_cols, rb, eb0, eb1, s_bcol, tid);
     if (kValues) {
-      edge_loads(a_vals, rav, ea0, ea1, s_aval, tid, kAddRows);
-      edge_loads(b_vals, rbv, eb0, eb1, s_bval, tid, kAddRows);
+      edge_loads_small(a_vals, rav, ea0, ea1, s_aval, tid);
+      edge_loads_small(b_vals, rbv, eb0, eb1, s_bval, tid);
     }
     __syncthreads();
     mbar_wait(&bar, 0);
@@ -269,8 +315,9 @@ add_tile_kernel(int64_t nrows, const int32_t* __restrict__ a_pos, const int32_t*
     int cnt = 0;
     if (mine) {
       if (fits) {
-        cnt = merge_row<false>(s_apos[tid], s_apos[tid + 1], s_bpos[tid], s_bpos[tid + 1], sacc,
-                               NoEmit{});
+        cnt = merge_row_smem<false>(s_apos[tid], s_apos[tid + 1], s_bpos[tid], s_bpos[tid + 1],
+                                    s_acrd - ra.lo0, nullptr, s_bcol - rb.lo0, nullptr, nullptr,
+                                    nullptr);
       } else {
         cnt = merge_row<false>(s_apos[tid], s_apos[tid + 1], s_bpos[tid], s_bpos[tid + 1], gacc,
                                NoEmit{});
@@ -314,17 +361,20 @@ add_tile_kernel(int64_t nrows, const int32_t* __restrict__ a_pos, const int32_t*
   if (mine) {
     const int32_t lo = s_rbase[tid];
     if (fits)
-      merge_row<true>(s_apos[tid], s_apos[tid + 1], s_bpos[tid], s_bpos[tid + 1], sacc,
-                      FillEmit{oc + lo, ov + lo});
+      merge_row_smem<true>(s_apos[tid], s_apos[tid + 1], s_bpos[tid], s_bpos[tid + 1],
+                           s_acrd - ra.lo0, s_aval - rav.lo0, s_bcol - rb.lo0, s_bval - rbv.lo0,
+                           oc + lo, ov + lo);
     else
       merge_row<true>(s_apos[tid], s_apos[tid + 1], s_bpos[tid], s_bpos[tid + 1], gacc,
                       FillEmit{oc + lo, ov + lo});
   }
   if (staged_out) {
     __syncthreads();
-    for (int64_t q = tid; q < n_out; q += kAddRows) {
-      c_crd[tile_out + q] = s_ccrd[q];
-      c_vals[tile_out + q] = s_cval[q];
+    int32_t* gc = c_crd + tile_out;
+    double* gv = c_vals + tile_out;
+    for (int q = tid; q < (int)n_out; q += kAddRows) {
+      gc[q] = s_ccrd[q];
+      gv[q] = s_cval[q];
     }
   }
 }

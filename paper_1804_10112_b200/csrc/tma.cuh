@@ -119,4 +119,18 @@ SL_DEV void edge_loads(const T* g, const BulkRange<T>& r, int64_t lo, int64_t hi
     if (e >= r.blo) s[e - r.lo0] = g[e];
 }
 
+// Constant-time version for callers whose ranges are known to be short at the
+// ends: the unaligned head and tail each hold fewer than 16/sizeof(T)
+// elements, loaded by threads [0, head) and [64, 64 + tail) (blockDim >= 96).
+template <typename T>
+SL_DEV void edge_loads_small(const T* g, const BulkRange<T>& r, int64_t lo, int64_t hi, T* s,
+                             int tid) {
+  const int nh = (int)(min64(r.blo, hi) - lo);
+  if (tid < nh) s[lo + tid - r.lo0] = g[lo + tid];
+  const int64_t t0 = max64(r.bhi, lo) > min64(r.blo, hi) ? max64(r.bhi, lo) : min64(r.blo, hi);
+  const int nt = (int)(hi - t0);
+  const int k = tid - 64;
+  if (k >= 0 && k < nt) s[t0 + k - r.lo0] = g[t0 + k];
+}
+
 }  // namespace sl
