@@ -213,6 +213,25 @@ int sl_spmv_csr_hashx_map_f64(int64_t nrows, int64_t n, const int32_t* pos, cons
                               const double* x_vals, double* y, void* ws, size_t ws_bytes,
                               void* stream);
 
+/* CSR x sparse-vector x (compressed, ordered, unique; dimension n): the
+ * product's j-lattice is the intersection {A1, x1} (engine.py:211-225,
+ * 591-634) — only coordinates present in both contribute, in ascending j.
+ * Replaces that merge with an index map (coordinate -> position in x) built
+ * in ws, then the CSR row-block kernel.  ws: sl_spmv_csr_spx_workspace_bytes(n). */
+size_t sl_spmv_csr_spx_workspace_bytes(int64_t n);
+int sl_spmv_csr_spx_f64(int64_t nrows, int64_t n, const int32_t* pos, const int32_t* crd,
+                        const double* vals, int64_t x_nnz, const int32_t* x_crd,
+                        const double* x_vals, double* y, void* ws, size_t ws_bytes,
+                        void* stream);
+
+/* ---- SpMM  Y(i,k) = A(i,j) * X(j,k): A CSR, X (ncols x K) and Y (nrows x K)
+ * dense row-major (dense-2).  Replaces the (i, j, k) loop nest with dense
+ * scatter (engine.py:591-634, 281-320): each Y(i,k) accumulates the row's
+ * products in storage order from +0.0 — bit-identical. */
+int sl_spmm_csr_f64(int64_t nrows, int64_t ncols, int64_t K, const int32_t* pos,
+                    const int32_t* crd, const double* vals, const double* X, double* Y,
+                    void* stream);
+
 size_t sl_add_csr_workspace_bytes(int64_t nrows, int64_t b_nnz);
 int sl_add_csr_count(int64_t nrows,
                      const int32_t* a_pos, const int32_t* a_crd,

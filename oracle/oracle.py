@@ -67,6 +67,9 @@ def lib():
                               _ptr, _ptr],
             "or_mttkrp_csf_mt": [_i64, _i32, _i64, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr,
                                  _ptr, _ptr, ctypes.c_int],
+            "or_spmv_csr_spx": [_i64, _ptr, _ptr, _ptr, _i64, _ptr, _ptr, _ptr, _ptr],
+            "or_spmm_csr": [_i64, _i64, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr],
+            "or_spmm_csr_mt": [_i64, _i64, _ptr, _ptr, _ptr, _ptr, _ptr, ctypes.c_int],
             "or_num_threads": [],
         }
         for name, args in sig.items():
@@ -166,6 +169,30 @@ def spmv_csr_hashx(nrows, pos, crd, vals, w, xcrd, xvals, threads=None):
     lib().or_spmv_csr_hashx_mt(nrows, _p(pos), _p(crd), _p(vals), w, _p(xcrd), _p(xvals), _p(y),
                                threads)
     return y
+
+
+def spmv_csr_spx(nrows, pos, crd, vals, xcrd, xvals):
+    """CSR x sparse-vector (intersection), see or_spmv_csr_spx."""
+    pos, crd, vals = _c(pos, np.int32), _c(crd, np.int32), _c(vals, np.float64)
+    xcrd, xvals = _c(xcrd, np.int32), _c(xvals, np.float64)
+    y = np.empty(nrows, dtype=np.float64)
+    a = np.empty(nrows, dtype=np.float64)
+    lib().or_spmv_csr_spx(nrows, _p(pos), _p(crd), _p(vals), len(xcrd), _p(xcrd), _p(xvals),
+                          _p(y), _p(a))
+    return y, a
+
+
+def spmm_csr(nrows, K, pos, crd, vals, X, threads=None):
+    """Y = A X with A CSR, X dense (ncols x K), see or_spmm_csr."""
+    pos, crd, vals = _c(pos, np.int32), _c(crd, np.int32), _c(vals, np.float64)
+    X = _c(X, np.float64)
+    Y = np.empty(nrows * K, dtype=np.float64)
+    if threads is None:
+        a = np.empty(nrows * K, dtype=np.float64)
+        lib().or_spmm_csr(nrows, K, _p(pos), _p(crd), _p(vals), _p(X), _p(Y), _p(a))
+        return Y.reshape(nrows, K), a.reshape(nrows, K)
+    lib().or_spmm_csr_mt(nrows, K, _p(pos), _p(crd), _p(vals), _p(X), _p(Y), threads)
+    return Y.reshape(nrows, K)
 
 
 def add_csr(nrows, a_pos, a_crd, a_vals, b_cols, b_vals, b_rows=None, b_pos=None, threads=None):

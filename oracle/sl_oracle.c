@@ -432,4 +432,68 @@ void or_mttkrp_csf_mt(int64_t I, int32_t R, int64_t nslices, const int32_t* crd0
   }
 }
 
+/* ------------------------------------------------------------------------
+ * SpMV CSR x sparse-vector (compressed, ordered, unique: formats.py
+ * "sparse-vector").  The j-lattice of a product is the intersection {A1, x1}:
+ * merge_visits (engine.py:211-225) walks both sorted streams and the case
+ * body runs only where both are present, in ascending j (run_node,
+ * engine.py:591-634); the scatter writer adds each term to y(i) from +0.0. */
+void or_spmv_csr_spx(int64_t nrows, const int32_t* pos, const int32_t* crd, const double* vals,
+                     int64_t xnnz, const int32_t* xcrd, const double* xvals, double* y,
+                     double* absy) {
+  for (int64_t r = 0; r < nrows; ++r) {
+    double acc = 0.0, a = 0.0;
+    int64_t q = 0;
+    for (int64_t p = pos[r]; p < pos[r + 1]; ++p) {
+      while (q < xnnz && xcrd[q] < crd[p]) ++q;
+      if (q == xnnz) break;
+      if (xcrd[q] != crd[p]) continue;
+      const double t = vals[p] * xvals[q];
+      acc = acc + t;
+      a += fabs(t);
+    }
+    y[r] = acc;
+    if (absy) absy[r] = a;
+  }
+}
+
+/* SpMM Y(i,k) = A(i,j) * X(j,k): A CSR, X and Y dense-2 (row-major).  Loop
+ * nest (i, j, k) with Y located densely (engine.py:591-634, scatter writer
+ * :281-320): each Y(i,k) receives A(i,j) * X(j,k) for the row's j in storage
+ * order, accumulated from +0.0.  Y has nrows * K entries. */
+void or_spmm_csr(int64_t nrows, int64_t K, const int32_t* pos, const int32_t* crd,
+                 const double* vals, const double* X, double* Y, double* absY) {
+  for (int64_t q = 0; q < nrows * K; ++q) {
+    Y[q] = 0.0;
+    if (absY) absY[q] = 0.0;
+  }
+  for (int64_t r = 0; r < nrows; ++r) {
+    double* yr = Y + r * K;
+    for (int64_t p = pos[r]; p < pos[r + 1]; ++p) {
+      const double a = vals[p];
+      const double* xr = X + (int64_t)crd[p] * K;
+      for (int64_t k = 0; k < K; ++k) {
+        const double t = a * xr[k];
+        yr[k] = yr[k] + t;
+        if (absY) absY[r * K + k] += fabs(t);
+      }
+    }
+  }
+}
+
+void or_spmm_csr_mt(int64_t nrows, int64_t K, const int32_t* pos, const int32_t* crd,
+                    const double* vals, const double* X, double* Y, int nthreads) {
+  nthreads = clamp_threads(nthreads);
+#pragma omp parallel for num_threads(nthreads) schedule(static, 256)
+  for (int64_t r = 0; r < nrows; ++r) {
+    double* yr = Y + r * K;
+    for (int64_t k = 0; k < K; ++k) yr[k] = 0.0;
+    for (int64_t p = pos[r]; p < pos[r + 1]; ++p) {
+      const double a = vals[p];
+      const double* xr = X + (int64_t)crd[p] * K;
+      for (int64_t k = 0; k < K; ++k) yr[k] = yr[k] + a * xr[k];
+    }
+  }
+}
+
 int or_num_threads(void) { return clamp_threads(0); }

@@ -229,6 +229,18 @@ struct XOperand<2> {                // hashed x through the slot map (hashed.cu)
   }
 };
 
+template <>
+struct XOperand<3> {                // sparse-vector x (compressed, ordered, unique):
+  const int32_t* map;               // index of coordinate c in x, -1 if absent — the
+  const double* xv;                 // intersection {A1, x1} of the product's j-lattice
+  int64_t n;                        // (engine.py:211-225, 591-634): absent -> no term
+  SL_DEV int64_t slot(int32_t c) const { return c < n ? (int64_t)__ldg(map + c) : -1; }
+  SL_DEV double term(double a, int32_t c) const {
+    const int64_t sl = slot(c);
+    return sl >= 0 ? dmul(a, ldg(xv + sl)) : 0.0;
+  }
+};
+
 // Stage products of elements [cs, cs + n) into s_prod with every load of a
 // thread issued before its first use (crd/vals stream, then the x gathers).
 template <int kThreads, int kIpt>
@@ -265,9 +277,9 @@ SL_DEV void stage_products(const int32_t* __restrict__ crd, const double* __rest
 
 // Mapped hashed x: crd/vals, then the map entries, then x — each batch of
 // loads independent of the next batch's wait.
-template <int kThreads, int kIpt>
+template <int kThreads, int kIpt, int kX>
 SL_DEV void stage_products(const int32_t* __restrict__ crd, const double* __restrict__ vals,
-                           int64_t cs, int n, XOperand<2> xop, double* s_prod) {
+                           int64_t cs, int n, XOperand<kX> xop, double* s_prod) {
   const int tid = threadIdx.x;
   int32_t c[kIpt];
   double v[kIpt];
@@ -721,6 +733,43 @@ extern "C" int sl_spmv_csr_hashx_map_f64(int64_t nrows, int64_t n, const int32_t
   if (st != SL_OK) return st;
   XOperand<2> xop{HashedLevel{x_crd, w}, x_vals, static_cast<const unsigned long long*>(ws), n};
   return launch_csr<2>(nrows, pos, crd, vals, xop, y, 0, nullptr, 0, as_stream(stream));
+}
+
+__global__ void spx_map_kernel(int64_t n, int64_t xnnz, const int32_t* __restrict__ xcrd,
+                               int32_t* __restrict__ map) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (int64_t i = t; i < n; i += stride) map[i] = -1;
+}
+
+__global__ void spx_scatter_kernel(int64_t n, int64_t xnnz, const int32_t* __restrict__ xcrd,
+                                   int32_t* __restrict__ map) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < xnnz; q += stride) {
+    const int32_t c = ldg(xcrd + q);
+    if (c >= 0 && c < n) map[c] = (int32_t)q;
+  }
+}
+
+extern "C" size_t sl_spmv_csr_spx_workspace_bytes(int64_t n) { return (size_t)n * 4 + 256; }
+
+extern "C" int sl_spmv_csr_spx_f64(int64_t nrows, int64_t n, const int32_t* pos,
+                                   const int32_t* crd, const double* vals, int64_t xnnz,
+                                   const int32_t* x_crd, const double* x_vals, double* y,
+                                   void* ws, size_t ws_bytes, void* stream) {
+  if (nrows < 0 || n < 0 || xnnz < 0) return SL_ERR_INVALID;
+  if (nrows > INT32_MAX || n > INT32_MAX || xnnz > INT32_MAX) return SL_ERR_RANGE;
+  if (nrows == 0) return SL_OK;
+  if (!pos || !y || (xnnz > 0 && (!x_crd || !x_vals))) return SL_ERR_INVALID;
+  if (!ws || ws_bytes < sl_spmv_csr_spx_workspace_bytes(n)) return SL_ERR_WORKSPACE;
+  cudaStream_t s = as_stream(stream);
+  int32_t* map = static_cast<int32_t*>(ws);
+  const int sms = sl_host::sm_count();
+  if (n > 0) spx_map_kernel<<<min(ceil_div(n, 256), 8 * sms), 256, 0, s>>>(n, xnnz, x_crd, map);
+  if (xnnz > 0)
+    spx_scatter_kernel<<<min(ceil_div(xnnz, 256), 8 * sms), 256, 0, s>>>(n, xnnz, x_crd, map);
+  XOperand<3> xop{map, x_vals, n};
+  return launch_csr<3>(nrows, pos, crd, vals, xop, y, 0, nullptr, 0, s);
 }
 
 extern "C" int sl_spmv_ell_f64(int64_t nrows, int64_t ncols, int32_t nslots, const int32_t* crd,

@@ -76,6 +76,8 @@ def format_class(fmt: TensorFormat) -> str:
             return "csf"
         if k == (LK.HASHED,):
             return "hash1"
+        if k == (LK.COMPRESSED,) and fmt.levels[0].props.ordered and fmt.levels[0].props.unique:
+            return "spvec"
     roles = tuple(r.part for r in fmt.roles)
     if k == (LK.DENSE, LK.DENSE, LK.SINGLETON) and roles == ("slot", "whole", "whole"):
         return "ell"
@@ -128,8 +130,28 @@ def plan(checked: CheckedExpr, bindings, out_format: TensorFormat,
                 if cx == "hash1" and ca == "csr":
                     return Plan("spmv", "spmv_csr_hashx", {"A": A.tensor, "x": x.tensor},
                                 out_format, out_dims)
+                if cx == "spvec" and ca == "csr":
+                    return Plan("spmv", "spmv_csr_spx", {"A": A.tensor, "x": x.tensor},
+                                out_format, out_dims)
                 raise UnsupportedMergeError(
                     f"no B200 kernel for SpMV with A {ca} and x {cx}")
+
+    # ---- SpMM: Y(i,k) = A(i,j) * X(j,k), A CSR, X dense-2
+    if isinstance(rhs, Mul) and all(isinstance(t, Access) for t in (rhs.left, rhs.right)):
+        acc = [rhs.left, rhs.right]
+        if all(len(t.ivars) == 2 for t in acc) and len(lhs.ivars) == 2:
+            for A, X in ((acc[0], acc[1]), (acc[1], acc[0])):
+                i, j = A.ivars
+                if (X.ivars[0] == j and lhs.ivars == (i, X.ivars[1])
+                        and len({i, j, X.ivars[1]}) == 3):
+                    ca, cx = cls[A.tensor], cls[X.tensor]
+                    if ca == "csr" and cx == "dense2":
+                        if ocls != "dense2":
+                            raise UnsupportedOutputError("SpMM output must be dense-2")
+                        return Plan("spmm", "spmm_csr", {"A": A.tensor, "X": X.tensor},
+                                    out_format, out_dims)
+            raise UnsupportedMergeError("no B200 kernel for this matrix product "
+                                        "(supported: CSR x dense-2)")
 
     # ---- C(i,j) = A(i,j) + B(i,j)
     if isinstance(rhs, Add) and all(isinstance(t, Access) for t in (rhs.left, rhs.right)):
@@ -175,8 +197,8 @@ def plan(checked: CheckedExpr, bindings, out_format: TensorFormat,
                         f"C {cls[Cm.tensor]}")
     raise UnsupportedMergeError(
         "no B200 kernel implements this expression/format combination "
-        "(supported: SpMV over coo/csr/ell/dia with dense or hashed x, CSR + COO/CSR -> CSR, "
-        "MTTKRP over COO-3/CSF)")
+        "(supported: SpMV over coo/csr/ell/dia with dense x, CSR with hashed or sparse-vector x, "
+        "SpMM CSR x dense-2, CSR + COO/CSR -> CSR, MTTKRP over COO-3/CSF)")
 
 
 # ---------------------------------------------------------------------------
@@ -224,6 +246,11 @@ def _run(p: Plan, inputs: Dict[str, TensorStorage], stats: Optional[EvalStats]):
             y = K.spmv_dia(nrows, ncols, offs, A.vals, x.vals)
             visits = {"diag": len(offs), "i": int(sum(
                 max(0, min(nrows, ncols - o) - max(0, -o)) for o in offs.tolist()))}
+        elif p.kernel == "spmv_csr_spx":
+            sx = x.levels[0]
+            y = K.spmv_csr_spx(nrows, int(x.dims[0]), A.levels[1].pos, A.levels[1].crd, A.vals,
+                               sx.crd, x.vals)
+            visits = {"i": nrows, "j": int(A.levels[1].crd.numel())}
         else:  # spmv_csr_hashx
             hx = x.levels[0]
             nq = int(A.levels[1].crd.numel())
@@ -248,6 +275,17 @@ def _run(p: Plan, inputs: Dict[str, TensorStorage], stats: Optional[EvalStats]):
                                         LevelStorage(f.levels[1], pos=c_pos, crd=c_crd,
                                                      device=dev)], c_vals)
         visits = {"i": nrows, "j": int(c_crd.numel())}
+    elif p.pattern == "spmm":
+        A, X = ops["A"], ops["X"]
+        nrows, ncols = A.dims
+        Kc = X.dims[1]
+        Y = K.spmm_csr(nrows, ncols, A.levels[1].pos, A.levels[1].crd, A.vals,
+                       X.vals.view(ncols, Kc))
+        f = p.out_format
+        out = TensorStorage(f, (nrows, Kc), [LevelStorage(f.levels[0], n=nrows, device=dev),
+                                             LevelStorage(f.levels[1], n=Kc, device=dev)],
+                            Y.reshape(-1))
+        visits = {"i": nrows, "k": int(A.levels[1].crd.numel()) * Kc}
     else:  # mttkrp
         X, B, C = ops["X"], ops["B"], ops["C"]
         I, J, Kd = X.dims

@@ -253,6 +253,16 @@ def dia_storage(offsets, vals, dims, device="cuda") -> TensorStorage:
     return st
 
 
+def sparse_vector_storage(crd, vals, n, device="cuda") -> TensorStorage:
+    """sparse-vector (formats.py:122-123): one compressed level, sorted unique
+    coordinates, pos = [0, nnz]."""
+    fmt = preset("sparse-vector")
+    crd = np.asarray(crd, dtype=np.int32) if not hasattr(crd, "is_cuda") else crd
+    nnz = len(crd)
+    l0 = LevelStorage(fmt.levels[0], pos=[0, nnz], crd=crd, device=device)
+    return TensorStorage(fmt, (n,), [l0], _f64(vals, device))
+
+
 def hash_vector_storage(crd, vals, n, width, device="cuda") -> TensorStorage:
     """hash-vector (formats.py:124-125): one hashed level of width W,
     crd[W] with -1 empties, vals[W] by slot."""

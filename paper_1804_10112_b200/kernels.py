@@ -119,6 +119,30 @@ def spmv_csr_hashx(nrows, pos, crd, vals, w, x_crd, x_vals, y=None, n=None, ws=N
     return y
 
 
+def spmv_csr_spx(nrows, n, pos, crd, vals, x_crd, x_vals, y=None, ws=None):
+    """CSR x sparse-vector (intersection), x of dimension n."""
+    pos, crd, vals = _t(pos, I32, "pos"), _t(crd, I32, "crd"), _t(vals, F64, "vals")
+    x_crd, x_vals = _t(x_crd, I32, "x_crd"), _t(x_vals, F64, "x_vals")
+    y = _out(y, nrows, F64, vals, "y")
+    need = L().sl_spmv_csr_spx_workspace_bytes(n)
+    if ws is None or ws.numel() < need:
+        ws = _ws(need, vals)
+    _lib.check(L().sl_spmv_csr_spx_f64(nrows, n, P(pos), P(crd), P(vals), x_crd.numel(), P(x_crd),
+                                       P(x_vals), P(y), P(ws), ws.numel(), S()), "spmv_csr_spx")
+    return y
+
+
+def spmm_csr(nrows, ncols, pos, crd, vals, X, Y=None):
+    """Y = A X, A CSR (nrows x ncols), X dense (ncols x K) row-major."""
+    pos, crd, vals = _t(pos, I32, "pos"), _t(crd, I32, "crd"), _t(vals, F64, "vals")
+    X = _t(X, F64, "X")
+    K = X.shape[-1] if X.dim() == 2 else X.numel() // max(ncols, 1)
+    Y = _out(Y, nrows * K, F64, vals, "Y").view(nrows, K) if Y is None else _t(Y, F64, "Y")
+    _lib.check(L().sl_spmm_csr_f64(nrows, ncols, K, P(pos), P(crd), P(vals), P(X), P(Y), S()),
+               "spmm_csr")
+    return Y
+
+
 def hashed_slot_map(n, w, crd, ws=None):
     """u64 per coordinate c < n: (probe distance << 32 | slot) of locate(c), ~0 absent."""
     crd = _t(crd, I32, "crd")

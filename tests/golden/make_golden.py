@@ -334,6 +334,55 @@ def convert_cases():
     return cases
 
 
+# ---------------------------------------------------------------------------
+# widening: CSR x sparse-vector and SpMM
+
+def spx_case(name, nrows, ncols, rows, cols, vals, x_keep, x_vals):
+    out = {"nrows": nrows, "ncols": ncols}
+    csr = sl.assemble(sl.preset("csr"), (nrows, ncols), coordlist((nrows, ncols), zip(rows, cols), vals))
+    _csr_arrays(csr, "csr", out)
+    xs = sl.assemble(sl.preset("sparse-vector"), (ncols,),
+                     coordlist((ncols,), [(int(c),) for c in x_keep], x_vals))
+    out["x_crd"] = i32(xs.levels[0].crd)
+    out["x_vals"] = f64(xs.vals[:len(xs.levels[0].crd)] if xs.levels[0].crd else [])
+    out["y"] = f64(sl.evaluate("y(i) = A(i,j) * x(j)", {"A": csr, "x": xs}).vals[:nrows])
+    return name, out
+
+
+def spmm_case(name, nrows, ncols, K, rows, cols, vals, X):
+    out = {"nrows": nrows, "ncols": ncols, "K": K}
+    csr = sl.assemble(sl.preset("csr"), (nrows, ncols), coordlist((nrows, ncols), zip(rows, cols), vals))
+    _csr_arrays(csr, "csr", out)
+    X = np.asarray(X, dtype=np.float64).reshape(ncols, K)
+    out["X"] = X.reshape(-1)
+    Y = sl.evaluate("Y(i,k) = A(i,j) * X(j,k)", {"A": csr, "X": dense_mat(X)})
+    out["Y"] = f64(Y.vals[:nrows * K])
+    return name, out
+
+
+def widen_cases():
+    cases = []
+    for seed in range(3):
+        d = wl.coo_spmv(n=30 + 11 * seed, ncols=40 + 5 * seed, nnz=6 * (30 + 11 * seed), lam=6.0,
+                        seed=300 + seed)
+        rng = np.random.default_rng(700 + seed)
+        keep = np.sort(rng.choice(d["ncols"], size=d["ncols"] // 3, replace=False))
+        xv = rng.uniform(-1, 1, len(keep))
+        xv[::5] = -0.0
+        cases.append(spx_case(f"spx_rand{seed}", d["nrows"], d["ncols"], d["rows"], d["cols"],
+                              d["vals"], keep, xv))
+        for K in (1, 3, 8, 33):
+            X = rng.uniform(-1, 1, d["ncols"] * K)
+            cases.append(spmm_case(f"spmm_rand{seed}_k{K}", d["nrows"], d["ncols"], K, d["rows"],
+                                   d["cols"], d["vals"], X))
+    cases.append(spx_case("spx_empty_x", 5, 6, [0, 1, 4], [1, 2, 5], [1.0, 2.0, 3.0], [], []))
+    cases.append(spx_case("spx_signed", 3, 4, [0, 0, 1, 2], [0, 3, 1, 2], [-0.0, 1.5, -2.0, 0.0],
+                          [0, 1, 3], [2.0, -0.0, 1e-300]))
+    cases.append(spmm_case("spmm_empty_rows", 4, 3, 2, [1, 1, 3], [0, 2, 1], [1.0, -1.0, 0.5],
+                           np.arange(6, dtype=np.float64) - 2.5))
+    return cases
+
+
 def level_kats():
     """Run the reference level functions on the test_levels.py fixtures."""
     E = rl.EMPTY
@@ -466,6 +515,7 @@ def main():
         "add": add_cases(),
         "mttkrp": mttkrp_cases(),
         "convert": convert_cases(),
+        "widen": widen_cases(),
     }
     for group, cases in groups.items():
         flat = {}

@@ -168,3 +168,25 @@ def test_oracle_convert_goldens(orc):
             offs, dv = orc.convert_coo_to_dia(n, m, c["coo_rows"], c["coo_cols"], c["coo_vals"])
             assert np.array_equal(offs, c["dia_offsets"]), name
             assert orc.bits_equal(dv, c["dia_vals"]), name
+
+
+# ---------------------------------------------------------------------------
+# widening: CSR x sparse-vector and SpMM against the reference's evaluate()
+
+def test_oracle_widen_goldens(orc):
+    n_spx = n_spmm = 0
+    for name, c in load_cases("widen").items():
+        n = int(c["nrows"])
+        if name.startswith("spx"):
+            y, _ = orc.spmv_csr_spx(n, c["csr_pos"], c["csr_crd"], c["csr_vals"], c["x_crd"],
+                                    c["x_vals"])
+            assert orc.bits_equal(y, c["y"]), name
+            n_spx += 1
+        else:
+            K = int(c["K"])
+            Y, _ = orc.spmm_csr(n, K, c["csr_pos"], c["csr_crd"], c["csr_vals"], c["X"])
+            assert orc.bits_equal(Y.reshape(-1), c["Y"]), name
+            Ymt = orc.spmm_csr(n, K, c["csr_pos"], c["csr_crd"], c["csr_vals"], c["X"], threads=4)
+            assert orc.bits_equal(Ymt.reshape(-1), c["Y"]), name
+            n_spmm += 1
+    assert n_spx >= 4 and n_spmm >= 12
