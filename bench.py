@@ -388,7 +388,40 @@ def run_formats(torch, K, wl, dev, timer, peak, steps):
     t = float(np.mean(tt["csr"]))
     res["csr_spmv_D1"] = {"ms": round(t, 5), "GB/s": round(bs / t / 1e6, 1),
                           "frac": round(bs / t / 1e6 / peak, 4), "bytes": bs}
+    # the paper's end-to-end question (Fig. 13): COO SpMV on unconverted
+    # coordinates vs converting to CSR first (exact identity copy) and then CSR SpMV
+    res["coo_vs_convert_then_csr_D1"] = {
+        "coo_spmv_ms": res["coo_spmv_D1"]["ms"],
+        "convert_plus_csr_ms": round(res["convert_coo_to_csr_D1"]["ms"] + t, 5),
+        "rowptr_only_plus_csr_ms": round(res["coo_rowptr_D1"]["ms"] + t, 5)}
     del r, c, v, x, y, pos, rp
+
+    # widened patterns on the headline stencil: SpMM with
+    # K = 16 dense columns, and CSR x sparse-vector x holding half the coordinates
+    st = wl.stencil27()
+    n, nnz = st["nrows"], len(st["crd"])
+    sp, sc, sv = T(st["pos"]), T(st["crd"]), T(st["vals"])
+    Kc = 16
+    rng = np.random.default_rng(5)
+    Xd = T(rng.uniform(-1, 1, (n, Kc)))
+    Yd = torch.empty((n, Kc), dtype=torch.float64, device=dev)
+    keep = np.sort(rng.choice(n, n // 2, replace=False)).astype(np.int32)
+    xk, xkv = T(keep), T(rng.uniform(-1, 1, len(keep)))
+    ys = torch.empty(n, dtype=torch.float64, device=dev)
+    sws = torch.empty(int(K.L().sl_spmv_csr_spx_workspace_bytes(n)), dtype=torch.uint8, device=dev)
+    tt = timer.run({"spmm": lambda: K.spmm_csr(n, n, sp, sc, sv, Xd, Yd),
+                    "spx": lambda: K.spmv_csr_spx(n, n, sp, sc, sv, xk, xkv, ys, sws)}, steps, 3)
+    b = 4 * (n + 1) + 12 * nnz + 16 * n * Kc
+    t = float(np.mean(tt["spmm"]))
+    res["spmm_csr_stencil_K16"] = {"ms": round(t, 5), "GB/s": round(b / t / 1e6, 1),
+                                   "frac": round(b / t / 1e6 / peak, 4), "bytes": b,
+                                   "GFLOP/s": round(2 * nnz * Kc / t / 1e6, 1)}
+    b = 4 * (n + 1) + 12 * nnz + 12 * len(keep) + 8 * n
+    t = float(np.mean(tt["spx"]))
+    res["spmv_csr_spx_stencil"] = {"ms": round(t, 5), "GB/s": round(b / t / 1e6, 1),
+                                   "frac": round(b / t / 1e6 / peak, 4), "bytes": b,
+                                   "x_nnz": int(len(keep))}
+    del sp, sc, sv, Xd, Yd, xk, xkv, ys, sws
 
     g = wl.dia7()
     n = g["nrows"]

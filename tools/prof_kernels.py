@@ -67,6 +67,11 @@ def main():
         jobs["csr_vec"] = (bc, lambda: K.spmv_csr(n, n, p, c, v, x, y, variant=1))
         jobs["csr_merge"] = (bc, lambda: K.spmv_csr(n, n, p, c, v, x, y, variant=2))
         jobs["csr_warp"] = (bc, lambda: K.spmv_csr(n, n, p, c, v, x, y, variant=3))
+        for Kc in (4, 16, 32):
+            Xd = torch.rand((n, Kc), dtype=torch.float64, device=dev)
+            Yd = torch.empty((n, Kc), dtype=torch.float64, device=dev)
+            jobs[f"spmm{Kc}"] = (4 * (n + 1) + 12 * len(s["crd"]) + 16 * n * Kc,
+                                 lambda Xd=Xd, Yd=Yd: K.spmm_csr(n, n, p, c, v, Xd, Yd))
         jobs["ell"] = (12 * 27 * n + 16 * n, lambda: K.spmv_ell(n, n, 27, ec, ev, x, y))
 
     def d3():
@@ -103,7 +108,8 @@ def main():
     if (want("coo") or want("hashx") or want("hashx_wdef") or want("csr_d1")
             or want("hashx_map") or want("hashx_wdef_map")):
         d1()
-    if want("csr") or want("ell") or want("csr_vec") or want("csr_merge") or want("csr_warp"):
+    if (want("csr") or want("ell") or want("csr_vec") or want("csr_merge") or want("csr_warp")
+            or want("spmm4") or want("spmm16") or want("spmm32")):
         d2()
     if want("dia"):
         d3()
