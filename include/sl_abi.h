@@ -232,6 +232,28 @@ int sl_spmm_csr_f64(int64_t nrows, int64_t ncols, int64_t K, const int32_t* pos,
                     const int32_t* crd, const double* vals, const double* X, double* Y,
                     void* stream);
 
+/* ---- 3-tensor kernels beyond MTTKRP (X CSF) ----------
+ * TTV Y(i,j) = X(i,j,k) v(k) and TTM Y(i,j,r) = X(i,j,k) U(k,r) reduce over k
+ * inside each (i, j) fiber: the fiber sums are sl_spmv_csr_f64 /
+ * sl_spmm_csr_f64 over the fibers as rows (pos2, crd2, vals), bit-identical.
+ * Then, dense output: rows (nfibers x R) scattered to out (I x J x R, zero
+ * elsewhere); CSR output (gather writer, engine.py:330-434): one entry per
+ * fiber, pos over i from the slice structure, crd = crd1, vals = fiber sums. */
+int sl_csf_fiber_scatter_f64(int64_t I, int64_t J, int64_t R, int64_t nslices, int64_t nfibers,
+                             const int32_t* crd0, const int32_t* pos1, const int32_t* crd1,
+                             const double* rows, double* out, void* stream);
+int sl_csf_fiber_rowptr(int64_t I, int64_t nslices, const int32_t* crd0, const int32_t* pos1,
+                        int32_t* pos_out, void* stream);
+/* INNERPROD a() = X(i,j,k) * Z(i,j,k), both COO-3 sorted: intersection at
+ * every level (engine.py:211-225).  *out (device) = the sum, reduced in a
+ * fixed tree order: deterministic, within the fp64 reduction tolerance of the
+ * reference's per-fiber / per-slice order.  ws: sl_inner_coo3_workspace_bytes(nx). */
+size_t sl_inner_coo3_workspace_bytes(int64_t nx);
+int sl_inner_coo3_f64(int64_t I, int64_t J, int64_t K, int64_t nx, const int32_t* xi,
+                      const int32_t* xj, const int32_t* xk, const double* xv, int64_t nz,
+                      const int32_t* zi, const int32_t* zj, const int32_t* zk, const double* zv,
+                      double* out, void* ws, size_t ws_bytes, void* stream);
+
 size_t sl_add_csr_workspace_bytes(int64_t nrows, int64_t b_nnz);
 int sl_add_csr_count(int64_t nrows,
                      const int32_t* a_pos, const int32_t* a_crd,

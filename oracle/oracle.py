@@ -70,6 +70,9 @@ def lib():
             "or_spmv_csr_spx": [_i64, _ptr, _ptr, _ptr, _i64, _ptr, _ptr, _ptr, _ptr],
             "or_spmm_csr": [_i64, _i64, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr],
             "or_spmm_csr_mt": [_i64, _i64, _ptr, _ptr, _ptr, _ptr, _ptr, ctypes.c_int],
+            "or_ttv_csf": [_i64, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr],
+            "or_ttm_csf": [_i64, _i32, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr],
+            "or_inner_coo3": [_i64, _ptr, _ptr, _ptr, _ptr, _i64, _ptr, _ptr, _ptr, _ptr, _ptr],
             "or_num_threads": [],
         }
         for name, args in sig.items():
@@ -79,6 +82,7 @@ def lib():
         L.or_add_csr_mt.restype = _i64
         L.or_hashed_insert.restype = ctypes.c_int
         L.or_num_threads.restype = ctypes.c_int
+        L.or_inner_coo3.restype = ctypes.c_double
         _LIB = L
     return _LIB
 
@@ -193,6 +197,38 @@ def spmm_csr(nrows, K, pos, crd, vals, X, threads=None):
         return Y.reshape(nrows, K), a.reshape(nrows, K)
     lib().or_spmm_csr_mt(nrows, K, _p(pos), _p(crd), _p(vals), _p(X), _p(Y), threads)
     return Y.reshape(nrows, K)
+
+
+def ttv_csf(csf, vals, v):
+    """Fiber sums of TTV over a CSF tensor (dict with pos0..crd2): (sums, abs sums)."""
+    c = {k: _c(csf[k], np.int32) for k in ("crd0", "pos1", "crd1", "pos2", "crd2")}
+    vals, v = _c(vals, np.float64), _c(v, np.float64)
+    nf = len(c["crd1"])
+    out, a = np.empty(nf, np.float64), np.empty(nf, np.float64)
+    lib().or_ttv_csf(len(c["crd0"]), _p(c["crd0"]), _p(c["pos1"]), _p(c["crd1"]), _p(c["pos2"]),
+                     _p(c["crd2"]), _p(vals), _p(v), _p(out), _p(a))
+    return out, a
+
+
+def ttm_csf(csf, vals, U):
+    """One R-row per fiber of TTM over a CSF tensor (nfibers x R)."""
+    c = {k: _c(csf[k], np.int32) for k in ("crd0", "pos1", "pos2", "crd2")}
+    vals, U = _c(vals, np.float64), _c(U, np.float64)
+    R = U.shape[1]
+    out = np.empty((len(_c(csf["crd1"], np.int32)), R), np.float64)
+    lib().or_ttm_csf(len(c["crd0"]), R, _p(c["pos1"]), _p(c["pos2"]), _p(c["crd2"]), _p(vals),
+                     _p(U), _p(out))
+    return out
+
+
+def inner_coo3(x, z):
+    """a() = X(i,j,k) * Z(i,j,k) over two sorted COO-3 tensors (dicts i, j, k, vals)."""
+    xs = [_c(x[k], np.int32) for k in ("i", "j", "k")] + [_c(x["vals"], np.float64)]
+    zs = [_c(z[k], np.int32) for k in ("i", "j", "k")] + [_c(z["vals"], np.float64)]
+    a = np.zeros(1, np.float64)
+    r = lib().or_inner_coo3(len(xs[0]), *[_p(t) for t in xs], len(zs[0]),
+                            *[_p(t) for t in zs], _p(a))
+    return float(r), float(a[0])
 
 
 def add_csr(nrows, a_pos, a_crd, a_vals, b_cols, b_vals, b_rows=None, b_pos=None, threads=None):

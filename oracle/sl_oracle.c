@@ -496,4 +496,88 @@ void or_spmm_csr_mt(int64_t nrows, int64_t K, const int32_t* pos, const int32_t*
   }
 }
 
+/* ------------------------------------------------------------------------
+ * TTV Y(i,j) = X(i,j,k) * v(k), X CSF: loop nest (i, j, k) (engine.py:591-634);
+ * each (i, j) fiber's products accumulate from +0.0 in storage order.
+ * Dense output (I x J, absent fibers 0.0) via the scatter writer; the CSR
+ * output (gather writer, engine.py:330-434) stores the same fiber sums
+ * (0.0 then += each product) with pos over i and crd = the fibers' j. */
+void or_ttv_csf(int64_t nslices, const int32_t* crd0, const int32_t* pos1, const int32_t* crd1,
+                const int32_t* pos2, const int32_t* crd2, const double* vals, const double* v,
+                double* fiber_sums, double* abs_sums) {
+  for (int64_t s = 0; s < nslices; ++s)
+    for (int64_t f = pos1[s]; f < pos1[s + 1]; ++f) {
+      double acc = 0.0, a = 0.0;
+      for (int64_t p = pos2[f]; p < pos2[f + 1]; ++p) {
+        const double t = vals[p] * v[crd2[p]];
+        acc = acc + t;
+        a += fabs(t);
+      }
+      fiber_sums[f] = acc;
+      if (abs_sums) abs_sums[f] = a;
+    }
+  (void)crd0;
+  (void)crd1;
+}
+
+/* TTM Y(i,j,r) = X(i,j,k) * U(k,r), X CSF, U and Y dense: loop nest
+ * (i, j, k, r); each Y(i,j,r) accumulates the fiber's products x * U(k,r)
+ * from +0.0 in storage order.  Writes one R-row per fiber. */
+void or_ttm_csf(int64_t nslices, int32_t R, const int32_t* pos1, const int32_t* pos2,
+                const int32_t* crd2, const double* vals, const double* U, double* fiber_rows) {
+  for (int64_t s = 0; s < nslices; ++s)
+    for (int64_t f = pos1[s]; f < pos1[s + 1]; ++f) {
+      double* y = fiber_rows + f * R;
+      for (int32_t r = 0; r < R; ++r) y[r] = 0.0;
+      for (int64_t p = pos2[f]; p < pos2[f + 1]; ++p) {
+        const double x = vals[p];
+        const double* u = U + (int64_t)crd2[p] * R;
+        for (int32_t r = 0; r < R; ++r) y[r] = y[r] + x * u[r];
+      }
+    }
+}
+
+/* INNERPROD a() = X(i,j,k) * Z(i,j,k), both COO-3 sorted lexicographically:
+ * the product's lattice at every level is the intersection (merge_visits,
+ * engine.py:211-225), and each loop level reduces into its own temporary
+ * before adding it to the parent's (run_node, engine.py:591-634): per (i, j)
+ * fiber the k products from +0.0, per slice i the fiber sums from +0.0, then
+ * the slice sums from +0.0 — verified bit for bit against the reference's
+ * evaluate() (tests/golden/widen.npz).  Returns the sum; *abs_sum = sum |x z|. */
+double or_inner_coo3(int64_t nx, const int32_t* xi, const int32_t* xj, const int32_t* xk,
+                     const double* xv, int64_t nz, const int32_t* zi, const int32_t* zj,
+                     const int32_t* zk, const double* zv, double* abs_sum) {
+  double total = 0.0, slice = 0.0, fiber = 0.0, a = 0.0;
+  int64_t cur_i = -1, cur_j = -1;
+  int64_t p = 0, q = 0;
+  while (p < nx && q < nz) {
+    const int c = xi[p] != zi[q] ? (xi[p] < zi[q] ? -1 : 1)
+                : xj[p] != zj[q] ? (xj[p] < zj[q] ? -1 : 1)
+                : xk[p] != zk[q] ? (xk[p] < zk[q] ? -1 : 1) : 0;
+    if (c < 0) { ++p; continue; }
+    if (c > 0) { ++q; continue; }
+    if (xi[p] != cur_i || xj[p] != cur_j) {
+      if (cur_i >= 0) slice = slice + fiber;
+      fiber = 0.0;
+      if (xi[p] != cur_i) {
+        if (cur_i >= 0) total = total + slice;
+        slice = 0.0;
+      }
+      cur_i = xi[p];
+      cur_j = xj[p];
+    }
+    const double t = xv[p] * zv[q];
+    fiber = fiber + t;
+    a += fabs(t);
+    ++p;
+    ++q;
+  }
+  if (cur_i >= 0) {
+    slice = slice + fiber;
+    total = total + slice;
+  }
+  if (abs_sum) *abs_sum = a;
+  return total;
+}
+
 int or_num_threads(void) { return clamp_threads(0); }

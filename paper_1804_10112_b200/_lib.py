@@ -89,6 +89,12 @@ SIGNATURES = {
     "sl_spmv_csr_spx_workspace_bytes": ([_i64], _sz),
     "sl_spmv_csr_spx_f64": ([_i64, _i64, _p, _p, _p, _i64, _p, _p, _p, _p, _sz, _p], ctypes.c_int),
     "sl_spmm_csr_f64": ([_i64, _i64, _i64, _p, _p, _p, _p, _p, _p], ctypes.c_int),
+    "sl_csf_fiber_scatter_f64": ([_i64, _i64, _i64, _i64, _i64, _p, _p, _p, _p, _p, _p],
+                                 ctypes.c_int),
+    "sl_csf_fiber_rowptr": ([_i64, _i64, _p, _p, _p, _p], ctypes.c_int),
+    "sl_inner_coo3_workspace_bytes": ([_i64], _sz),
+    "sl_inner_coo3_f64": ([_i64, _i64, _i64, _i64, _p, _p, _p, _p, _i64, _p, _p, _p, _p, _p, _p,
+                           _sz, _p], ctypes.c_int),
     "sl_l2_flush": ([_p, _sz, _p], ctypes.c_int),
 }
 

@@ -153,6 +153,42 @@ def plan(checked: CheckedExpr, bindings, out_format: TensorFormat,
             raise UnsupportedMergeError("no B200 kernel for this matrix product "
                                         "(supported: CSR x dense-2)")
 
+    # ---- 3-tensor x vector / matrix / tensor (X CSF or COO-3)
+    if isinstance(rhs, Mul) and all(isinstance(t, Access) for t in (rhs.left, rhs.right)):
+        acc = [rhs.left, rhs.right]
+        X3 = [t for t in acc if len(t.ivars) == 3]
+        if len(X3) >= 1:
+            X = X3[0]
+            other = acc[1] if acc[0] is X else acc[0]
+            i, j, k = X.ivars
+            cX, cO = cls[X.tensor], cls[other.tensor]
+            # TTV: Y(i,j) = X(i,j,k) * v(k)
+            if other.ivars == (k,) and lhs.ivars == (i, j) and len({i, j, k}) == 3:
+                if cX == "csf" and cO == "dense1":
+                    if ocls not in ("dense2", "csr"):
+                        raise UnsupportedOutputError("TTV output must be dense-2 or CSR")
+                    return Plan("ttv", f"ttv_csf_{ocls}", {"X": X.tensor, "v": other.tensor},
+                                out_format, out_dims)
+                raise UnsupportedMergeError(f"no B200 kernel for TTV with X {cX}, v {cO}")
+            # TTM: Y(i,j,r) = X(i,j,k) * U(k,r)
+            if (len(other.ivars) == 2 and other.ivars[0] == k and len(lhs.ivars) == 3
+                    and lhs.ivars == (i, j, other.ivars[1]) and len({i, j, k, other.ivars[1]}) == 4):
+                if cX == "csf" and cO == "dense2":
+                    if ocls != "dense3":
+                        raise UnsupportedOutputError("TTM output must be dense-3")
+                    return Plan("ttm", "ttm_csf", {"X": X.tensor, "U": other.tensor},
+                                out_format, out_dims)
+                raise UnsupportedMergeError(f"no B200 kernel for TTM with X {cX}, U {cO}")
+            # INNERPROD: a() = X(i,j,k) * Z(i,j,k)
+            if other.ivars == X.ivars and lhs.ivars == () and len({i, j, k}) == 3:
+                if cX == "coo3" and cO == "coo3":
+                    if ocls != "dense0":
+                        raise UnsupportedOutputError("inner product output must be a scalar")
+                    return Plan("inner", "inner_coo3", {"X": X.tensor, "Z": other.tensor},
+                                out_format, out_dims)
+                raise UnsupportedMergeError(
+                    f"no B200 kernel for the inner product of {cX} and {cO} (COO-3 x COO-3)")
+
     # ---- C(i,j) = A(i,j) + B(i,j)
     if isinstance(rhs, Add) and all(isinstance(t, Access) for t in (rhs.left, rhs.right)):
         L_, R_ = rhs.left, rhs.right
@@ -198,7 +234,8 @@ def plan(checked: CheckedExpr, bindings, out_format: TensorFormat,
     raise UnsupportedMergeError(
         "no B200 kernel implements this expression/format combination "
         "(supported: SpMV over coo/csr/ell/dia with dense x, CSR with hashed or sparse-vector x, "
-        "SpMM CSR x dense-2, CSR + COO/CSR -> CSR, MTTKRP over COO-3/CSF)")
+        "SpMM CSR x dense-2, CSR + COO/CSR -> CSR, MTTKRP over COO-3/CSF, TTV/TTM over CSF, "
+        "inner product of COO-3 tensors)")
 
 
 # ---------------------------------------------------------------------------
@@ -286,6 +323,39 @@ def _run(p: Plan, inputs: Dict[str, TensorStorage], stats: Optional[EvalStats]):
                                              LevelStorage(f.levels[1], n=Kc, device=dev)],
                             Y.reshape(-1))
         visits = {"i": nrows, "k": int(A.levels[1].crd.numel()) * Kc}
+    elif p.pattern in ("ttv", "ttm"):
+        X = ops["X"]
+        I, J, Kd = X.dims
+        lv = X.levels
+        args = (I, J, Kd, lv[0].crd, lv[1].pos, lv[1].crd, lv[2].pos, lv[2].crd, X.vals)
+        f = p.out_format
+        if p.kernel == "ttv_csf_csr":
+            pos, crd, vals = K.ttv_csf(*args, ops["v"].vals, out="csr")
+            out = TensorStorage(f, (I, J), [LevelStorage(f.levels[0], n=I, device=dev),
+                                            LevelStorage(f.levels[1], pos=pos, crd=crd,
+                                                         device=dev)], vals)
+        elif p.kernel == "ttv_csf_dense2":
+            Y = K.ttv_csf(*args, ops["v"].vals)
+            out = TensorStorage(f, (I, J), [LevelStorage(f.levels[0], n=I, device=dev),
+                                            LevelStorage(f.levels[1], n=J, device=dev)],
+                                Y.reshape(-1))
+        else:
+            U = ops["U"]
+            R = U.dims[1]
+            Y = K.ttm_csf(*args, U.vals.view(Kd, R))
+            out = TensorStorage(f, (I, J, R), [LevelStorage(f.levels[0], n=I, device=dev),
+                                               LevelStorage(f.levels[1], n=J, device=dev),
+                                               LevelStorage(f.levels[2], n=R, device=dev)],
+                                Y.reshape(-1))
+        visits = {"k": int(X.vals.numel())}
+    elif p.pattern == "inner":
+        X, Z = ops["X"], ops["Z"]
+        I, J, Kd = X.dims
+        xs = (X.levels[0].crd, X.levels[1].crd, X.levels[2].crd, X.vals)
+        zs = (Z.levels[0].crd, Z.levels[1].crd, Z.levels[2].crd, Z.vals)
+        a = K.inner_coo3(I, J, Kd, xs, zs)
+        out = TensorStorage(p.out_format, (), [], a)
+        visits = {"k": int(X.vals.numel())}
     else:  # mttkrp
         X, B, C = ops["X"], ops["B"], ops["C"]
         I, J, Kd = X.dims

@@ -143,6 +143,61 @@ def spmm_csr(nrows, ncols, pos, crd, vals, X, Y=None):
     return Y
 
 
+# ---- 3-tensor kernels beyond MTTKRP ---------------------------------------------
+
+def _fibers(crd0, pos1, crd1, pos2, crd2, vals):
+    return (_t(crd0, I32, "crd0"), _t(pos1, I32, "pos1"), _t(crd1, I32, "crd1"),
+            _t(pos2, I32, "pos2"), _t(crd2, I32, "crd2"), _t(vals, F64, "vals"))
+
+
+def ttv_csf(I, J, K, crd0, pos1, crd1, pos2, crd2, vals, v, out="dense"):
+    """TTV over a CSF tensor.  out="dense": (I, J) tensor; out="csr":
+    (pos, crd, vals) with one entry per fiber."""
+    crd0, pos1, crd1, pos2, crd2, vals = _fibers(crd0, pos1, crd1, pos2, crd2, vals)
+    v = _t(v, F64, "v")
+    nf = crd1.numel()
+    sums = torch.empty(nf, dtype=F64, device=vals.device)
+    if nf:
+        spmv_csr(nf, K, pos2, crd2, vals, v, sums)
+    if out == "csr":
+        pos = torch.empty(I + 1, dtype=I32, device=vals.device)
+        _lib.check(L().sl_csf_fiber_rowptr(I, crd0.numel(), P(crd0), P(pos1), P(pos), S()),
+                   "csf_fiber_rowptr")
+        return pos, crd1.clone(), sums
+    Y = torch.empty((I, J), dtype=F64, device=vals.device)
+    _lib.check(L().sl_csf_fiber_scatter_f64(I, J, 1, crd0.numel(), nf, P(crd0), P(pos1), P(crd1),
+                                            P(sums), P(Y), S()), "csf_fiber_scatter")
+    return Y
+
+
+def ttm_csf(I, J, K, crd0, pos1, crd1, pos2, crd2, vals, U):
+    """TTM over a CSF tensor: Y (I, J, R) dense."""
+    crd0, pos1, crd1, pos2, crd2, vals = _fibers(crd0, pos1, crd1, pos2, crd2, vals)
+    U = _t(U, F64, "U")
+    R = U.shape[-1]
+    nf = crd1.numel()
+    rows = torch.empty((nf, R), dtype=F64, device=vals.device)
+    if nf:
+        spmm_csr(nf, K, pos2, crd2, vals, U.view(K, R), rows)
+    Y = torch.empty((I, J, R), dtype=F64, device=vals.device)
+    _lib.check(L().sl_csf_fiber_scatter_f64(I, J, R, crd0.numel(), nf, P(crd0), P(pos1), P(crd1),
+                                            P(rows), P(Y), S()), "csf_fiber_scatter")
+    return Y
+
+
+def inner_coo3(I, J, K, x, z):
+    """a() = X(i,j,k) * Z(i,j,k) over two sorted COO-3 tensors given as
+    (i, j, k, vals) tuples of CUDA tensors; returns a 1-element device tensor."""
+    xi, xj, xk, xv = (_t(t, d, n) for t, d, n in zip(x, (I32, I32, I32, F64), "ijkv"))
+    zi, zj, zk, zv = (_t(t, d, n) for t, d, n in zip(z, (I32, I32, I32, F64), "ijkv"))
+    out = torch.empty(1, dtype=F64, device=xv.device)
+    ws = _ws(L().sl_inner_coo3_workspace_bytes(xi.numel()), xv)
+    _lib.check(L().sl_inner_coo3_f64(I, J, K, xi.numel(), P(xi), P(xj), P(xk), P(xv), zi.numel(),
+                                     P(zi), P(zj), P(zk), P(zv), P(out), P(ws), ws.numel(), S()),
+               "inner_coo3")
+    return out
+
+
 def hashed_slot_map(n, w, crd, ws=None):
     """u64 per coordinate c < n: (probe distance << 32 | slot) of locate(c), ~0 absent."""
     crd = _t(crd, I32, "crd")

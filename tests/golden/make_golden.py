@@ -360,6 +360,56 @@ def spmm_case(name, nrows, ncols, K, rows, cols, vals, X):
     return name, out
 
 
+def dense_tensor(values, dims):
+    fmt = sl.preset("dense", len(dims))
+    lv = [rl.LevelStorage(l, n=n) for l, n in zip(fmt.levels, dims)]
+    return sl.TensorStorage(fmt, tuple(dims), lv, [float(v) for v in np.asarray(values).reshape(-1)])
+
+
+def tensor3_case(name, I, J, K, nnz, R, seed, nnz_z):
+    """TTV (dense and CSR outputs), TTM (dense) and INNERPROD (scalar) on a
+    Zipf-ish 3-tensor, through the reference's evaluate()."""
+    d = wl.mttkrp(I=I, J=J, K=K, nnz=nnz, R=R, seed=seed)
+    data = coordlist((I, J, K), zip(d["i"], d["j"], d["k"]), d["vals"])
+    out = {"I": I, "J": J, "K": K, "R": R}
+    csf = sl.assemble(sl.preset("csf"), (I, J, K), data)
+    for lvl in range(3):
+        out[f"csf_pos{lvl}"] = i32(csf.levels[lvl].pos)
+        out[f"csf_crd{lvl}"] = i32(csf.levels[lvl].crd)
+    out["csf_vals"] = f64(csf.vals)
+    rng = np.random.default_rng(seed + 1)
+    v = rng.uniform(-1, 1, K)
+    v[::7] = -0.0
+    U = rng.uniform(-1, 1, (K, R))
+    out["v"], out["U"] = v, U.reshape(-1)
+    out["ttv_dense"] = f64(sl.evaluate("Y(i,j) = X(i,j,k) * v(k)",
+                                       {"X": csf, "v": dense_tensor(v, (K,))}).vals[:I * J])
+    yc = sl.evaluate("Y(i,j) = X(i,j,k) * v(k)", {"X": csf, "v": dense_tensor(v, (K,))},
+                     sl.preset("csr"))
+    _csr_arrays(yc, "ttv_csr", out)
+    out["ttm_dense"] = f64(sl.evaluate("Y(i,j,r) = X(i,j,k) * U(k,r)",
+                                       {"X": csf, "U": dense_tensor(U, (K, R))}).vals[:I * J * R])
+    # inner product against a second tensor sharing part of the pattern
+    z = wl.mttkrp(I=I, J=J, K=K, nnz=nnz_z, R=R, seed=seed + 50)
+    zi = np.concatenate([d["i"][::3], z["i"]])
+    zj = np.concatenate([d["j"][::3], z["j"]])
+    zk = np.concatenate([d["k"][::3], z["k"]])
+    key = (zi.astype(np.int64) * J + zj) * K + zk
+    key, first = np.unique(key, return_index=True)
+    zv = np.random.default_rng(seed + 2).uniform(-1, 1, len(key))
+    zi, zj, zk = (key // (J * K)), (key // K) % J, key % K
+    Xc = sl.assemble(sl.preset("coo-3"), (I, J, K), data)
+    Zc = sl.assemble(sl.preset("coo-3"), (I, J, K),
+                     coordlist((I, J, K), zip(zi, zj, zk), zv))
+    for tag, T in (("x", Xc), ("z", Zc)):
+        out[f"{tag}_i"] = i32(T.levels[0].crd)
+        out[f"{tag}_j"] = i32(T.levels[1].crd)
+        out[f"{tag}_k"] = i32(T.levels[2].crd)
+        out[f"{tag}_vals"] = f64(T.vals[:len(T.levels[2].crd)])
+    out["inner"] = f64(sl.evaluate("a() = X(i,j,k) * Z(i,j,k)", {"X": Xc, "Z": Zc}).vals)
+    return name, out
+
+
 def widen_cases():
     cases = []
     for seed in range(3):
@@ -380,6 +430,8 @@ def widen_cases():
                           [0, 1, 3], [2.0, -0.0, 1e-300]))
     cases.append(spmm_case("spmm_empty_rows", 4, 3, 2, [1, 1, 3], [0, 2, 1], [1.0, -1.0, 0.5],
                            np.arange(6, dtype=np.float64) - 2.5))
+    cases.append(tensor3_case("t3_small", 9, 11, 13, 300, 3, 41, 200))
+    cases.append(tensor3_case("t3_medium", 40, 50, 60, 6000, 8, 42, 3000))
     return cases
 
 

@@ -176,6 +176,8 @@ def test_oracle_convert_goldens(orc):
 def test_oracle_widen_goldens(orc):
     n_spx = n_spmm = 0
     for name, c in load_cases("widen").items():
+        if name.startswith("t3"):
+            continue
         n = int(c["nrows"])
         if name.startswith("spx"):
             y, _ = orc.spmv_csr_spx(n, c["csr_pos"], c["csr_crd"], c["csr_vals"], c["x_crd"],
@@ -190,3 +192,42 @@ def test_oracle_widen_goldens(orc):
             assert orc.bits_equal(Ymt.reshape(-1), c["Y"]), name
             n_spmm += 1
     assert n_spx >= 4 and n_spmm >= 12
+
+
+def _csf(c):
+    return {k: c[f"csf_{k}"] for k in ("pos0", "crd0", "pos1", "crd1", "pos2", "crd2")}
+
+
+def fiber_coords(c):
+    """(i, j) of every CSF fiber"""
+    pos1 = np.asarray(c["csf_pos1"], np.int64)
+    slice_of = np.repeat(np.arange(len(c["csf_crd0"])), np.diff(pos1))
+    return np.asarray(c["csf_crd0"])[slice_of], np.asarray(c["csf_crd1"])
+
+
+def test_oracle_tensor3_goldens(orc):
+    """TTV (dense, CSR), TTM and INNERPROD restatements vs the reference."""
+    n = 0
+    for name, c in load_cases("widen").items():
+        if not name.startswith("t3"):
+            continue
+        I, J, K, R = (int(c[k]) for k in ("I", "J", "K", "R"))
+        fi, fj = fiber_coords(c)
+        sums, _ = orc.ttv_csf(_csf(c), c["csf_vals"], c["v"])
+        Y = np.zeros(I * J)
+        Y[fi * J + fj] = sums
+        assert orc.bits_equal(Y, c["ttv_dense"]), name
+        assert orc.bits_equal(sums, c["ttv_csr_vals"]), name
+        assert np.array_equal(fj, c["ttv_csr_crd"]), name
+        counts = np.bincount(fi, minlength=I)
+        assert np.array_equal(np.concatenate([[0], np.cumsum(counts)]), c["ttv_csr_pos"]), name
+        rows = orc.ttm_csf(_csf(c), c["csf_vals"], np.asarray(c["U"]).reshape(K, R))
+        Y3 = np.zeros((I * J, R))
+        Y3[fi * J + fj] = rows
+        assert orc.bits_equal(Y3.reshape(-1), c["ttm_dense"]), name
+        x = {k: c[f"x_{k}"] for k in ("i", "j", "k", "vals")}
+        z = {k: c[f"z_{k}"] for k in ("i", "j", "k", "vals")}
+        a, _ = orc.inner_coo3(x, z)
+        assert orc.bits_equal(np.array([a]), c["inner"]), name
+        n += 1
+    assert n == 2
