@@ -435,6 +435,95 @@ def widen_cases():
     return cases
 
 
+# ---------------------------------------------------------------------------
+# assembly (formats.assemble) and file readers (io.read_mtx / read_tns)
+
+def _storage_arrays(st, prefix, out):
+    for k, lv in enumerate(st.levels):
+        for attr in ("pos", "crd", "offset"):
+            a = getattr(lv, attr, None)
+            if a is not None and len(a):
+                out[f"{prefix}_l{k}_{attr}"] = i32(a)
+        if getattr(lv, "n", None) is not None:
+            out[f"{prefix}_l{k}_n"] = int(lv.n)
+        if getattr(lv, "w", None):
+            out[f"{prefix}_l{k}_w"] = int(lv.w)
+    out[f"{prefix}_vals"] = f64(st.vals)
+
+
+def assembly_case(name, dims, coords, vals, fmts, **kw):
+    out = {"dims": np.array(dims), "coords": np.asarray(coords, np.int64).reshape(-1, len(dims)),
+           "vals": f64(vals)}
+    data = sl.CoordList(tuple(dims), [(tuple(int(x) for x in c), float(v))
+                                      for c, v in zip(out["coords"], out["vals"])])
+    for f in fmts:
+        st = sl.assemble(sl.preset(f, **kw.get(f, {})) if f in kw else sl.preset(f), tuple(dims),
+                         data)
+        _storage_arrays(st, f.replace("-", "_"), out)
+    return name, out
+
+
+def assembly_cases():
+    cases = []
+    rng = np.random.default_rng(77)
+    n, m, nnz = 12, 9, 60
+    c = np.stack([rng.integers(0, n, nnz), rng.integers(0, m, nnz)], 1)
+    v = rng.uniform(-1, 1, nnz)
+    v[::9] = 0.0
+    v[::11] = -0.0
+    c[5] = c[3]                      # explicit duplicates, in file order
+    c[40] = c[3]
+    cases.append(assembly_case("asm_mat", (n, m), c, v,
+                               ["coo-soa", "csr", "ell", "dia", "hash-vector"][:4]))
+    cases.append(assembly_case("asm_ell_declared", (n, m), c, v, ["ell"], ell={"slots": 12}))
+    vec_c = rng.integers(0, 40, (25, 1))
+    cases.append(assembly_case("asm_vec", (40,), vec_c, rng.uniform(-1, 1, 25),
+                               ["sparse-vector", "hash-vector", "dense"]))
+    t = np.stack([rng.integers(0, 5, 80), rng.integers(0, 6, 80), rng.integers(0, 7, 80)], 1)
+    tv = rng.uniform(-1, 1, 80)
+    tv[::13] = 0.0
+    cases.append(assembly_case("asm_t3", (5, 6, 7), t, tv, ["coo-3", "csf"]))
+    cases.append(assembly_case("asm_empty", (4, 5), np.zeros((0, 2), np.int64), [],
+                               ["coo-soa", "csr", "ell", "dia"]))
+    return cases
+
+
+def io_cases():
+    from sparselevels import io as rio
+    import tempfile
+    texts = {
+        "mtx_real": ("mtx", "%%MatrixMarket matrix coordinate real general\n% c\n3 4 4\n"
+                            "1 1 1.5\n3 4 -2\n2 2 0\n1 1 0.25\n"),
+        "mtx_pattern": ("mtx", "%%MatrixMarket matrix coordinate pattern general\n2 2 2\n1 2\n2 1\n"),
+        "mtx_int": ("mtx", "%%MatrixMarket matrix coordinate integer general\n\n2 3 1\n2 3 7\n"),
+        "mtx_bad_sym": ("mtx", "%%MatrixMarket matrix coordinate real symmetric\n2 2 1\n1 1 1\n"),
+        "mtx_bad_count": ("mtx", "%%MatrixMarket matrix coordinate real general\n2 2 2\n1 1 1\n"),
+        "mtx_out_of_range": ("mtx", "%%MatrixMarket matrix coordinate real general\n2 2 1\n3 1 1\n"),
+        "mtx_no_header": ("mtx", "2 2 1\n1 1 1\n"),
+        "mtx_bad_field": ("mtx", "%%MatrixMarket matrix coordinate complex general\n1 1 1\n1 1 1 0\n"),
+        "tns_basic": ("tns", "# t\n1 1 1 1.0\n2 3 1 -2.5\n1 1 1 0.5\n"),
+        "tns_bad_order": ("tns", "1 1 1 1.0\n1 1 2.0\n"),
+        "tns_zero_based": ("tns", "0 1 1 1.0\n"),
+    }
+    out = {}
+    with tempfile.TemporaryDirectory() as d:
+        for name, (kind, text) in texts.items():
+            path = f"{d}/{name}.{kind}"
+            with open(path, "w") as fh:
+                fh.write(text)
+            rec = {"kind": kind, "text": text}
+            try:
+                cl = rio.read_mtx(path) if kind == "mtx" else rio.read_tns(path)
+                rec["dims"] = np.array(cl.dims)
+                rec["coords"] = np.array([c for c, _ in cl.entries], np.int64).reshape(
+                    -1, len(cl.dims))
+                rec["vals"] = f64([v for _, v in cl.entries])
+            except rio.FileFormatError as exc:
+                rec["error"] = str(exc).replace(d + "/", "")
+            out[name] = rec
+    return list(out.items())
+
+
 def level_kats():
     """Run the reference level functions on the test_levels.py fixtures."""
     E = rl.EMPTY
@@ -568,6 +657,8 @@ def main():
         "mttkrp": mttkrp_cases(),
         "convert": convert_cases(),
         "widen": widen_cases(),
+        "assembly": assembly_cases(),
+        "io": io_cases(),
     }
     for group, cases in groups.items():
         flat = {}
