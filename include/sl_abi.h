@@ -322,6 +322,11 @@ int sl_convert_coo_to_dia_values(int64_t nrows, int64_t ncols, int64_t nnz, int3
                                  const int32_t* rows, const int32_t* cols, const double* vals,
                                  double* dia_vals, void* ws, size_t ws_bytes, void* stream);
 
+/* CSR -> COO-SoA row coordinates (rows[p] = i for p in [pos[i], pos[i+1])):
+ * with the A+B entry points (empty B) this is the identity copy into COO and
+ * the COO output of a gather-append (engine.py:330-434). */
+int sl_csr_row_indices(int64_t nrows, const int32_t* pos, int32_t* rows, void* stream);
+
 /* ---- utilities used by the benchmark ------------------------------------- */
 /* Writes `bytes` of junk into `buf` to evict L2 between timed iterations. */
 int sl_l2_flush(void* buf, size_t bytes, void* stream);

@@ -95,6 +95,7 @@ SIGNATURES = {
     "sl_inner_coo3_workspace_bytes": ([_i64], _sz),
     "sl_inner_coo3_f64": ([_i64, _i64, _i64, _i64, _p, _p, _p, _p, _i64, _p, _p, _p, _p, _p, _p,
                            _sz, _p], ctypes.c_int),
+    "sl_csr_row_indices": ([_i64, _p, _p, _p], ctypes.c_int),
     "sl_l2_flush": ([_p, _sz, _p], ctypes.c_int),
 }
 

@@ -116,6 +116,14 @@ __global__ void dia_scatter_kernel(int64_t nnz, int64_t nrows, const int32_t* __
   }
 }
 
+// COO row coordinates of a CSR matrix: rows[p] = i for p in [pos[i], pos[i+1])
+__global__ void csr_rows_kernel(int64_t nrows, const int32_t* __restrict__ pos,
+                                int32_t* __restrict__ rows) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nrows; i += stride)
+    for (int32_t p = ldg(pos + i); p < ldg(pos + i + 1); ++p) rows[p] = (int32_t)i;
+}
+
 __global__ void fill_zero_f64_kernel(double* __restrict__ a, int64_t n) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
@@ -203,5 +211,13 @@ extern "C" int sl_convert_coo_to_dia_values(int64_t nrows, int64_t ncols, int64_
   if (nnz > 0)
     dia_scatter_kernel<<<min(ceil_div(nnz, 256), 8 * sl_host::sm_count()), 256, 0, s>>>(
         nnz, nrows, rows, cols, vals, index, dvals);
+  return sl_host::launch_status();
+}
+
+extern "C" int sl_csr_row_indices(int64_t nrows, const int32_t* pos, int32_t* rows, void* stream) {
+  if (nrows < 0 || !pos) return SL_ERR_INVALID;
+  if (nrows == 0) return SL_OK;
+  csr_rows_kernel<<<min(ceil_div(nrows, 256), 16 * sl_host::sm_count()), 256, 0,
+                    as_stream(stream)>>>(nrows, pos, rows);
   return sl_host::launch_status();
 }

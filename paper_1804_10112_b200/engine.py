@@ -193,17 +193,18 @@ def plan(checked: CheckedExpr, bindings, out_format: TensorFormat,
     if isinstance(rhs, Add) and all(isinstance(t, Access) for t in (rhs.left, rhs.right)):
         L_, R_ = rhs.left, rhs.right
         if len(lhs.ivars) == 2 and L_.ivars == lhs.ivars and R_.ivars == lhs.ivars:
-            if ocls != "csr":
+            if ocls not in ("csr", "coo"):
                 raise UnsupportedOutputError(
-                    f"A + B is assembled as CSR (gather-append); got {out_format.describe()}")
+                    f"A + B is assembled by gather-append into CSR or COO; got "
+                    f"{out_format.describe()}")
             cl, cr = cls[L_.tensor], cls[R_.tensor]
-            # a + b == b + a bit-for-bit, so the CSR operand can take either side
-            if cl == "csr" and cr in ("coo", "csr"):
-                return Plan("add", f"add_csr_{cr}", {"A": L_.tensor, "B": R_.tensor},
-                            out_format, out_dims)
-            if cr == "csr" and cl == "coo":
-                return Plan("add", "add_csr_coo", {"A": R_.tensor, "B": L_.tensor},
-                            out_format, out_dims)
+            if cl in ("csr", "coo") and cr in ("csr", "coo"):
+                # a + b == b + a bit-for-bit: keep a CSR operand (if any) as A and
+                # a COO one as B, whose duplicate coordinates the kernels group
+                A_, B_ = (L_, R_) if (cl == "csr" or cr == "coo") else (R_, L_)
+                ca = cls[A_.tensor]
+                return Plan("add", f"add_{ca}_{cls[B_.tensor]}_{ocls}",
+                            {"A": A_.tensor, "B": B_.tensor}, out_format, out_dims)
             raise UnsupportedMergeError(f"no B200 kernel for A + B with {cl} + {cr}")
 
     # ---- A(i,r) = X(i,j,k) * B(j,r) * C(k,r), association (X*B)*C
@@ -301,16 +302,29 @@ def _run(p: Plan, inputs: Dict[str, TensorStorage], stats: Optional[EvalStats]):
     elif p.pattern == "add":
         A, B = ops["A"], ops["B"]
         nrows = A.dims[0]
-        if p.kernel == "add_csr_coo":
-            c_pos, c_crd, c_vals = K.add_csr(nrows, A.levels[1].pos, A.levels[1].crd, A.vals,
-                                             B.levels[1].crd, B.vals, b_rows=B.levels[0].crd)
+        _, ka, kb, ko = p.kernel.split("_")
+        if ka == "coo":          # COO A (possibly duplicated): its exact CSR copy
+            a_pos, a_crd, a_vals = K.coo_to_csr(nrows, A.levels[0].crd, A.levels[1].crd, A.vals)
         else:
-            c_pos, c_crd, c_vals = K.add_csr(nrows, A.levels[1].pos, A.levels[1].crd, A.vals,
-                                             B.levels[1].crd, B.vals, b_pos=B.levels[1].pos)
+            a_pos, a_crd, a_vals = A.levels[1].pos, A.levels[1].crd, A.vals
+        if kb == "coo":
+            c_pos, c_crd, c_vals = K.add_csr(nrows, a_pos, a_crd, a_vals, B.levels[1].crd, B.vals,
+                                             b_rows=B.levels[0].crd)
+        else:
+            c_pos, c_crd, c_vals = K.add_csr(nrows, a_pos, a_crd, a_vals, B.levels[1].crd, B.vals,
+                                             b_pos=B.levels[1].pos)
         f = p.out_format
-        out = TensorStorage(f, A.dims, [LevelStorage(f.levels[0], n=nrows, device=dev),
-                                        LevelStorage(f.levels[1], pos=c_pos, crd=c_crd,
-                                                     device=dev)], c_vals)
+        if ko == "csr":
+            out = TensorStorage(f, A.dims, [LevelStorage(f.levels[0], n=nrows, device=dev),
+                                            LevelStorage(f.levels[1], pos=c_pos, crd=c_crd,
+                                                         device=dev)], c_vals)
+        else:
+            rows = K.csr_rows(nrows, c_pos, c_crd.numel())
+            nnz = int(c_crd.numel())
+            out = TensorStorage(f, A.dims, [LevelStorage(f.levels[0], pos=[0, nnz], crd=rows,
+                                                         device=dev),
+                                            LevelStorage(f.levels[1], crd=c_crd, device=dev)],
+                                c_vals)
         visits = {"i": nrows, "j": int(c_crd.numel())}
     elif p.pattern == "spmm":
         A, X = ops["A"], ops["X"]

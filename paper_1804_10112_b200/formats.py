@@ -304,6 +304,7 @@ def convert(src: TensorStorage, dst: TensorFormat) -> TensorStorage:
       CSR -> ELL : reorder writer + assemble — exact zeros dropped, 0.0 + v
       COO -> ELL : COO -> CSR -> ELL (same values as the direct copy)
       COO -> DIA : reorder writer + assemble (unique coordinates)
+      CSR -> COO : gather-append copy (0.0 + v, explicit zeros kept)
     Other pairs raise UnsupportedOutputError (no CPU interpretation)."""
     from . import kernels as K
     from .engine import format_class
@@ -323,6 +324,10 @@ def convert(src: TensorStorage, dst: TensorFormat) -> TensorStorage:
         l1 = src.levels[1]
         nslots, ecrd, evals = K.csr_to_ell(n, l1.pos, l1.crd, src.vals)
         return ell_storage(nslots, ecrd, evals, dims, device=dev)
+    if s == "csr" and d == "coo":
+        l1 = src.levels[1]
+        rows, cols, vals = K.csr_to_coo(n, l1.pos, l1.crd, src.vals)
+        return coo_storage(rows, cols, vals, dims, device=dev)
     if s == "coo" and d == "dia":
         offs, dvals = K.coo_to_dia(n, m, src.levels[0].crd, src.levels[1].crd, src.vals)
         return dia_storage(offs.cpu().numpy(), dvals, dims, device=dev)

@@ -285,6 +285,26 @@ def coo_to_csr(nrows, rows, cols, vals, sync=True, two_pass=True):
                    two_pass=two_pass)
 
 
+def csr_rows(nrows, pos, nnz=None):
+    """COO row coordinates of a CSR structure."""
+    pos = _t(pos, I32, "pos")
+    nnz = int(pos[nrows].item()) if nnz is None else nnz
+    rows = torch.empty(nnz, dtype=I32, device=pos.device)
+    _lib.check(L().sl_csr_row_indices(nrows, P(pos), P(rows), S()), "csr_rows")
+    return rows
+
+
+def csr_to_coo(nrows, pos, crd, vals):
+    """CSR -> COO-SoA exactly as the identity copy: gather-append of 0.0 + v
+    (the A+B kernels with an empty B), explicit zeros kept."""
+    pos, crd, vals = _t(pos, I32, "pos"), _t(crd, I32, "crd"), _t(vals, F64, "vals")
+    e_i = torch.empty(0, dtype=I32, device=pos.device)
+    e_f = torch.empty(0, dtype=F64, device=pos.device)
+    b_pos = torch.zeros(nrows + 1, dtype=I32, device=pos.device)
+    c_pos, c_crd, c_vals = add_csr(nrows, pos, crd, vals, e_i, e_f, b_pos=b_pos)
+    return csr_rows(nrows, c_pos, c_crd.numel()), c_crd, c_vals
+
+
 def coo_rowptr(nrows, rows, pos=None):
     """Structural part alone: the row pointer of a row-sorted COO."""
     rows = _t(rows, I32, "rows")

@@ -524,6 +524,51 @@ def io_cases():
     return list(out.items())
 
 
+# ---------------------------------------------------------------------------
+# general gather-append outputs: A + B over any CSR/COO
+# operands into CSR or COO-SoA, and convert CSR -> COO
+
+def _coo_arrays(st, prefix, out):
+    out[f"{prefix}_rows"] = i32(st.levels[0].crd)
+    out[f"{prefix}_cols"] = i32(st.levels[1].crd)
+    out[f"{prefix}_vals"] = f64(st.vals[:len(st.levels[1].crd)] if st.levels[1].crd else [])
+
+
+def addx_case(name, n, m, a, b, fa, fb):
+    A = sl.assemble(sl.preset(fa), (n, m), coordlist((n, m), zip(a[0], a[1]), a[2]))
+    B = sl.assemble(sl.preset(fb), (n, m), coordlist((n, m), zip(b[0], b[1]), b[2]))
+    out = {"nrows": n, "ncols": m, "fa": fa, "fb": fb}
+    for tag, T, f in (("a", A, fa), ("b", B, fb)):
+        if f == "csr":
+            _csr_arrays(T, tag, out)
+        else:
+            _coo_arrays(T, tag, out)
+    Cc = sl.evaluate("C(i,j) = A(i,j) + B(i,j)", {"A": A, "B": B}, sl.preset("csr"))
+    _csr_arrays(Cc, "c_csr", out)
+    Co = sl.evaluate("C(i,j) = A(i,j) + B(i,j)", {"A": A, "B": B}, sl.preset("coo-soa"))
+    _coo_arrays(Co, "c_coo", out)
+    if fa == "csr":
+        _coo_arrays(rf.convert(A, sl.preset("coo-soa")), "a_to_coo", out)
+    return name, out
+
+
+def addx_cases():
+    cases = []
+    rng = np.random.default_rng(91)
+    for seed, (fa, fb) in enumerate((("coo-soa", "coo-soa"), ("csr", "csr"), ("coo-soa", "csr"),
+                                      ("csr", "coo-soa"))):
+        n, m, k = 25, 20, 120
+        a = [np.sort(rng.integers(0, n, k)), rng.integers(0, m, k), rng.uniform(-1, 1, k)]
+        b = [np.sort(rng.integers(0, n, k)), rng.integers(0, m, k), rng.uniform(-1, 1, k)]
+        for x in (a, b):
+            o = np.lexsort((x[1], x[0]))
+            x[0], x[1], x[2] = x[0][o], x[1][o], x[2][o]
+            x[2][::10] = 0.0
+            x[2][::17] = -0.0
+        cases.append(addx_case(f"addx_{seed}", n, m, a, b, fa, fb))
+    return cases
+
+
 def level_kats():
     """Run the reference level functions on the test_levels.py fixtures."""
     E = rl.EMPTY
@@ -659,6 +704,7 @@ def main():
         "widen": widen_cases(),
         "assembly": assembly_cases(),
         "io": io_cases(),
+        "addx": addx_cases(),
     }
     for group, cases in groups.items():
         flat = {}

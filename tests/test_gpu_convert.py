@@ -135,4 +135,50 @@ def test_convert_dia7_full_size():
 def test_convert_unsupported_pair():
     st = sl.csr_storage(np.array([0, 1], np.int32), np.array([0], np.int32), np.array([1.0]), (1, 1))
     with pytest.raises(sl.UnsupportedOutputError):
-        sl.convert(st, sl.preset("coo-soa"))
+        sl.convert(st, sl.preset("dia"))
+
+
+# ---------------------------------------------------------------------------
+# general gather-append outputs: A + B over CSR/COO operands into CSR or COO,
+# and convert CSR -> COO, against the reference's evaluate()/convert()
+
+def _storage(c, tag, fmt, dims):
+    if fmt == "csr":
+        return sl.csr_storage(c[f"{tag}_pos"], c[f"{tag}_crd"], c[f"{tag}_vals"], dims)
+    return sl.coo_storage(c[f"{tag}_rows"], c[f"{tag}_cols"], c[f"{tag}_vals"], dims)
+
+
+def test_add_any_operands_any_output():
+    for name, c in load_cases("addx").items():
+        n, m = int(c["nrows"]), int(c["ncols"])
+        fa, fb = str(c["fa"]), str(c["fb"])
+        A, B = _storage(c, "a", fa, (n, m)), _storage(c, "b", fb, (n, m))
+        for expr in ("C(i,j) = A(i,j) + B(i,j)", "C(i,j) = B(i,j) + A(i,j)"):
+            C = sl.evaluate(expr, {"A": A, "B": B}, sl.preset("csr"))
+            assert np.array_equal(host(C.levels[1].pos), c["c_csr_pos"]), (name, expr)
+            assert np.array_equal(host(C.levels[1].crd), c["c_csr_crd"]), (name, expr)
+            assert np.array_equal(bits(C.vals), bits(c["c_csr_vals"])), (name, expr)
+            Co = sl.evaluate(expr, {"A": A, "B": B}, sl.preset("coo-soa"))
+            assert np.array_equal(host(Co.levels[0].crd), c["c_coo_rows"]), (name, expr)
+            assert np.array_equal(host(Co.levels[1].crd), c["c_coo_cols"]), (name, expr)
+            assert np.array_equal(bits(Co.vals), bits(c["c_coo_vals"])), (name, expr)
+        if fa == "csr":
+            coo = sl.convert(A, sl.preset("coo-soa"))
+            assert np.array_equal(host(coo.levels[0].crd), c["a_to_coo_rows"]), name
+            assert np.array_equal(host(coo.levels[1].crd), c["a_to_coo_cols"]), name
+            assert np.array_equal(bits(coo.vals), bits(c["a_to_coo_vals"])), name
+
+
+def test_assemble_on_device_then_evaluate(orc, tmp_path):
+    """io -> assemble (device) -> evaluate: the files-to-result path."""
+    from paper_1804_10112_b200 import io as IO
+    d = wl.coo_spmv(n=3000, nnz=30000, seed=5)
+    data = sl.CoordList((3000, 3000), np.stack([d["rows"], d["cols"]], 1), d["vals"])
+    IO.write_mtx(data, str(tmp_path / "a.mtx"))
+    back = IO.read_mtx(str(tmp_path / "a.mtx"))
+    x = sl.dense_storage(d["x"])
+    ref, _ = orc.spmv_coo(3000, d["rows"], d["cols"], d["vals"], d["x"])
+    for fmt in ("coo-soa", "csr", "ell", "dia"):
+        A = sl.assemble(fmt, (3000, 3000), back)
+        y = sl.evaluate("y(i) = A(i,j) * x(j)", {"A": A, "x": x})
+        assert np.array_equal(bits(y.vals), bits(ref)), fmt

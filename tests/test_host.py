@@ -205,13 +205,15 @@ def test_plan_dispatch_and_errors():
         plan("y(i) = A(i,j) * x(j)", {"A": _st("csr", (3, 4)), "x": x}, F.preset("sv"))
     A, B = _st("csr", (3, 4)), _st("coo-soa", (3, 4))
     p = plan("C(i,j) = B(i,j) + A(i,j)", {"A": A, "B": B}, F.preset("csr"))
-    assert p.kernel == "add_csr_coo" and p.operands == {"A": "A", "B": "B"}
+    assert p.kernel == "add_csr_coo_csr" and p.operands == {"A": "A", "B": "B"}
     assert plan("C(i,j) = A(i,j) + B(i,j)", {"A": A, "B": _st("csr", (3, 4))},
-                F.preset("csr")).kernel == "add_csr_csr"
+                F.preset("csr")).kernel == "add_csr_csr_csr"
+    assert plan("C(i,j) = A(i,j) + B(i,j)", {"A": B, "B": B},
+                F.preset("coo-soa")).kernel == "add_coo_coo_coo"
     with pytest.raises(UnsupportedOutputError):
         plan("C(i,j) = A(i,j) + B(i,j)", {"A": A, "B": B})
     with pytest.raises(UnsupportedMergeError):
-        plan("C(i,j) = A(i,j) + B(i,j)", {"A": B, "B": B}, F.preset("csr"))
+        plan("C(i,j) = A(i,j) + B(i,j)", {"A": _st("ell", (3, 4)), "B": B}, F.preset("csr"))
     X, Bd, Cd = _st("coo-3", (5, 6, 7)), _st("dense-2", (6, 3)), _st("dense-2", (7, 3))
     for expr in ("A(i,r) = X(i,j,k) * B(j,r) * C(k,r)", "A(i,r) = B(j,r) * X(i,j,k) * C(k,r)",
                  "A(i,r) = C(k,r) * (X(i,j,k) * B(j,r))"):
