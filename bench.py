@@ -159,26 +159,39 @@ class KernelTimer:
         self.torch = torch
         self.K = K
         self.flush = torch.empty(int(flush_bytes), dtype=torch.uint8, device="cuda")
+        # "write+read" (default): the write sweep is followed by a read sweep of
+        # another 2x-L2 buffer, so the timed kernel starts with a cold AND clean
+        # L2 (no write-backs of the flush's dirty lines charged to it);
+        # SL_BENCH_FLUSH=write keeps only the write sweep
+        self.mode = os.environ.get("SL_BENCH_FLUSH", "write+read")
+        self.rbuf = (torch.zeros(int(flush_bytes), dtype=torch.uint8, device="cuda")
+                     if self.mode == "write+read" else None)
+        self.sink = torch.zeros(1, dtype=torch.int32, device="cuda")
         self.launches = 0
+
+    def _flush(self):
+        self.K.l2_flush(self.flush)
+        if self.rbuf is not None:
+            self.K.l2_read(self.rbuf, self.sink)
 
     def run(self, fns, steps, warmup):
         """fns: {name: callable}; returns {name: [ms per step]}"""
         torch, K = self.torch, self.K
         for _ in range(warmup):
             for fn in fns.values():
-                K.l2_flush(self.flush)
+                self._flush()
                 fn()
         torch.cuda.synchronize()
         evs = {n: [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
                    for _ in range(steps)] for n in fns}
         for s in range(steps):
             for n, fn in fns.items():
-                K.l2_flush(self.flush)
+                self._flush()
                 e0, e1 = evs[n][s]
                 e0.record()
                 fn()
                 e1.record()
-                self.launches += 2
+                self.launches += 3 if self.rbuf is not None else 2   # flush sweep(s) + kernel
         torch.cuda.synchronize()
         return {n: [e0.elapsed_time(e1) for e0, e1 in evs[n]] for n in fns}
 
@@ -237,7 +250,7 @@ def run_ours(args, rank, world, local_rank):
     t_total = D.max_over_ranks(t_csr + t_ell, dev)          # ms over K steps, max over ranks
     bytes_all = D.sum_over_ranks(float(b_csr + b_ell) * args.steps, dev)
     value = bytes_all / (t_total * 1e-3) / 1e9
-    launches = timer.launches // 2 * 2                       # flush + SpMV per timed launch
+    launches = timer.launches                                # flush sweep(s) + SpMV per launch
 
     # roofline: dominant kernel of the step
     avg = {"csr": t_csr / args.steps, "ell": t_ell / args.steps}
@@ -284,7 +297,9 @@ def run_ours(args, rank, world, local_rank):
         "config": {"workload": WORKLOAD, "grid": f"{G}x{G}x{G * world}",
                    "rows_per_gpu": nrows, "nnz_per_gpu": nnz, "ell_slots": S,
                    "step": "CSR SpMV + ELL SpMV, each after an L2 flush",
-                   "l2": f"flushed before every launch ({2 * l2_bytes(torch) >> 20} MiB write)",
+                   "l2": (f"flushed before every launch ({2 * l2_bytes(torch) >> 20} MiB write sweep"
+               + (f" + {2 * l2_bytes(torch) >> 20} MiB read sweep: cold and clean)"
+                  if timer.mode == "write+read" else ")")),
                    "parallelism": f"row-block shards x{world}, x replicated (NCCL broadcast)"},
         "pct_of_peak": round(100.0 * value / (peak * world), 2),
         "per_kernel_ms": {k: round(v, 6) for k, v in avg.items()},

@@ -330,6 +330,9 @@ int sl_csr_row_indices(int64_t nrows, const int32_t* pos, int32_t* rows, void* s
 /* ---- utilities used by the benchmark ------------------------------------- */
 /* Writes `bytes` of junk into `buf` to evict L2 between timed iterations. */
 int sl_l2_flush(void* buf, size_t bytes, void* stream);
+/* Read-only sweep of `bytes` (>= the L2 size): evicts L2 and leaves it clean,
+ * so the next kernel starts cold without paying for earlier write-backs. */
+int sl_l2_read(const void* buf, size_t bytes, void* sink, void* stream);
 
 #ifdef __cplusplus
 }

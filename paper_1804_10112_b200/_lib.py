@@ -97,6 +97,7 @@ SIGNATURES = {
                            _sz, _p], ctypes.c_int),
     "sl_csr_row_indices": ([_i64, _p, _p, _p], ctypes.c_int),
     "sl_l2_flush": ([_p, _sz, _p], ctypes.c_int),
+    "sl_l2_read": ([_p, _sz, _p, _p], ctypes.c_int),
 }
 
 _LIB = None

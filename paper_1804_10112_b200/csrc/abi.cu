@@ -73,6 +73,19 @@ __global__ void l2_flush_kernel(uint4* __restrict__ buf, size_t n, uint32_t salt
     buf[i] = make_uint4((uint32_t)i ^ salt, salt, (uint32_t)(i >> 7), ~salt);
 }
 
+// read-only sweep: evicts whatever L2 holds (writing dirty lines back now)
+// and leaves clean lines of `buf`, so a following kernel starts cold without
+// paying for someone else's write-backs
+__global__ void l2_read_kernel(const uint4* __restrict__ buf, size_t n, uint32_t* __restrict__ sink) {
+  uint32_t acc = 0;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
+       i += (size_t)gridDim.x * blockDim.x) {
+    const uint4 v = __ldcg(buf + i);
+    acc ^= v.x ^ v.y ^ v.z ^ v.w;
+  }
+  if (acc == 0x9e3779b9u) *sink = acc;
+}
+
 }  // namespace sl
 
 using namespace sl;
@@ -158,6 +171,15 @@ extern "C" int sl_level_query(const sl_level* lv, int32_t fn, int64_t nq, const 
     default:
       return SL_ERR_INVALID;
   }
+  return sl_host::launch_status();
+}
+
+extern "C" int sl_l2_read(const void* buf, size_t bytes, void* sink, void* stream) {
+  if (!buf || !sink) return SL_ERR_INVALID;
+  const size_t n = bytes / sizeof(uint4);
+  if (n == 0) return SL_OK;
+  sl::l2_read_kernel<<<4 * sl_host::sm_count(), 512, 0, sl_host::as_stream(stream)>>>(
+      static_cast<const uint4*>(buf), n, static_cast<uint32_t*>(sink));
   return sl_host::launch_status();
 }
 

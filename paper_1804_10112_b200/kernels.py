@@ -385,3 +385,8 @@ def mttkrp_csf(I, J, K, crd0, pos1, crd1, pos2, crd2, vals, B, C, A=None, ws=Non
 def l2_flush(buf):
     buf = _t(buf, torch.uint8, "buf")
     _lib.check(L().sl_l2_flush(P(buf), buf.numel(), S()), "l2_flush")
+
+
+def l2_read(buf, sink):
+    buf = _t(buf, torch.uint8, "buf")
+    _lib.check(L().sl_l2_read(P(buf), buf.numel(), P(sink), S()), "l2_read")
