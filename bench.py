@@ -261,23 +261,32 @@ def run_ours(args, rank, world, local_rank):
     traffic = traffic_db.get(kname)
 
     # ---- e2e through the public API: x from pinned host memory each step,
-    # the matrix resident on the device (like weights), y read back.
+    # the matrix resident on the device (like weights), y read back.  Steps
+    # alternate between two streams (and two pinned x / y buffers), so step
+    # k+1's host->device copy overlaps step k's kernel and device->host copy —
+    # a serving loop's pipelining; every step still moves its own x in and y out.
     A_st = F.csr_storage(pos, crd, vals, (nrows, ncols), device=dev)
-    x_host = torch.as_tensor(st["x"]).pin_memory()
-    xs = F.dense_storage(x_host, device=None)
-    y_host = torch.empty(nrows, dtype=torch.float64).pin_memory()
+    x_hosts = [torch.as_tensor(st["x"]).pin_memory() for _ in range(2)]
+    xs = [F.dense_storage(xh, device=None) for xh in x_hosts]
+    y_hosts = [torch.empty(nrows, dtype=torch.float64).pin_memory() for _ in range(2)]
+    streams = [torch.cuda.Stream(device=dev) for _ in range(2)]
     expr = "y(i) = A(i,j) * x(j)"
-    for _ in range(max(args.warmup, 3)):
-        y_host.copy_(evaluate(expr, {"A": A_st, "x": xs}).vals, non_blocking=True)
+
+    def e2e_step(k):
+        with torch.cuda.stream(streams[k % 2]):
+            y_dev = evaluate(expr, {"A": A_st, "x": xs[k % 2]}).vals
+            y_hosts[k % 2].copy_(y_dev, non_blocking=True)
+
+    for k in range(max(args.warmup, 3)):
+        e2e_step(k)
     torch.cuda.synchronize()
     e2e_steps = max(10, min(args.steps, 200))
     if world > 1:
         dist.barrier()
     t0 = time.perf_counter()
-    for _ in range(e2e_steps):
-        y_dev = evaluate(expr, {"A": A_st, "x": xs}).vals
-        y_host.copy_(y_dev, non_blocking=True)
-        torch.cuda.current_stream().synchronize()
+    for k in range(e2e_steps):
+        e2e_step(k)
+    torch.cuda.synchronize()
     t_e2e = D.max_over_ranks((time.perf_counter() - t0) / e2e_steps, dev)
     e2e_val = D.sum_over_ranks(float(b_csr), dev) / t_e2e / 1e9
 
@@ -310,11 +319,11 @@ def run_ours(args, rank, world, local_rank):
                      "frac": round(achieved / peak, 4), "algorithmic_bytes": dom_bytes,
                      "traffic": traffic},
         "e2e": {"value": round(e2e_val, 3), "unit": "GB/s",
-                "h2d_bytes_per_step": int(x_host.numel() * 8),
+                "h2d_bytes_per_step": int(x_hosts[0].numel() * 8),
                 "d2h_bytes_per_step": int(nrows * 8),
                 "ms_per_step": round(t_e2e * 1e3, 4),
-                "path": "evaluate('y(i) = A(i,j) * x(j)') CSR, pinned host x in, y out; "
-                        "matrix resident in HBM"},
+                "path": "evaluate('y(i) = A(i,j) * x(j)') CSR, pinned host x in, y out every "
+                        "step; matrix resident in HBM; steps alternate over 2 streams"},
         "gpu_launches": launches,
         "clocks": clk.summary(),
     }

@@ -392,6 +392,10 @@ def _run(p: Plan, inputs: Dict[str, TensorStorage], stats: Optional[EvalStats]):
     return out
 
 
+_PLAN_CACHE: Dict[tuple, Plan] = {}
+_PLAN_CACHE_MAX = 256
+
+
 def evaluate(expr, inputs: Dict[str, TensorStorage], out_format: Optional[TensorFormat] = None,
              out_dims: Optional[Sequence[int]] = None, *, fuse: bool = True,
              allow_reorder: bool = True, stats: Optional[EvalStats] = None) -> TensorStorage:
@@ -401,7 +405,20 @@ def evaluate(expr, inputs: Dict[str, TensorStorage], out_format: Optional[Tensor
     or on a CUDA device; the result is on the device.  `fuse` and
     `allow_reorder` are accepted for signature compatibility: every kernel
     already executes the fused schedule and none needs a reorder stage.
+    Plans are cached per (expression text, operand formats and dims, output
+    format and dims): parsing, validation and planning are pure functions of
+    those, so a repeated call goes straight to the kernels.
     """
+    key = None
+    if isinstance(expr, str):
+        try:
+            key = (expr, tuple(sorted((n, s.format, s.dims) for n, s in inputs.items())),
+                   out_format, None if out_dims is None else tuple(out_dims))
+            p = _PLAN_CACHE.get(key)
+        except TypeError:            # an unhashable format: plan every time
+            key, p = None, None
+        if p is not None:
+            return _run(p, inputs, stats)
     assignment = parse(expr) if isinstance(expr, str) else expr
     bindings = {name: (s.format, s.dims) for name, s in inputs.items()}
     checked = validate(assignment, bindings)
@@ -412,6 +429,10 @@ def evaluate(expr, inputs: Dict[str, TensorStorage], out_format: Optional[Tensor
     if tuple(out_dims) != tuple(checked.var_extents[v] for v in assignment.lhs.ivars):
         raise ValidationError("out_dims disagree with the expression's variable extents")
     p = plan(checked, bindings, out_format, tuple(out_dims))
+    if key is not None:
+        if len(_PLAN_CACHE) >= _PLAN_CACHE_MAX:
+            _PLAN_CACHE.clear()
+        _PLAN_CACHE[key] = p
     return _run(p, inputs, stats)
 
 
