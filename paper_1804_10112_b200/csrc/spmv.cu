@@ -41,17 +41,16 @@ __global__ void fill_zero_kernel(double* __restrict__ y, int64_t n) {
 // later row's start: y needs no memset.  (engine.py:636-713 run_fused over the
 // COO chain, _ScatterWriter engine.py:281-320.)
 
-constexpr int kCooThreads = 256;
 constexpr int kCooVec = 4;                       // elements per vector load
-constexpr int kCooVecPerThread = 2;
-constexpr int kCooIpt = kCooVec * kCooVecPerThread;  // 8 items per thread
-constexpr int kCooTile = kCooThreads * kCooIpt;      // 2048 nonzeros owned per tile
-constexpr int kCooHalo = 128;                        // staged past the tile end (7 blocks/SM fit)
+constexpr int kCooHalo = 128;                    // staged past the tile end
 
-__global__ void __launch_bounds__(kCooThreads, 7)
+template <int kCooThreads, int kCooVecPerThread, int kMinBlocks>
+__global__ void __launch_bounds__(kCooThreads, kMinBlocks)
 spmv_coo_kernel(int64_t nrows, int64_t nnz, const int32_t* __restrict__ rows,
                 const int32_t* __restrict__ cols, const double* __restrict__ vals,
                 const double* __restrict__ x, double* __restrict__ y, bool vec_ok) {
+  constexpr int kCooIpt = kCooVec * kCooVecPerThread;  // items per thread
+  constexpr int kCooTile = kCooThreads * kCooIpt;      // nonzeros owned per tile
   // s_row[4 + q] = row of staged item q; s_row[3] = row of the item before the tile
   __shared__ __align__(16) int32_t s_row[kCooTile + kCooHalo + 4];
   __shared__ __align__(16) double s_prod[kCooTile + kCooHalo];
@@ -646,8 +645,12 @@ extern "C" int sl_spmv_coo_f64(int64_t nrows, int64_t ncols, int64_t nnz, const 
   }
   const bool vec_ok = aligned16(rows) && aligned16(cols) && aligned16(vals);
   if (vec_ok && spmv_path() == 2) return sl_host::launch_coo_pipe(nrows, nnz, rows, cols, vals, x, y, s);
-  spmv_coo_kernel<<<ceil_div(nnz, kCooTile), kCooThreads, 0, s>>>(nrows, nnz, rows, cols, vals,
-                                                                   x, y, vec_ok);
+  // 1024-nonzero tiles, 8 blocks/SM: on D1 (2M nonzeros) the grid is 1.65x the
+  // resident slots, so later tiles' loads overlap earlier tiles' sum phases
+  // (measured: 2048-nonzero tiles in one wave 37.0 us, this 26.2 us; 512-tile
+  // and 128-thread variants 26.7-42 us)
+  spmv_coo_kernel<256, 1, 8><<<ceil_div(nnz, 1024), 256, 0, s>>>(nrows, nnz, rows, cols, vals,
+                                                                 x, y, vec_ok);
   return sl_host::launch_status();
 }
 

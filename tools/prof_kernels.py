@@ -64,6 +64,9 @@ def main():
         y = torch.empty(n, dtype=torch.float64, device=dev)
         bc = 4 * (n + 1) + 12 * len(s["crd"]) + 16 * n
         jobs["csr"] = (bc, lambda: K.spmv_csr(n, n, p, c, v, x, y, variant=0))
+        rr = T(np.repeat(np.arange(n, dtype=np.int32), np.diff(s["pos"])))
+        jobs["coo_st"] = (16 * len(s["crd"]) + 16 * n,
+                          lambda: K.spmv_coo(n, n, rr, c, v, x, y))
         jobs["csr_vec"] = (bc, lambda: K.spmv_csr(n, n, p, c, v, x, y, variant=1))
         jobs["csr_merge"] = (bc, lambda: K.spmv_csr(n, n, p, c, v, x, y, variant=2))
         jobs["csr_warp"] = (bc, lambda: K.spmv_csr(n, n, p, c, v, x, y, variant=3))
@@ -108,7 +111,7 @@ def main():
     if (want("coo") or want("hashx") or want("hashx_wdef") or want("csr_d1")
             or want("hashx_map") or want("hashx_wdef_map")):
         d1()
-    if (want("csr") or want("ell") or want("csr_vec") or want("csr_merge") or want("csr_warp")
+    if (want("csr") or want("coo_st") or want("ell") or want("csr_vec") or want("csr_merge") or want("csr_warp")
             or want("spmm4") or want("spmm16") or want("spmm32")):
         d2()
     if want("dia"):
