@@ -372,16 +372,16 @@ SL_DEV void stage_products(const int32_t* __restrict__ crd, const double* __rest
   }
 }
 
-template <int kHashX>
+template <int kHashX, int kRows = kCsrRows>
 __global__ void __launch_bounds__(kCsrThreads, kHashX == 1 ? 4 : 8)
 spmv_csr_rowblock_kernel(int64_t nrows, const int32_t* __restrict__ pos,
                          const int32_t* __restrict__ crd, const double* __restrict__ vals,
                          XOperand<kHashX> xop, double* __restrict__ y) {
-  __shared__ int32_t s_pos[kCsrRows + 1];
+  __shared__ int32_t s_pos[kRows + 1];
   __shared__ __align__(16) double s_prod[kCsrChunk];
   const int tid = threadIdx.x;
-  const int64_t r0 = (int64_t)blockIdx.x * kCsrRows;
-  const int nr = (int)min64(kCsrRows, nrows - r0);
+  const int64_t r0 = (int64_t)blockIdx.x * kRows;
+  const int nr = (int)min64(kRows, nrows - r0);
   for (int t = tid; t <= nr; t += kCsrThreads) s_pos[t] = ldg(pos + r0 + t);
   __syncthreads();
   const int32_t eb = s_pos[0], ee = s_pos[nr];
@@ -661,13 +661,24 @@ extern "C" size_t sl_spmv_csr_workspace_bytes(int64_t nrows, int64_t nnz, int32_
 }
 
 template <int kHashX>
-static int launch_csr(int64_t nrows, const int32_t* pos, const int32_t* crd, const double* vals,
-                      XOperand<kHashX> xop, double* y, int32_t variant, void* ws,
-                      size_t ws_bytes, cudaStream_t s) {
+static int launch_csr(int64_t nrows, int64_t nnz, const int32_t* pos, const int32_t* crd,
+                      const double* vals, XOperand<kHashX> xop, double* y, int32_t variant,
+                      void* ws, size_t ws_bytes, cudaStream_t s) {
   if (variant == 0 && !kHashX && aligned16(crd) && aligned16(vals) && spmv_path() == 2) {
     const double* xd = reinterpret_cast<const XOperand<0>&>(xop).x;
     return sl_host::launch_csr_pipe(nrows, pos, crd, vals, xd, y, s);
   } else if (variant == 0) {
+    // short rows (<= 16 per row on average): 192-row blocks, about one chunk
+    // each and more blocks than resident slots, so blocks' load and sum phases
+    // interleave (D1 22.8 -> 21.2 us, hashed x 40.7 -> 32.8 us); long rows
+    // (the 27-point stencil) keep 256-row blocks (29.0 vs 35.2 us)
+    // (nnz < 0: not known to the entry point — the located-x paths, whose
+    // per-nonzero locate latency also favours more, smaller blocks)
+    if (nnz <= 16 * nrows) {
+      spmv_csr_rowblock_kernel<kHashX, 192><<<ceil_div(nrows, 192), kCsrThreads, 0, s>>>(
+          nrows, pos, crd, vals, xop, y);
+      return sl_host::launch_status();
+    }
     spmv_csr_rowblock_kernel<kHashX><<<ceil_div(nrows, kCsrRows), kCsrThreads, 0, s>>>(
         nrows, pos, crd, vals, xop, y);
   } else if (variant == 3 && !kHashX) {
@@ -706,7 +717,7 @@ extern "C" int sl_spmv_csr_f64(int64_t nrows, int64_t ncols, int64_t nnz, const 
                                                                    part, y);
     return sl_host::launch_status();
   }
-  return launch_csr<0>(nrows, pos, crd, vals, xop, y, variant, ws, ws_bytes, s);
+  return launch_csr<0>(nrows, nnz, pos, crd, vals, xop, y, variant, ws, ws_bytes, s);
 }
 
 extern "C" int sl_spmv_csr_hashx_f64(int64_t nrows, const int32_t* pos, const int32_t* crd,
@@ -717,7 +728,7 @@ extern "C" int sl_spmv_csr_hashx_f64(int64_t nrows, const int32_t* pos, const in
   if (nrows == 0) return SL_OK;
   if (!pos || !y || !x_crd || !x_vals) return SL_ERR_INVALID;
   XOperand<1> xop{HashedLevel{x_crd, w}, x_vals};
-  return launch_csr<1>(nrows, pos, crd, vals, xop, y, 0, nullptr, 0, as_stream(stream));
+  return launch_csr<1>(nrows, -1, pos, crd, vals, xop, y, 0, nullptr, 0, as_stream(stream));
 }
 
 extern "C" size_t sl_spmv_csr_hashx_map_workspace_bytes(int64_t n, int64_t w) {
@@ -735,7 +746,7 @@ extern "C" int sl_spmv_csr_hashx_map_f64(int64_t nrows, int64_t n, const int32_t
   const int st = sl_hashed_slot_map(n, w, x_crd, ws, ws_bytes, stream);
   if (st != SL_OK) return st;
   XOperand<2> xop{HashedLevel{x_crd, w}, x_vals, static_cast<const unsigned long long*>(ws), n};
-  return launch_csr<2>(nrows, pos, crd, vals, xop, y, 0, nullptr, 0, as_stream(stream));
+  return launch_csr<2>(nrows, -1, pos, crd, vals, xop, y, 0, nullptr, 0, as_stream(stream));
 }
 
 __global__ void spx_map_kernel(int64_t n, int64_t xnnz, const int32_t* __restrict__ xcrd,
@@ -772,7 +783,7 @@ extern "C" int sl_spmv_csr_spx_f64(int64_t nrows, int64_t n, const int32_t* pos,
   if (xnnz > 0)
     spx_scatter_kernel<<<min(ceil_div(xnnz, 256), 8 * sms), 256, 0, s>>>(n, xnnz, x_crd, map);
   XOperand<3> xop{map, x_vals, n};
-  return launch_csr<3>(nrows, pos, crd, vals, xop, y, 0, nullptr, 0, s);
+  return launch_csr<3>(nrows, -1, pos, crd, vals, xop, y, 0, nullptr, 0, s);
 }
 
 extern "C" int sl_spmv_ell_f64(int64_t nrows, int64_t ncols, int32_t nslots, const int32_t* crd,
