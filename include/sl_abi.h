@@ -208,8 +208,9 @@ int sl_spmv_csr_hashx_f64(int64_t nrows, const int32_t* pos, const int32_t* crd,
  * results as sl_spmv_csr_hashx_f64, one locate per coordinate instead of per
  * nonzero.  ws: sl_spmv_csr_hashx_map_workspace_bytes(n, w). */
 size_t sl_spmv_csr_hashx_map_workspace_bytes(int64_t n, int64_t w);
-int sl_spmv_csr_hashx_map_f64(int64_t nrows, int64_t n, const int32_t* pos, const int32_t* crd,
-                              const double* vals, int64_t w, const int32_t* x_crd,
+int sl_spmv_csr_hashx_map_f64(int64_t nrows, int64_t n, int64_t nnz, const int32_t* pos,
+                              const int32_t* crd, const double* vals, int64_t w,
+                              const int32_t* x_crd,
                               const double* x_vals, double* y, void* ws, size_t ws_bytes,
                               void* stream);
 
@@ -219,8 +220,8 @@ int sl_spmv_csr_hashx_map_f64(int64_t nrows, int64_t n, const int32_t* pos, cons
  * Replaces that merge with an index map (coordinate -> position in x) built
  * in ws, then the CSR row-block kernel.  ws: sl_spmv_csr_spx_workspace_bytes(n). */
 size_t sl_spmv_csr_spx_workspace_bytes(int64_t n);
-int sl_spmv_csr_spx_f64(int64_t nrows, int64_t n, const int32_t* pos, const int32_t* crd,
-                        const double* vals, int64_t x_nnz, const int32_t* x_crd,
+int sl_spmv_csr_spx_f64(int64_t nrows, int64_t n, int64_t nnz, const int32_t* pos,
+                        const int32_t* crd, const double* vals, int64_t x_nnz, const int32_t* x_crd,
                         const double* x_vals, double* y, void* ws, size_t ws_bytes,
                         void* stream);
 

@@ -84,10 +84,11 @@ SIGNATURES = {
     "sl_hashed_slot_map_workspace_bytes": ([_i64, _i64], _sz),
     "sl_hashed_slot_map": ([_i64, _i64, _p, _p, _sz, _p], ctypes.c_int),
     "sl_spmv_csr_hashx_map_workspace_bytes": ([_i64, _i64], _sz),
-    "sl_spmv_csr_hashx_map_f64": ([_i64, _i64, _p, _p, _p, _i64, _p, _p, _p, _p, _sz, _p],
+    "sl_spmv_csr_hashx_map_f64": ([_i64, _i64, _i64, _p, _p, _p, _i64, _p, _p, _p, _p, _sz, _p],
                                   ctypes.c_int),
     "sl_spmv_csr_spx_workspace_bytes": ([_i64], _sz),
-    "sl_spmv_csr_spx_f64": ([_i64, _i64, _p, _p, _p, _i64, _p, _p, _p, _p, _sz, _p], ctypes.c_int),
+    "sl_spmv_csr_spx_f64": ([_i64, _i64, _i64, _p, _p, _p, _i64, _p, _p, _p, _p, _sz, _p],
+                            ctypes.c_int),
     "sl_spmm_csr_f64": ([_i64, _i64, _i64, _p, _p, _p, _p, _p, _p], ctypes.c_int),
     "sl_csf_fiber_scatter_f64": ([_i64, _i64, _i64, _i64, _i64, _p, _p, _p, _p, _p, _p],
                                  ctypes.c_int),

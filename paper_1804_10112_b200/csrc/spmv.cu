@@ -740,8 +740,9 @@ extern "C" size_t sl_spmv_csr_hashx_map_workspace_bytes(int64_t n, int64_t w) {
   return sl_hashed_slot_map_workspace_bytes(n, w);
 }
 
-extern "C" int sl_spmv_csr_hashx_map_f64(int64_t nrows, int64_t n, const int32_t* pos,
-                                         const int32_t* crd, const double* vals, int64_t w,
+extern "C" int sl_spmv_csr_hashx_map_f64(int64_t nrows, int64_t n, int64_t nnz,
+                                         const int32_t* pos, const int32_t* crd,
+                                         const double* vals, int64_t w,
                                          const int32_t* x_crd, const double* x_vals, double* y,
                                          void* ws, size_t ws_bytes, void* stream) {
   if (nrows < 0 || n < 0 || w <= 0) return SL_ERR_INVALID;
@@ -751,7 +752,7 @@ extern "C" int sl_spmv_csr_hashx_map_f64(int64_t nrows, int64_t n, const int32_t
   const int st = sl_hashed_slot_map(n, w, x_crd, ws, ws_bytes, stream);
   if (st != SL_OK) return st;
   XOperand<2> xop{HashedLevel{x_crd, w}, x_vals, static_cast<const unsigned long long*>(ws), n};
-  return launch_csr<2>(nrows, -1, pos, crd, vals, xop, y, 0, nullptr, 0, as_stream(stream));
+  return launch_csr<2>(nrows, nnz, pos, crd, vals, xop, y, 0, nullptr, 0, as_stream(stream));
 }
 
 __global__ void spx_map_kernel(int64_t n, int64_t xnnz, const int32_t* __restrict__ xcrd,
@@ -772,7 +773,7 @@ __global__ void spx_scatter_kernel(int64_t n, int64_t xnnz, const int32_t* __res
 
 extern "C" size_t sl_spmv_csr_spx_workspace_bytes(int64_t n) { return (size_t)n * 4 + 256; }
 
-extern "C" int sl_spmv_csr_spx_f64(int64_t nrows, int64_t n, const int32_t* pos,
+extern "C" int sl_spmv_csr_spx_f64(int64_t nrows, int64_t n, int64_t nnz, const int32_t* pos,
                                    const int32_t* crd, const double* vals, int64_t xnnz,
                                    const int32_t* x_crd, const double* x_vals, double* y,
                                    void* ws, size_t ws_bytes, void* stream) {
@@ -788,7 +789,7 @@ extern "C" int sl_spmv_csr_spx_f64(int64_t nrows, int64_t n, const int32_t* pos,
   if (xnnz > 0)
     spx_scatter_kernel<<<min(ceil_div(xnnz, 256), 8 * sms), 256, 0, s>>>(n, xnnz, x_crd, map);
   XOperand<3> xop{map, x_vals, n};
-  return launch_csr<3>(nrows, -1, pos, crd, vals, xop, y, 0, nullptr, 0, s);
+  return launch_csr<3>(nrows, nnz, pos, crd, vals, xop, y, 0, nullptr, 0, s);
 }
 
 extern "C" int sl_spmv_ell_f64(int64_t nrows, int64_t ncols, int32_t nslots, const int32_t* crd,

@@ -113,7 +113,8 @@ def spmv_csr_hashx(nrows, pos, crd, vals, w, x_crd, x_vals, y=None, n=None, ws=N
     need = L().sl_spmv_csr_hashx_map_workspace_bytes(n, w)
     if ws is None or ws.numel() < need:
         ws = _ws(need, vals)
-    _lib.check(L().sl_spmv_csr_hashx_map_f64(nrows, n, P(pos), P(crd), P(vals), w, P(x_crd),
+    _lib.check(L().sl_spmv_csr_hashx_map_f64(nrows, n, crd.numel(), P(pos), P(crd), P(vals), w,
+                                             P(x_crd),
                                              P(x_vals), P(y), P(ws), ws.numel(), S()),
                "spmv_csr_hashx_map")
     return y
@@ -127,7 +128,8 @@ def spmv_csr_spx(nrows, n, pos, crd, vals, x_crd, x_vals, y=None, ws=None):
     need = L().sl_spmv_csr_spx_workspace_bytes(n)
     if ws is None or ws.numel() < need:
         ws = _ws(need, vals)
-    _lib.check(L().sl_spmv_csr_spx_f64(nrows, n, P(pos), P(crd), P(vals), x_crd.numel(), P(x_crd),
+    _lib.check(L().sl_spmv_csr_spx_f64(nrows, n, crd.numel(), P(pos), P(crd), P(vals),
+                                       x_crd.numel(), P(x_crd),
                                        P(x_vals), P(y), P(ws), ws.numel(), S()), "spmv_csr_spx")
     return y
 

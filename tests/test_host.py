@@ -50,16 +50,16 @@ def test_library_host_only_calls():
     # widened entry points validate before launching too (1 = invalid, 7 = range, 8 = workspace)
     assert lib.sl_spmm_csr_f64(1, 1, -1, None, None, None, None, None, None) == 1
     assert lib.sl_spmm_csr_f64(2**40, 1, 4, None, None, None, None, None, None) == 7
-    assert lib.sl_spmv_csr_spx_f64(1, 2**40, None, None, None, 0, None, None, None, None, 0,
+    assert lib.sl_spmv_csr_spx_f64(1, 2**40, 0, None, None, None, 0, None, None, None, None, 0,
                                    None) == 7
-    assert lib.sl_spmv_csr_spx_f64(1, 10, ctypes.c_void_p(8), None, None, 0, None, None,
+    assert lib.sl_spmv_csr_spx_f64(1, 10, 0, ctypes.c_void_p(8), None, None, 0, None, None,
                                    ctypes.c_void_p(8), None, 0, None) == 8
     assert lib.sl_inner_coo3_f64(1, 1, 1, -1, None, None, None, None, 0, None, None, None, None,
                                  None, None, 0, None) == 1
     assert lib.sl_convert_coo_to_csr(1, 2**40, None, None, None) == 7
     assert lib.sl_hashed_slot_map(10, 0, None, None, 0, None) == 1
-    assert lib.sl_spmv_csr_hashx_map_f64(1, 10, None, None, None, 0, None, None, None, None, 0,
-                                         None) == 1
+    assert lib.sl_spmv_csr_hashx_map_f64(1, 10, 0, None, None, None, 0, None, None, None, None,
+                                         0, None) == 1
     assert lib.sl_csf_fiber_scatter_f64(-1, 1, 1, 0, 0, None, None, None, None, None, None) == 1
     assert lib.sl_add_csr_f64(-1, None, None, None, 0, None, None, None, None, None, None, None,
                               None, 0, None) == 1
