@@ -111,6 +111,47 @@ def gather_row_blocks(y_local, bounds: Sequence[int], group=None):
     return torch.cat([parts[p][:sizes[p]] for p in range(world)])
 
 
+def shard_add(a_pos, a_crd, a_vals, b_rows, b_cols, b_vals, r0, r1):
+    """Row block [r0, r1) of C = A + B's operands (A CSR, B row-sorted COO):
+    each rank computes its block of C with no exchange."""
+    a = shard_csr(a_pos, a_crd, a_vals, r0, r1)
+    b = shard_coo(b_rows, b_cols, b_vals, r0, r1)
+    return a, b
+
+
+def concat_csr_blocks(pos_local, crd_local, vals_local, group=None):
+    """Assemble the global CSR of row-blocked results on every rank: an
+    all-gather of the per-rank nnz totals gives each block's offset (the
+    exclusive scan SURVEY.md §8(e) names), then the blocks' arrays are
+    all-gathered (padded to the largest block)."""
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    dev = crd_local.device
+    nnz = torch.tensor([crd_local.numel(), pos_local.numel() - 1], dtype=torch.int64, device=dev)
+    sizes = [torch.empty_like(nnz) for _ in range(world)]
+    dist.all_gather(sizes, nnz, group=group)
+    nnzs = [int(t[0]) for t in sizes]
+    rows = [int(t[1]) for t in sizes]
+    offs = np.concatenate([[0], np.cumsum(nnzs)])
+
+    def gather_padded(t, counts):
+        m = max(max(counts), 1)
+        pad = torch.zeros(m, dtype=t.dtype, device=dev)
+        pad[:t.numel()] = t
+        parts = [torch.empty_like(pad) for _ in range(world)]
+        dist.all_gather(parts, pad, group=group)
+        return [parts[p][:counts[p]] for p in range(world)]
+
+    crd = torch.cat(gather_padded(crd_local, nnzs))
+    vals = torch.cat(gather_padded(vals_local, nnzs))
+    pos_parts = gather_padded(pos_local[1:].to(torch.int64), rows)
+    pos = torch.cat([torch.zeros(1, dtype=torch.int64, device=dev)] +
+                    [pos_parts[p] + int(offs[p]) for p in range(world)])
+    return pos.to(torch.int32), crd, vals
+
+
 def replicate(t, src: int = 0, group=None):
     """Broadcast x (or a factor matrix) from `src` to every rank."""
     import torch.distributed as dist

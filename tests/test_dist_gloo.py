@@ -53,11 +53,21 @@ def _worker(rank, world, port, out_dir):
         ii, jj, kk, vv = D.shard_coo3(m["i"], m["j"], m["k"], m["vals"], s0, s1)
         A_loc = oracle.mttkrp_coo3(s1 - s0, ii, jj, kk, vv, m["B"], m["C"], threads=1)
         A = D.gather_row_blocks(torch.as_tensor(A_loc.reshape(-1)), [b * m["R"] for b in sb])
+        # A + B (CSR + COO -> CSR): row blocks, nnz totals all-gathered for the offsets
+        ab = wl.add_ab(n=4000, nnz_a=16000, nnz_b=16000, seed=8)
+        ab_bounds = D.balanced_row_blocks(ab["a_pos"], world)
+        q0, q1 = int(ab_bounds[rank]), int(ab_bounds[rank + 1])
+        (ap, ac, av), (br, bc, bv) = D.shard_add(ab["a_pos"], ab["a_crd"], ab["a_vals"],
+                                                 ab["b_rows"], ab["b_cols"], ab["b_vals"], q0, q1)
+        cp, cc, cv = oracle.add_csr(q1 - q0, ap, ac, av, bc, bv, b_rows=br)
+        gp, gc, gv = D.concat_csr_blocks(torch.as_tensor(cp), torch.as_tensor(cc),
+                                         torch.as_tensor(cv))
         t_max = D.max_over_ranks(float(rank + 1))
         t_sum = D.sum_over_ranks(float(rank + 1))
         if rank == 0:
             np.savez(out_dir / "dist.npz", y=y.numpy(), A=A.numpy(), bounds=bounds, sb=sb,
-                     t_max=t_max, t_sum=t_sum)
+                     t_max=t_max, t_sum=t_sum, c_pos=gp.numpy(), c_crd=gc.numpy(),
+                     c_vals=gv.numpy())
     finally:
         dist.destroy_process_group()
 
@@ -76,6 +86,11 @@ def test_two_rank_gloo_spmv_and_mttkrp(tmp_path, orc):
     b = r["bounds"]
     assert b[0] == 0 and b[-1] == 3000 and (np.diff(b) > 0).all()
     assert float(r["t_max"]) == 2.0 and float(r["t_sum"]) == 3.0
+    ab = wl.add_ab(n=4000, nnz_a=16000, nnz_b=16000, seed=8)
+    rp, rc, rv = orc.add_csr(4000, ab["a_pos"], ab["a_crd"], ab["a_vals"], ab["b_cols"],
+                             ab["b_vals"], b_rows=ab["b_rows"])
+    assert np.array_equal(r["c_pos"], rp) and np.array_equal(r["c_crd"], rc)
+    assert np.array_equal(r["c_vals"].view(np.int64), rv.view(np.int64))
 
 
 @pytest.mark.parametrize("parts", [1, 2, 3, 8])
