@@ -153,13 +153,18 @@ int sl_spmv_coo_f64(int64_t nrows, int64_t ncols, int64_t nnz,
 
 /* CSR (formats.py:126-127). Replaces run_node(i) -> run_node(j) with
  * locate of x (engine.py:591-634).
- * variant 0 = row-block (rows tiled; nonzeros of the tile staged through
- *             shared memory in coalesced chunks; thread per row sums in order);
+ * variant 0 = automatic: row-stage (variant 4) when rows average >= 16
+ *             nonzeros and crd/vals are 16-byte aligned, else row-block (5);
  * variant 1 = vector-per-row (a warp per row; lanes load the row's nonzeros
  *             coalesced, lane 0 sums them in order from registers via shuffles);
  * variant 2 = merge-path (nnz+rows balanced tiles; row-owner sums in order);
  * variant 3 = warp row-block (each warp owns 32 rows, warp-private staging);
- * All variants are bit-identical.  ws may be NULL for variants 0 and 1. */
+ * variant 4 = row-stage (the block's crd/vals bulk-copied (TMA) to shared
+ *             memory; thread per row walks its row in order; crd and vals
+ *             must be 16-byte aligned, else SL_ERR_INVALID);
+ * variant 5 = row-block (rows tiled; nonzeros of the tile staged through
+ *             shared memory in coalesced chunks; thread per row sums in order);
+ * All variants are bit-identical.  ws may be NULL for every variant but 2. */
 size_t sl_spmv_csr_workspace_bytes(int64_t nrows, int64_t nnz, int32_t variant);
 int sl_spmv_csr_f64(int64_t nrows, int64_t ncols, int64_t nnz, const int32_t* pos,
                     const int32_t* crd, const double* vals,

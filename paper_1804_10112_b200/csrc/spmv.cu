@@ -399,6 +399,113 @@ spmv_csr_rowblock_kernel(int64_t nrows, const int32_t* __restrict__ pos,
   if (mine) y[r0 + tid] = acc;
 }
 
+// K2f: CSR row-stage.  The block's whole nonzero range (up to kCap elements
+// per round) is bulk-copied (TMA, cp.async.bulk: no LSU wavefronts, no
+// registers) into shared memory; then the thread of row r walks its own row
+// in storage order like the ELL kernel walks its slots: batches of kBatch
+// crd reads from smem (stride = row length: odd strides are conflict-free),
+// kBatch x gathers in flight (consecutive rows' u-th columns are adjacent for
+// banded matrices, so these coalesce), then the ordered add chain.  Products
+// never round-trip through smem.  Many small blocks per SM, several waves:
+// while some blocks walk their rows, others' copies are in flight.
+//
+// Measured on the 64^3 27-point stencil (tools/ab_csr.py, L2 cold and clean,
+// DESIGN.md §3): K2a 28.6 us -> 32-row blocks at 20/SM 23.8 us (64-row
+// blocks at 10/SM 24.5, 128-row at 5/SM 24.7, batch 14/27 no better).  Also
+// measured and dropped: K2a with a 2-4 stage cp.async (LDGSTS) ring of
+// chunks (29-41 us: the in-place products and read-back cost more L1
+// wavefronts than the latency they hide), and a persistent warp-specialised
+// version of this kernel (one CTA/SM, producer warp + 2-8 consumer groups
+// with double-buffered stages: 26.7-37.6 us; too few row-walking threads per
+// SM).  On short, irregular rows (D1, Poisson(10)) the row walk diverges
+// (warps run the longest row) and K2a stays faster (20.5 vs 29 us), so the
+// automatic choice takes K2f only for rows averaging >= 16 nonzeros.
+
+constexpr int kCsrStageRows = 32;
+constexpr int kCsrStageCap = 896;     // 28 per row: the 27-point stencil's rows fit in one round
+constexpr int kCsrStageBatch = 9;
+constexpr int kCsrStageBlocks = 20;   // 20 x 11.3 KB of shared memory per SM
+
+template <int kRows, int kCap>
+struct CsrStageSmem {
+  uint64_t bar;
+  int32_t pos[kRows + 1];
+  __align__(16) int32_t crd[kCap];
+  __align__(16) double val[kCap];
+};
+
+template <int kRows, int kCap, int kBatch, int kMinBlocks>
+__global__ void __launch_bounds__(kRows, kMinBlocks)
+spmv_csr_stage_kernel(int64_t nrows, const int32_t* __restrict__ pos,
+                      const int32_t* __restrict__ crd, const double* __restrict__ vals,
+                      const double* __restrict__ x, double* __restrict__ y) {
+  static_assert(kCap % 4 == 0, "granule-aligned capacity");
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  auto& sm = *reinterpret_cast<CsrStageSmem<kRows, kCap>*>(smem_raw);
+  const int tid = threadIdx.x;
+  const int64_t r0 = (int64_t)blockIdx.x * kRows;
+  const int nr = (int)min64(kRows, nrows - r0);
+  if (tid == 0) {
+    mbar_init(&sm.bar, 1);
+    fence_mbar_init();
+  }
+  for (int t = tid; t <= nr; t += kRows) sm.pos[t] = ldg(pos + r0 + t);
+  __syncthreads();
+  const int32_t eb = sm.pos[0], ee = sm.pos[nr];
+  const int32_t a0 = eb & ~3;
+  const int nch = ee > eb ? (ee - a0 + kCap - 1) / kCap : 0;
+  const bool mine = tid < nr;
+  const int32_t rb = mine ? sm.pos[tid] : 0, re = mine ? sm.pos[tid + 1] : 0;
+  double acc = 0.0;
+  for (int k = 0; k < nch; ++k) {
+    const int32_t c0 = a0 + k * kCap;
+    const int32_t c1 = min(c0 + kCap, ee);
+    if (tid == 0) {
+      const uint32_t bc = (uint32_t)(((c1 - c0 + 3) & ~3) * 4);
+      const uint32_t bv = (uint32_t)(((c1 - c0 + 1) & ~1) * 8);
+      mbar_arrive_expect_tx(&sm.bar, bc + bv);
+      bulk_g2s(sm.crd, crd + c0, bc, &sm.bar);
+      bulk_g2s(sm.val, vals + c0, bv, &sm.bar);
+    }
+    mbar_wait(&sm.bar, k & 1);
+    const int lo = max(rb, c0) - c0, hi = min(re, c1) - c0;
+    for (int u = lo; u < hi; u += kBatch) {
+      const int n = min(kBatch, hi - u);
+      int32_t c[kBatch];
+      double xv[kBatch], v[kBatch];
+#pragma unroll
+      for (int b = 0; b < kBatch; ++b) c[b] = b < n ? sm.crd[u + b] : 0;
+#pragma unroll
+      for (int b = 0; b < kBatch; ++b) xv[b] = b < n ? ldg(x + c[b]) : 0.0;
+#pragma unroll
+      for (int b = 0; b < kBatch; ++b) v[b] = b < n ? sm.val[u + b] : 0.0;
+#pragma unroll
+      for (int b = 0; b < kBatch; ++b)
+        if (b < n) acc = dadd(acc, dmul(v[b], xv[b]));
+    }
+    if (k + 1 < nch) {
+      __syncthreads();            // every row done with this round's stage
+      if (tid == 0) fence_proxy_async_smem();
+    }
+  }
+  if (mine) y[r0 + tid] = acc;
+}
+
+template <int kRows, int kCap, int kBatch, int kMinBlocks>
+static void launch_csr_stage(int64_t nrows, const int32_t* pos, const int32_t* crd,
+                             const double* vals, const double* x, double* y, cudaStream_t s) {
+  constexpr size_t smem = sizeof(CsrStageSmem<kRows, kCap>);
+  auto kern = spmv_csr_stage_kernel<kRows, kCap, kBatch, kMinBlocks>;
+  static unsigned long long attr_set = 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (smem > 48 * 1024 && !(__atomic_load_n(&attr_set, __ATOMIC_ACQUIRE) >> (dev & 63) & 1ull)) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    __atomic_fetch_or(&attr_set, 1ull << (dev & 63), __ATOMIC_ACQ_REL);
+  }
+  kern<<<(int)((nrows + kRows - 1) / kRows), kRows, smem, s>>>(nrows, pos, crd, vals, x, y);
+}
+
 // K2d: CSR warp row-block.  Each warp owns 32 consecutive rows; their
 // nonzeros (contiguous) are staged in warp-private shared memory in rounds of
 // 256 products (8 coalesced loads per lane), and lane r adds the round's
@@ -516,6 +623,10 @@ spmv_csr_merge_kernel(int64_t nrows, const int32_t* __restrict__ pos,
   // rows [rb, re) end inside this tile; their nonzeros span [pos[rb], pos[re]).
   if (rb >= re) return;
   const int64_t eb = ldg(pos + rb), ee = ldg(pos + re);
+  if (eb == ee) {   // every row owned by this tile is empty: no chunk writes them
+    for (int64_t r = rb + tid; r < re; r += kMpThreads) y[r] = 0.0;
+    return;
+  }
   for (int64_t cs = eb; cs < ee; cs += kMpItems) {
     const int n_in = (int)min64(kMpItems, ee - cs);
     stage_products<kMpThreads, kMpItems / kMpThreads>(crd, vals, cs, n_in, xop, s_prod);
@@ -672,13 +783,20 @@ static int launch_csr(int64_t nrows, int64_t nnz, const int32_t* pos, const int3
   if (variant == 0 && !kHashX && aligned16(crd) && aligned16(vals) && spmv_path() == 2) {
     const double* xd = reinterpret_cast<const XOperand<0>&>(xop).x;
     return sl_host::launch_csr_pipe(nrows, pos, crd, vals, xd, y, s);
-  } else if (variant == 0) {
-    // short rows (<= 16 per row on average): 192-row blocks, about one chunk
+  } else if (variant == 0 || variant == 5) {
+    // variant 0 (automatic): rows averaging >= 16 nonzeros take the row-stage
+    // kernel K2f, the rest the row-block kernel K2a (variant 5 forces K2a).
+    // K2a: short rows (<= 16 per row on average): 192-row blocks, about one chunk
     // each and more blocks than resident slots, so blocks' load and sum phases
     // interleave (D1 22.8 -> 21.2 us, hashed x 40.7 -> 32.8 us); long rows
     // (the 27-point stencil) keep 256-row blocks (29.0 vs 35.2 us)
     // (nnz < 0: not known to the entry point — the located-x paths, whose
     // per-nonzero locate latency also favours more, smaller blocks)
+    if (variant == 0 && !kHashX && nnz >= 16 * nrows && aligned16(crd) && aligned16(vals)) {
+      launch_csr_stage<kCsrStageRows, kCsrStageCap, kCsrStageBatch, kCsrStageBlocks>(
+          nrows, pos, crd, vals, reinterpret_cast<const XOperand<0>&>(xop).x, y, s);
+      return sl_host::launch_status();
+    }
     if (nnz <= 16 * nrows) {
       spmv_csr_rowblock_kernel<kHashX, 192><<<ceil_div(nrows, 192), kCsrThreads, 0, s>>>(
           nrows, pos, crd, vals, xop, y);
@@ -686,6 +804,10 @@ static int launch_csr(int64_t nrows, int64_t nnz, const int32_t* pos, const int3
     }
     spmv_csr_rowblock_kernel<kHashX><<<ceil_div(nrows, kCsrRows), kCsrThreads, 0, s>>>(
         nrows, pos, crd, vals, xop, y);
+  } else if (variant == 4 && !kHashX) {
+    if (!aligned16(crd) || !aligned16(vals)) return SL_ERR_INVALID;
+    launch_csr_stage<kCsrStageRows, kCsrStageCap, kCsrStageBatch, kCsrStageBlocks>(
+        nrows, pos, crd, vals, reinterpret_cast<const XOperand<0>&>(xop).x, y, s);
   } else if (variant == 3 && !kHashX) {
     const double* xd = reinterpret_cast<const XOperand<0>&>(xop).x;
     spmv_csr_warp_kernel<<<ceil_div(nrows, 256), 256, 0, s>>>(nrows, pos, crd, vals, xd, y);

@@ -43,7 +43,7 @@ def test_spmv_goldens_all_formats(golden):
                            cuda(c["coo_cols"], np.int32), cuda(c["coo_vals"], np.float64), x)
             assert np.array_equal(bits(y), bits(c["coo_y"])), name
         if "csr_y" in c:
-            for variant in (0, 1, 2, 3):
+            for variant in (0, 1, 2, 3, 4, 5):
                 y = K.spmv_csr(nrows, ncols, cuda(c["csr_pos"], np.int32),
                                cuda(c["csr_crd"], np.int32), cuda(c["csr_vals"], np.float64), x,
                                variant=variant)
@@ -85,7 +85,7 @@ def test_spmv_coo_csr_vs_oracle(orc, n, nnz, lam, seed):
     y = K.spmv_coo(n, d["ncols"], cuda(d["rows"]), cuda(d["cols"]), cuda(d["vals"]), x)
     assert np.array_equal(bits(y), bits(ref))
     pos = wl.coo_to_csr_pos(d["rows"], n)
-    for variant in (0, 1, 2, 3):
+    for variant in (0, 1, 2, 3, 4, 5):
         y = K.spmv_csr(n, d["ncols"], cuda(pos), cuda(d["cols"]), cuda(d["vals"]), x,
                        variant=variant)
         assert np.array_equal(bits(y), bits(ref)), variant
@@ -106,6 +106,27 @@ def test_spmv_coo_long_rows_cross_tiles(orc):
     ref, _ = orc.spmv_coo(8, rows, cols, vals, x)
     y = K.spmv_coo(8, 20000, cuda(rows), cuda(cols), cuda(vals), cuda(x))
     assert np.array_equal(bits(y), bits(ref))
+    # the same rows through every CSR variant (row-stage: blocks far beyond
+    # one staging round, rows cut by rounds)
+    pos = wl.coo_to_csr_pos(rows, 8)
+    for variant in (0, 1, 2, 3, 4, 5):
+        y = K.spmv_csr(8, 20000, cuda(pos), cuda(cols), cuda(vals), cuda(x), variant=variant)
+        assert np.array_equal(bits(y), bits(ref)), variant
+
+
+def test_spmv_csr_misaligned_operands(orc):
+    # crd/vals views starting one element in: the automatic choice falls back
+    # to the row-block kernel; the row-stage kernel refuses (it bulk-copies
+    # 16-byte granules)
+    s = wl.stencil27(g=16)
+    ref, _ = orc.spmv_csr(s["nrows"], s["pos"], s["crd"], s["vals"], s["x"])
+    c = cuda(np.concatenate([[0], s["crd"]]).astype(np.int32))[1:]
+    v = cuda(np.concatenate([[0.0], s["vals"]]))[1:]
+    x = cuda(s["x"])
+    y = K.spmv_csr(s["nrows"], s["ncols"], cuda(s["pos"]), c, v, x, variant=0)
+    assert np.array_equal(bits(y), bits(ref))
+    with pytest.raises(Exception):
+        K.spmv_csr(s["nrows"], s["ncols"], cuda(s["pos"]), c, v, x, variant=4)
 
 
 def test_spmv_empty_matrix():
@@ -113,9 +134,11 @@ def test_spmv_empty_matrix():
     y = K.spmv_coo(9, 5, cuda(np.zeros(0, np.int32)), cuda(np.zeros(0, np.int32)),
                    cuda(np.zeros(0)), x)
     assert np.array_equal(bits(y), bits(np.zeros(9)))
-    y = K.spmv_csr(9, 5, cuda(np.zeros(10, np.int32)), cuda(np.zeros(0, np.int32)),
-                   cuda(np.zeros(0)), x, variant=2)
-    assert np.array_equal(bits(y), bits(np.zeros(9)))
+    for variant in (0, 1, 2, 3, 4, 5):     # y pre-filled with NaN: every row must be written
+        y = cuda(np.full(9, np.nan))
+        K.spmv_csr(9, 5, cuda(np.zeros(10, np.int32)), cuda(np.zeros(0, np.int32)),
+                   cuda(np.zeros(0)), x, y=y, variant=variant)
+        assert np.array_equal(bits(y), bits(np.zeros(9))), variant
 
 
 def test_spmv_dia_vs_oracle_odd_shapes(orc):
@@ -140,7 +163,7 @@ def test_full_size_spmv_bit_exact(orc):
     s = wl.stencil27()
     ref, _ = orc.spmv_csr(s["nrows"], s["pos"], s["crd"], s["vals"], s["x"])
     x = cuda(s["x"])
-    for variant in (0, 1, 2, 3):
+    for variant in (0, 1, 2, 3, 4, 5):
         y = K.spmv_csr(s["nrows"], s["ncols"], cuda(s["pos"]), cuda(s["crd"]), cuda(s["vals"]),
                        x, variant=variant)
         assert np.array_equal(bits(y), bits(ref)), variant
