@@ -56,12 +56,25 @@ coo_rowptr_kernel(int64_t nrows, int64_t nnz, const int32_t* __restrict__ rows,
   // positions past the end read as row nrows, so element nnz closes the
   // trailing rows (rowptr[nrows] = nnz) and later ones write nothing
   int32_t prev = e0 == 0 ? -1 : ldg(rows + e0 - 1);
+  // a row change almost always advances by one row: one predicated store per
+  // element; the gap loop (empty rows) runs out of line.  (A per-change
+  // counted loop cost ~42 instructions per element: ncu, 6.7M warp
+  // instructions for D4's 5M coordinates.)
+  unsigned gaps = 0;
 #pragma unroll
   for (int t = 0; t < kRowptrIpt; ++t) {
     const int32_t cur = r[t];
-    if (cur != prev) {
-      for (int32_t q = prev + 1; q <= cur; ++q) rowptr[q] = (int32_t)(e0 + t);
-      prev = cur;
+    const int32_t pv = t == 0 ? prev : r[t - 1];
+    if (cur != pv) rowptr[cur] = (int32_t)(e0 + t);
+    gaps |= (cur - pv > 1 ? 1u : 0u) << t;
+  }
+  if (gaps) {
+#pragma unroll
+    for (int t = 0; t < kRowptrIpt; ++t) {
+      if (gaps >> t & 1u) {
+        const int32_t lo = t == 0 ? prev : r[t - 1];
+        for (int32_t q = lo + 1; q < r[t]; ++q) rowptr[q] = (int32_t)(e0 + t);
+      }
     }
   }
 }
@@ -113,50 +126,75 @@ SL_DEV int merge_row(int32_t alo, int32_t ahi, int32_t blo, int32_t bhi, const A
   return n;
 }
 
-// The same merge over the tile's shared-memory stage, written for SIMT: both
-// operands' next values are read unconditionally (indices stay inside the
-// stage) and selected, so the loop body has no divergent branch except the
-// rare duplicate-B group.  ac/av/bc/bv are indexed by global element number.
-template <bool kValues>
-SL_DEV int merge_row_smem(int32_t pa, int32_t ahi, int32_t pb, int32_t bhi,
-                          const int32_t* ac, const double* av, const int32_t* bc,
-                          const double* bv, int32_t* oc, double* ov) {
+// Count-only merge over the tile's unified column stage (A's slice at
+// [ia, iah), B's at [ib, ibh) of one shared array, 32-bit indices): the number
+// of distinct columns in A's row (unique) union B's row (sorted, possibly
+// repeated).  One element of either operand is consumed per iteration (A
+// first on ties) and a new output starts whenever the column differs from the
+// previous one, so matches and duplicate-B groups need no separate paths.
+// (ncu, D4: the pairwise merge with a duplicate look-ahead ran 30M warp
+// instructions at 90% issue; this form, with one shared load per element and
+// no 64-bit pointer selects, is what the count pass executes.)
+SL_DEV int count_row_idx(int ia, int iah, int ib, int ibh, const int32_t* s_col) {
   int n = 0;
-  int32_t ca = pa < ahi ? ac[pa] : INT32_MAX;
-  int32_t cb = pb < bhi ? bc[pb] : INT32_MAX;
-  while (pa < ahi || pb < bhi) {
-    const int32_t c = ca < cb ? ca : cb;
-    const bool ha = ca == c, hb = cb == c;
-    int32_t pb1 = pb + 1;
-    int32_t cb1 = pb1 < bhi ? bc[pb1] : INT32_MAX;
-    if (kValues) {
-      const double a = av[pa];
-      double b = bv[pb];
-      if (hb && cb1 == c) {           // duplicate B coordinates: Python sum over the group
-        b = dadd(0.0, b);
-        do {
-          b = dadd(b, bv[pb1]);
-          ++pb1;
-          cb1 = pb1 < bhi ? bc[pb1] : INT32_MAX;
-        } while (cb1 == c);
-      }
-      const double e = ha ? (hb ? dadd(a, b) : a) : b;
-      oc[n] = c;
-      ov[n] = dadd(0.0, e);
-    } else if (hb && cb1 == c) {
-      do {
-        ++pb1;
-        cb1 = pb1 < bhi ? bc[pb1] : INT32_MAX;
-      } while (cb1 == c);
-    }
-    pa += ha;
-    const int32_t na_ = ac[pa];
-    ca = ha ? (pa < ahi ? na_ : INT32_MAX) : ca;
-    pb = hb ? pb1 : pb;
-    cb = hb ? cb1 : cb;
-    ++n;
+  int32_t last = -1;
+  int32_t ca = ia < iah ? s_col[ia] : INT32_MAX;
+  int32_t cb = ib < ibh ? s_col[ib] : INT32_MAX;
+  for (int it = (iah - ia) + (ibh - ib); it > 0; --it) {
+    const bool ta = ca <= cb;
+    const int32_t c = ta ? ca : cb;
+    n += c != last;
+    last = c;
+    ia += ta;
+    ib += !ta;
+    const int idx = ta ? ia : ib;
+    const int32_t nx = idx < (ta ? iah : ibh) ? s_col[idx] : INT32_MAX;
+    ca = ta ? nx : ca;
+    cb = ta ? cb : nx;
   }
   return n;
+}
+
+// Fill merge in the same single-stream form (values staged at the same
+// indices as their columns): each iteration consumes one element, folds it
+// into the current output run (A value; B group sum in the reference's order,
+// (0 + b1) + b2 ... for a repeated coordinate, b1 alone otherwise) and
+// rewrites the run's output slot; the slot's last write, at the run's last
+// element, is the final value 0 + (a + bgroup | a | bgroup) (engine.py:404,
+// 413, 524-531, 625-631).  No divergent branches.
+SL_DEV int fill_row_idx(int ia, int iah, int ib, int ibh, const int32_t* s_col,
+                        const double* s_val, int32_t* oc, double* ov) {
+  int n = -1;
+  int32_t last = -1;
+  double ra = 0.0, bs = 0.0;
+  bool has_a = false;
+  int nb = 0;
+  int32_t ca = ia < iah ? s_col[ia] : INT32_MAX;
+  int32_t cb = ib < ibh ? s_col[ib] : INT32_MAX;
+  for (int it = (iah - ia) + (ibh - ib); it > 0; --it) {
+    const bool ta = ca <= cb;
+    const int32_t c = ta ? ca : cb;
+    const double v = s_val[ta ? ia : ib];
+    const bool fresh = c != last;
+    n += fresh;
+    last = c;
+    has_a = (fresh ? false : has_a) || ta;
+    nb = fresh ? 0 : nb;
+    ra = ta ? v : ra;
+    const double bnext = nb == 0 ? v : dadd(nb == 1 ? dadd(0.0, bs) : bs, v);
+    bs = ta ? bs : bnext;
+    nb += !ta;
+    const double e = has_a ? (nb ? dadd(ra, bs) : ra) : bs;
+    oc[n] = c;
+    ov[n] = dadd(0.0, e);
+    ia += ta;
+    ib += !ta;
+    const int idx = ta ? ia : ib;
+    const int32_t nx = idx < (ta ? iah : ibh) ? s_col[idx] : INT32_MAX;
+    ca = ta ? nx : ca;
+    cb = ta ? cb : nx;
+  }
+  return n + 1;
 }
 
 struct NoEmit {
@@ -182,20 +220,8 @@ constexpr int kAddRows = 128;
 constexpr int kAddCap = 768;     // staged elements per operand per tile (Poisson(5) tiles: 640 +- 25)
 constexpr int kSuper = 64;       // tiles per super-tile of the two-level prefix
 
-// Accessors: the whole tile staged in shared memory (the common case), or
-// read from global memory when a tile exceeds the stage capacity.
-struct SmemAcc {
-  const int32_t* s_acrd;
-  const double* s_aval;
-  const int32_t* s_bcol;
-  const double* s_bval;
-  int32_t ac0, bc0, av0, bv0;   // element index staged at smem index 0, per array
-  SL_DEV int32_t acol(int32_t p) const { return s_acrd[p - ac0]; }
-  SL_DEV double aval(int32_t p) const { return s_aval[p - av0]; }
-  SL_DEV int32_t bcol(int32_t p) const { return s_bcol[p - bc0]; }
-  SL_DEV double bval(int32_t p) const { return s_bval[p - bv0]; }
-};
-
+// Accessor for tiles that exceed the stage capacity (or unaligned operands):
+// elements read from global memory.
 struct GlobalAcc {
   const int32_t* a_crd;
   const double* a_vals;
@@ -250,11 +276,14 @@ add_tile_kernel(int64_t nrows, const int32_t* __restrict__ a_pos, const int32_t*
                 const int32_t* __restrict__ b_cols, const double* __restrict__ b_vals,
                 int32_t* __restrict__ c_pos, int32_t* __restrict__ c_crd,
                 double* __restrict__ c_vals, int64_t* __restrict__ tile_tot,
-                int64_t* __restrict__ super_tot) {
+                int64_t* __restrict__ super_tot, bool staged_ok) {
   constexpr bool kValues = kMode != 0;
   __shared__ int32_t s_apos[kAddRows + 1], s_bpos[kAddRows + 1];
-  __shared__ __align__(16) int32_t s_acrd[kAddCap + 8], s_bcol[kAddCap + 8];
-  __shared__ __align__(16) double s_aval[kValues ? kAddCap + 4 : 2], s_bval[kValues ? kAddCap + 4 : 2];
+  // unified stages: A's slice at [0, kCS), B's at [kCS, 2 kCS); a value is
+  // staged at the same index as its column
+  constexpr int kCS = kAddCap + 8;
+  __shared__ __align__(16) int32_t s_col[2 * kCS];
+  __shared__ __align__(16) double s_val[kValues ? 2 * kCS : 2];
   __shared__ int32_t s_rbase[kAddRows];         // row output offsets within the tile
   __shared__ int s_warp[kAddRows / 32];
   __shared__ int64_t s_tile_out;
@@ -278,7 +307,7 @@ add_tile_kernel(int64_t nrows, const int32_t* __restrict__ a_pos, const int32_t*
   const int32_t ea0 = s_apos[0], eb0 = s_bpos[0];
   const int32_t ea1 = s_apos[nr], eb1 = s_bpos[nr];
   const int na = ea1 - ea0, nb = eb1 - eb0;
-  const bool fits = na <= kAddCap && nb <= kAddCap;   // block-uniform
+  const bool fits = staged_ok && na <= kAddCap && nb <= kAddCap;   // block-uniform
   BulkRange<int32_t> ra{}, rb{};
   BulkRange<double> rav{}, rbv{};
   if (fits) {
@@ -288,36 +317,43 @@ add_tile_kernel(int64_t nrows, const int32_t* __restrict__ a_pos, const int32_t*
       rav = plan_range(a_vals, ea0, ea1);
       rbv = plan_range(b_vals, eb0, eb1);
     }
+    // element p of A lands at s_col[p - ra.lo0] and s_val[p - ra.lo0] (B: + kCS);
+    // with 16-byte-aligned operands (staged_ok) the value copies stay aligned
+    int32_t* sa = s_col;
+    int32_t* sb = s_col + kCS;
+    double* sav = s_val + (int32_t)(rav.lo0 - ra.lo0);
+    double* sbv = kValues ? s_val + kCS + (int32_t)(rbv.lo0 - rb.lo0) : s_val;
     if (tid == 0) {
       mbar_arrive_expect_tx(&bar, ra.tx_bytes + rb.tx_bytes + rav.tx_bytes + rbv.tx_bytes);
-      issue_range(a_crd, ra, s_acrd, &bar);
-      issue_range(b_cols, rb, s_bcol, &bar);
+      issue_range(a_crd, ra, sa, &bar);
+      issue_range(b_cols, rb, sb, &bar);
       if (kValues) {
-        issue_range(a_vals, rav, s_aval, &bar);
-        issue_range(b_vals, rbv, s_bval, &bar);
+        issue_range(a_vals, rav, sav, &bar);
+        issue_range(b_vals, rbv, sbv, &bar);
       }
     }
-    edge_loads_small(a_crd, ra, ea0, ea1, s_acrd, tid);
-    edge_loads_small(b_cols, rb, eb0, eb1, s_bcol, tid);
+    edge_loads_small(a_crd, ra, ea0, ea1, sa, tid);
+    edge_loads_small(b_cols, rb, eb0, eb1, sb, tid);
     if (kValues) {
-      edge_loads_small(a_vals, rav, ea0, ea1, s_aval, tid);
-      edge_loads_small(b_vals, rbv, eb0, eb1, s_bval, tid);
+      edge_loads_small(a_vals, rav, ea0, ea1, sav, tid);
+      edge_loads_small(b_vals, rbv, eb0, eb1, sbv, tid);
     }
     __syncthreads();
     mbar_wait(&bar, 0);
   }
   const bool mine = tid < nr;
-  const SmemAcc sacc{s_acrd, s_aval, s_bcol, s_bval, (int32_t)ra.lo0, (int32_t)rb.lo0,
-                     (int32_t)rav.lo0, (int32_t)rbv.lo0};
+  // this row's slices as stage indices
+  const int ia = mine ? s_apos[tid] - (int32_t)ra.lo0 : 0;
+  const int iah = mine ? s_apos[tid + 1] - (int32_t)ra.lo0 : 0;
+  const int ib = mine ? kCS + s_bpos[tid] - (int32_t)rb.lo0 : 0;
+  const int ibh = mine ? kCS + s_bpos[tid + 1] - (int32_t)rb.lo0 : 0;
   const GlobalAcc gacc{a_crd, a_vals, b_cols, b_vals};
   // ---- per-row counts (count mode) / row bases (fill modes)
   if (kMode == 0) {
     int cnt = 0;
     if (mine) {
       if (fits) {
-        cnt = merge_row_smem<false>(s_apos[tid], s_apos[tid + 1], s_bpos[tid], s_bpos[tid + 1],
-                                    s_acrd - ra.lo0, nullptr, s_bcol - rb.lo0, nullptr, nullptr,
-                                    nullptr);
+        cnt = count_row_idx(ia, iah, ib, ibh, s_col);
       } else {
         cnt = merge_row<false>(s_apos[tid], s_apos[tid + 1], s_bpos[tid], s_bpos[tid + 1], gacc,
                                NoEmit{});
@@ -361,9 +397,7 @@ add_tile_kernel(int64_t nrows, const int32_t* __restrict__ a_pos, const int32_t*
   if (mine) {
     const int32_t lo = s_rbase[tid];
     if (fits)
-      merge_row_smem<true>(s_apos[tid], s_apos[tid + 1], s_bpos[tid], s_bpos[tid + 1],
-                           s_acrd - ra.lo0, s_aval - rav.lo0, s_bcol - rb.lo0, s_bval - rbv.lo0,
-                           oc + lo, ov + lo);
+      fill_row_idx(ia, iah, ib, ibh, s_col, s_val, oc + lo, ov + lo);
     else
       merge_row<true>(s_apos[tid], s_apos[tid + 1], s_bpos[tid], s_bpos[tid + 1], gacc,
                       FillEmit{oc + lo, ov + lo});
@@ -414,6 +448,13 @@ extern "C" size_t sl_add_csr_workspace_bytes(int64_t nrows, int64_t b_nnz) {
          256;
 }
 
+// the fill stages values at their columns' indices: needs 16-byte-aligned operands
+static bool add_staged_ok(const int32_t* ac, const double* av, const int32_t* bc,
+                          const double* bv) {
+  return sl_host::aligned16(ac) && sl_host::aligned16(av) && sl_host::aligned16(bc) &&
+         sl_host::aligned16(bv);
+}
+
 struct AddWs {
   int64_t* tiles;
   int64_t* supers;
@@ -457,7 +498,7 @@ static const int32_t* add_count_pass(int64_t nrows, const int32_t* a_pos, const 
   const int32_t* bp = add_rowptr(nrows, b_nnz, b_pos, b_rows, w, true, s);
   add_tile_kernel<0><<<(int)add_ntiles(nrows), kAddRows, 0, s>>>(
       nrows, a_pos, a_crd, nullptr, bp, b_cols, nullptr, c_pos, nullptr, nullptr, w.tiles,
-      w.supers);
+      w.supers, true);
   return bp;
 }
 
@@ -491,7 +532,7 @@ extern "C" int sl_add_csr_fill(int64_t nrows, const int32_t* a_pos, const int32_
   const int32_t* bp = add_rowptr(nrows, b_nnz, b_pos, b_rows, w, false, s);
   add_tile_kernel<1><<<(int)add_ntiles(nrows), kAddRows, 0, s>>>(
       nrows, a_pos, a_crd, a_vals, bp, b_cols, b_vals, const_cast<int32_t*>(c_pos), c_crd, c_vals,
-      w.tiles, w.supers);
+      w.tiles, w.supers, add_staged_ok(a_crd, a_vals, b_cols, b_vals));
   return sl_host::launch_status();
 }
 
@@ -508,6 +549,7 @@ extern "C" int sl_add_csr_f64(int64_t nrows, const int32_t* a_pos, const int32_t
   const AddWs w = add_ws(ws, nrows);
   const int32_t* bp = add_count_pass(nrows, a_pos, a_crd, b_nnz, b_pos, b_rows, b_cols, c_pos, w, s);
   add_tile_kernel<2><<<(int)add_ntiles(nrows), kAddRows, 0, s>>>(
-      nrows, a_pos, a_crd, a_vals, bp, b_cols, b_vals, c_pos, c_crd, c_vals, w.tiles, w.supers);
+      nrows, a_pos, a_crd, a_vals, bp, b_cols, b_vals, c_pos, c_crd, c_vals, w.tiles, w.supers,
+      add_staged_ok(a_crd, a_vals, b_cols, b_vals));
   return sl_host::launch_status();
 }
