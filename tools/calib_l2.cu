@@ -55,6 +55,13 @@ __global__ void gather8_kernel(const double* __restrict__ x, const int32_t* __re
   if (acc == 12345.678) out[0] = acc;
 }
 
+__global__ void empty_kernel() {}
+
+extern "C" int calib_empty(int blocks, void* stream) {
+  empty_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>();
+  return (int)cudaGetLastError();
+}
+
 extern "C" int calib_gather8(const double* x, const int32_t* idx, int64_t n, double* out,
                              int blocks, void* stream) {
   gather8_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(x, idx, n, out);

@@ -70,6 +70,18 @@ def main():
         best = max(best, ix.numel() / t / 1e9)
         res[f"gather8_2M_{blocks}blk_us"] = round(t * 1e6, 2)
     res["gather8_G_per_s"] = round(best, 1)
+    # the same at 10x the count: separates throughput from the fixed
+    # launch/ramp/event cost of a ~20 us kernel
+    ix20 = torch.randint(0, x.numel(), (20_000_000,), dtype=torch.int32, device=dev)
+    best20 = 0.0
+    for blocks in (sm * 4, sm * 8, sm * 16):
+        t = timeit(lambda: L.calib_gather8(ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(ix20.data_ptr()),
+                                           ctypes.c_int64(ix20.numel()), ctypes.c_void_p(out.data_ptr()),
+                                           blocks, ctypes.c_void_p(s)))
+        best20 = max(best20, ix20.numel() / t / 1e9)
+        res[f"gather8_20M_{blocks}blk_us"] = round(t * 1e6, 2)
+    res["gather8_20M_G_per_s"] = round(best20, 1)
+    res["empty_kernel_event_us"] = round(timeit(lambda: L.calib_empty(sm, ctypes.c_void_p(s))) * 1e6, 2)
     # L2-resident stream (.cg), 32 MB buffer read 20 times
     buf = torch.randn(4 << 20, dtype=torch.float64, device=dev)
     reps = 20
