@@ -28,6 +28,8 @@ def main():
     ap.add_argument("--reps", type=int, default=200)
     ap.add_argument("--cfgs", default="0,1,2,3,4,5,6,7")
     ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--var", type=int, default=4)
+    ap.add_argument("--env", default="SL_CSR_RING")
     ap.add_argument("--mats", default="stencil27,d1,ragged")
     args = ap.parse_args()
     dev = torch.device("cuda", 0)
@@ -61,10 +63,10 @@ def main():
         nnz = len(crd)
         nbytes = 4 * (n + 1) + 12 * nnz + 16 * n
         fns = {"v0": lambda: K.spmv_csr(n, n, p, c, v, xx, variant=0),
-               "v3": lambda: K.spmv_csr(n, n, p, c, v, xx, variant=3)}
+               "v5": lambda: K.spmv_csr(n, n, p, c, v, xx, variant=5)}
         for cfg in args.cfgs.split(","):
-            os.environ["SL_CSR_RING"] = cfg
-            y = K.spmv_csr(n, n, p, c, v, xx, variant=4)
+            os.environ[args.env] = cfg
+            y = K.spmv_csr(n, n, p, c, v, xx, variant=args.var)
             torch.cuda.synchronize()
             ok = torch.equal(y.view(torch.int64), y0.view(torch.int64))
             print(f"{name} ring cfg {cfg}: bit-exact vs v0: {ok}", flush=True)
@@ -73,8 +75,8 @@ def main():
                 print("   first mismatches", bad, y[bad].tolist(), y0[bad].tolist())
 
             def f(cfg=cfg):
-                os.environ["SL_CSR_RING"] = cfg
-                K.spmv_csr(n, n, p, c, v, xx, variant=4)
+                os.environ[args.env] = cfg
+                K.spmv_csr(n, n, p, c, v, xx, variant=args.var)
             fns[f"ring{cfg}"] = f
         if name == "ragged":
             continue
