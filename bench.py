@@ -532,7 +532,9 @@ def run_reference(args, rank, world):
 
     st = wl.stencil27(g=G, gz=G * world, z0=0, z1=G * world)
     ell = wl.csr_to_ell(st["pos"], st["crd"], st["vals"], st["nrows"])
-    thr = oracle.num_threads()
+    # every host thread this process may run on (torchrun exports
+    # OMP_NUM_THREADS=1, which would otherwise pin the reference arm to 1 core)
+    thr = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
     nrows = st["nrows"]
     b = bytes_csr(nrows, len(st["crd"])) + bytes_ell(nrows, ell["nslots"])
     for _ in range(args.warmup):
@@ -582,9 +584,17 @@ def main():
     import torch
     import torch.distributed as dist
 
+    # one rank per GPU; SL_BENCH_BACKEND=gloo (with ranks folded onto the
+    # visible GPUs) only smoke-tests the multi-rank code path on a 1-GPU box —
+    # its numbers are not measurements
+    local_rank = local_rank % max(1, torch.cuda.device_count())
+    backend = os.environ.get("SL_BENCH_BACKEND", "nccl")
     if world > 1:
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        else:
+            dist.init_process_group(backend)
     from paper_1804_10112_b200 import _lib
 
     _lib.load()   # fail loudly if the kernel library is missing
