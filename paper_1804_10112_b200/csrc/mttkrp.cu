@@ -280,30 +280,51 @@ struct CsfSrc {
   int64_t f, s;        // fiber / slice of the batch's first nonzero (warp-uniform)
   int32_t nk;
   double nv;
+  // the batch's fiber-end / fiber-j / slice-end / slice-i windows, loaded one
+  // batch ahead: the next batch's first fiber and slice follow from the
+  // current windows alone, so these loads are never on the critical path
+  // (loading them at the start of each batch put an L2 round trip per 32
+  // nonzeros in series: CSF 1.25 ms vs COO-3 1.00 ms)
+  int32_t wfe, wjw, wse, wiw;
   SL_DEV void prefetch(int64_t base, int lane) {
     if (base + lane < e1) {
       nk = ld_stream(crd2 + base + lane);
       nv = ld_stream(vals + base + lane);
     }
   }
-  SL_DEV void start(int64_t e0, int lane) { prefetch(e0, lane); }
+  SL_DEV void load_windows(int lane) {
+    wfe = f + 1 + lane <= nfibers ? ldg(pos2 + f + 1 + lane) : INT32_MAX;
+    wjw = f + lane < nfibers ? ldg(crd1 + f + lane) : 0;
+    wse = s + 1 + lane <= nslices ? ldg(pos1 + s + 1 + lane) : INT32_MAX;
+    wiw = s + lane < nslices ? ldg(crd0 + s + lane) : 0;
+  }
+  SL_DEV void start(int64_t e0, int lane) {
+    prefetch(e0, lane);
+    load_windows(lane);
+  }
   SL_DEV void next(int64_t base, int lane, int32_t& li, int32_t& lj, int32_t& lk, double& lv) {
-    const int32_t fe = f + 1 + lane <= nfibers ? ldg(pos2 + f + 1 + lane) : INT32_MAX;
-    const int32_t jw = f + lane < nfibers ? ldg(crd1 + f + lane) : 0;
-    const int32_t se = s + 1 + lane <= nslices ? ldg(pos1 + s + 1 + lane) : INT32_MAX;
-    const int32_t iw = s + lane < nslices ? ldg(crd0 + s + lane) : 0;
+    const int32_t fe = wfe, jw = wjw, se = wse, iw = wiw;
     const int32_t e = (int32_t)(base + lane);
     const int df = window_count_le(fe, e);
     lj = __shfl_sync(0xffffffffu, jw, df);
     const int32_t fib = (int32_t)(f + df);
-    const int ds = window_count_le(se, fib);
-    li = __shfl_sync(0xffffffffu, iw, ds);
+    // slices average 2000 nonzeros: a batch usually lies in one slice (the
+    // first slice ends after the batch's last fiber) and skips the search
+    const int32_t se0 = __shfl_sync(0xffffffffu, se, 0);
+    const int32_t fib_last = __shfl_sync(0xffffffffu, fib, 31);
+    if (se0 > fib_last) {
+      li = __shfl_sync(0xffffffffu, iw, 0);
+    } else {
+      const int ds = window_count_le(se, fib);
+      li = __shfl_sync(0xffffffffu, iw, ds);
+    }
     lk = nk;
     lv = nv;
-    // advance to the next batch's first nonzero
+    // advance to the next batch's first nonzero and start its loads
     f += __popc(__ballot_sync(0xffffffffu, fe <= (int32_t)(base + 32)));
     s += __popc(__ballot_sync(0xffffffffu, se <= (int32_t)f));
     prefetch(base + 32, lane);
+    load_windows(lane);
   }
 };
 
