@@ -656,7 +656,8 @@ constexpr int kEllBatch = 9;   // slots loaded per batch (27 = 3 batches for the
 // waves, so later blocks' loads overlap earlier blocks' gathers and adds
 // (measured 24.2 -> 22.7 us; one wave at 8 blocks/SM starts every block's
 // batches in lockstep)
-__global__ void __launch_bounds__(256, 4)
+template <int kBatch, int kThreads, int kMinBlocks>
+__global__ void __launch_bounds__(kThreads, kMinBlocks)
 spmv_ell_kernel(int64_t nrows, int32_t nslots, const int32_t* __restrict__ crd,
                 const double* __restrict__ vals, const double* __restrict__ x,
                 double* __restrict__ y) {
@@ -664,17 +665,17 @@ spmv_ell_kernel(int64_t nrows, int32_t nslots, const int32_t* __restrict__ crd,
   if (i >= nrows) return;
   double a = 0.0;
   int32_t s0 = 0;
-  for (; s0 + kEllBatch <= nslots; s0 += kEllBatch) {   // full batches: no predicates
-    int32_t c[kEllBatch];
-    double v[kEllBatch], xv[kEllBatch];
+  for (; s0 + kBatch <= nslots; s0 += kBatch) {   // full batches: no predicates
+    int32_t c[kBatch];
+    double v[kBatch], xv[kBatch];
 #pragma unroll
-    for (int b = 0; b < kEllBatch; ++b) c[b] = ld_stream(crd + (int64_t)(s0 + b) * nrows + i);
+    for (int b = 0; b < kBatch; ++b) c[b] = ld_stream(crd + (int64_t)(s0 + b) * nrows + i);
 #pragma unroll
-    for (int b = 0; b < kEllBatch; ++b) v[b] = ld_stream(vals + (int64_t)(s0 + b) * nrows + i);
+    for (int b = 0; b < kBatch; ++b) v[b] = ld_stream(vals + (int64_t)(s0 + b) * nrows + i);
 #pragma unroll
-    for (int b = 0; b < kEllBatch; ++b) xv[b] = ldg(x + c[b]);
+    for (int b = 0; b < kBatch; ++b) xv[b] = ldg(x + c[b]);
 #pragma unroll
-    for (int b = 0; b < kEllBatch; ++b) a = dadd(a, dmul(v[b], xv[b]));
+    for (int b = 0; b < kBatch; ++b) a = dadd(a, dmul(v[b], xv[b]));
   }
   for (; s0 < nslots; ++s0) {
     const int64_t p = (int64_t)s0 * nrows + i;
@@ -927,7 +928,9 @@ extern "C" int sl_spmv_ell_f64(int64_t nrows, int64_t ncols, int32_t nslots, con
       spmv_path() == 2) {
     return sl_host::launch_ell_pipe(nrows, nslots, crd, vals, x, y, s);
   } else {
-    spmv_ell_kernel<<<ceil_div(nrows, 256), 256, 0, s>>>(nrows, nslots, crd, vals, x, y);
+    // batch 9 x 256 threads x 4 blocks/SM; batch 7-27 at 64-512 threads per
+    // block measured 20.5-24.5 us against 20.8 us here (profiles/ab/r1_ell_configs.txt)
+    spmv_ell_kernel<kEllBatch, 256, 4><<<ceil_div(nrows, 256), 256, 0, s>>>(nrows, nslots, crd, vals, x, y);
   }
   return sl_host::launch_status();
 }
