@@ -419,7 +419,9 @@ spmv_csr_rowblock_kernel(int64_t nrows, const int32_t* __restrict__ pos,
 // with double-buffered stages: 26.7-37.6 us; too few row-walking threads per
 // SM), and a persistent one-warp-per-block version that loads the next
 // tile's row bounds during the current walk (25.3-28.8 us at 10-20 blocks/SM:
-// hardware block scheduling of many short blocks beats the software loop).  On short, irregular rows (D1, Poisson(10)) the row walk diverges
+// hardware block scheduling of many short blocks beats the software loop).
+// Staging the range with 16-byte cp.async (LDGSTS) by all threads instead of
+// the bulk copy: 24.8 us (profiles/ab/r1_csr_stage_tma_vs_ldgsts.txt).  On short, irregular rows (D1, Poisson(10)) the row walk diverges
 // (warps run the longest row) and K2a stays faster (20.5 vs 29 us), so the
 // automatic choice takes K2f only for rows averaging >= 16 nonzeros.
 
