@@ -333,6 +333,28 @@ def run_ours(args, rank, world, local_rank):
         "clocks": clk.summary(),
     }
 
+    # ---- optional all-gather of the y row blocks (N > 1), timed on its own:
+    # the one data-path collective the north star allows after compute
+    if world > 1:
+        bounds = [nrows * p for p in range(world + 1)]
+        for _ in range(3):
+            D.gather_row_blocks(y1, bounds)
+        torch.cuda.synchronize()
+        dist.barrier()
+        reps = 20
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g0.record()
+        for _ in range(reps):
+            yfull = D.gather_row_blocks(y1, bounds)
+        g1.record()
+        torch.cuda.synchronize()
+        t_ag = D.max_over_ranks(g0.elapsed_time(g1) / reps, dev)
+        out["y_allgather"] = {"ms": round(t_ag, 5), "bytes_per_rank_out": nrows * 8,
+                              "full_y_bytes": int(yfull.numel() * 8),
+                              "GB/s_per_rank_in": round(yfull.numel() * 8 / (t_ag * 1e-3) / 1e9, 1),
+                              "note": "torch.distributed all_gather of padded y blocks "
+                                      "(NCCL); not part of `value`"}
+
     # ---- CPU baseline (rank 0, N = 1): the oracle port on the host cores
     if rank == 0 and world == 1:
         out["cpu_baseline"] = cpu_baseline(st, ell, args)
