@@ -259,7 +259,7 @@ def run_ours(args, rank, world, local_rank):
     dom = max(avg, key=avg.get)
     dom_bytes = b_csr if dom == "csr" else b_ell
     achieved = dom_bytes / (avg[dom] * 1e-3) / 1e9
-    kname = {"csr": "spmv_csr_stage_kernel", "ell": "spmv_ell_kernel"}[dom]
+    kname = {"csr": "spmv_csr_handoff_kernel", "ell": "spmv_ell_kernel"}[dom]
     traffic = traffic_db.get(kname)
 
     # ---- e2e through the public API: x from pinned host memory each step,

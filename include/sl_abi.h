@@ -153,8 +153,8 @@ int sl_spmv_coo_f64(int64_t nrows, int64_t ncols, int64_t nnz,
 
 /* CSR (formats.py:126-127). Replaces run_node(i) -> run_node(j) with
  * locate of x (engine.py:591-634).
- * variant 0 = automatic: row-stage (variant 4) when rows average >= 16
- *             nonzeros and crd/vals are 16-byte aligned, else row-block (5);
+ * variant 0 = automatic: register hand-off (variant 6) when rows average
+ *             <= 28 nonzeros and crd/vals are 16-byte aligned, else row-block (5);
  * variant 1 = vector-per-row (a warp per row; lanes load the row's nonzeros
  *             coalesced, lane 0 sums them in order from registers via shuffles);
  * variant 2 = merge-path (nnz+rows balanced tiles; row-owner sums in order);
@@ -164,6 +164,10 @@ int sl_spmv_coo_f64(int64_t nrows, int64_t ncols, int64_t nnz,
  *             must be 16-byte aligned, else SL_ERR_INVALID);
  * variant 5 = row-block (rows tiled; nonzeros of the tile staged through
  *             shared memory in coalesced chunks; thread per row sums in order);
+ * variant 6 = register hand-off (persistent one-warp blocks: a 32-row tile is
+ *             bulk-copied to shared memory, each lane moves its row into
+ *             registers and the next tile's copy starts while this one is
+ *             gathered and summed; 16-byte-aligned crd/vals, else SL_ERR_INVALID);
  * All variants are bit-identical.  ws may be NULL for every variant but 2. */
 size_t sl_spmv_csr_workspace_bytes(int64_t nrows, int64_t nnz, int32_t variant);
 int sl_spmv_csr_f64(int64_t nrows, int64_t ncols, int64_t nnz, const int32_t* pos,

@@ -510,6 +510,147 @@ static void launch_csr_stage(int64_t nrows, const int32_t* pos, const int32_t* c
   kern<<<(int)((nrows + kRows - 1) / kRows), kRows, smem, s>>>(nrows, pos, crd, vals, x, y);
 }
 
+// K2r: row-stage with a register hand-off.  K2f holds its shared-memory stage
+// for the whole walk (gathers and the ordered add chain), which caps the rows
+// in flight at ~640 per SM.  Here a persistent one-warp block copies each
+// lane's row (<= kMaxRow nonzeros) from the stage into registers and at once
+// bulk-copies the NEXT tile into the same stage, so one tile's gathers and
+// adds overlap the next tile's HBM read.  Tiles with a longer row walk the
+// stage as K2f does; tiles beyond the stage capacity read global memory.
+template <int kCap, int kMaxRow, int kBatch, int kMinBlocks>
+__global__ void __launch_bounds__(32, kMinBlocks)
+spmv_csr_handoff_kernel(int64_t nrows, const int32_t* __restrict__ pos,
+                        const int32_t* __restrict__ crd, const double* __restrict__ vals,
+                        const double* __restrict__ x, double* __restrict__ y) {
+  static_assert(kCap % 4 == 0 && kMaxRow % kBatch == 0, "shapes");
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw);
+  int32_t* s_crd = reinterpret_cast<int32_t*>(smem_raw + 16);
+  double* s_val = reinterpret_cast<double*>(smem_raw + 16 + kCap * 4);
+  const int lane = threadIdx.x;
+  const int64_t ntiles = (nrows + 31) / 32;
+  int64_t tile = blockIdx.x;
+  if (tile >= ntiles) return;
+  if (lane == 0) {
+    mbar_init(bar, 1);
+    fence_mbar_init();
+  }
+  __syncwarp();
+  auto issue = [&](int32_t a0, int32_t ee) {   // lane 0: stage [a0, ee) (granule-rounded)
+    const uint32_t bc = (uint32_t)(((ee - a0 + 3) & ~3) * 4);
+    const uint32_t bv = (uint32_t)(((ee - a0 + 1) & ~1) * 8);
+    mbar_arrive_expect_tx(bar, bc + bv);
+    bulk_g2s(s_crd, crd + a0, bc, bar);
+    bulk_g2s(s_val, vals + a0, bv, bar);
+  };
+  int64_t r0 = tile * 32;
+  int nr = (int)min64(32, nrows - r0);
+  int32_t pb = lane < nr ? ldg(pos + r0 + lane) : 0;
+  int32_t pe = lane < nr ? ldg(pos + r0 + lane + 1) : 0;
+  int32_t eb = __shfl_sync(0xffffffffu, pb, 0), ee = __shfl_sync(0xffffffffu, pe, nr - 1);
+  int32_t a0 = eb & ~3;
+  bool staged = ee > eb && ee - a0 <= kCap;
+  if (staged && lane == 0) issue(a0, ee);
+  uint32_t phase = 0;
+  for (;;) {
+    // next tile's bounds: in flight during this tile's wait and copy
+    const int64_t next = tile + gridDim.x;
+    const int64_t nr0 = next * 32;
+    const int nnr = next < ntiles ? (int)min64(32, nrows - nr0) : 0;
+    const int32_t npb = lane < nnr ? ldg(pos + nr0 + lane) : 0;
+    const int32_t npe = lane < nnr ? ldg(pos + nr0 + lane + 1) : 0;
+    auto issue_next = [&]() -> bool {
+      if (nnr == 0) return false;
+      const int32_t neb = __shfl_sync(0xffffffffu, npb, 0);
+      const int32_t nee = __shfl_sync(0xffffffffu, npe, nnr - 1);
+      const bool ns = nee > neb && nee - (neb & ~3) <= kCap;
+      if (ns && lane == 0) {
+        fence_proxy_async_smem();
+        issue(neb & ~3, nee);
+      }
+      return ns;
+    };
+    double acc = 0.0;
+    bool next_staged;
+    const int len = pe - pb;
+    if (staged) {
+      mbar_wait(bar, phase);
+      phase ^= 1u;
+      const int off = pb - a0;
+      if (__all_sync(0xffffffffu, len <= kMaxRow)) {
+        int32_t c[kMaxRow];
+        double v[kMaxRow];
+#pragma unroll
+        for (int u = 0; u < kMaxRow; ++u) {
+          c[u] = u < len ? s_crd[off + u] : 0;
+          v[u] = u < len ? s_val[off + u] : 0.0;
+        }
+        __syncwarp();                     // every lane's row is in registers
+        next_staged = issue_next();
+#pragma unroll
+        for (int u0 = 0; u0 < kMaxRow; u0 += kBatch) {
+          double xv[kBatch];
+#pragma unroll
+          for (int b = 0; b < kBatch; ++b) xv[b] = u0 + b < len ? ldg(x + c[u0 + b]) : 0.0;
+#pragma unroll
+          for (int b = 0; b < kBatch; ++b)
+            if (u0 + b < len) acc = dadd(acc, dmul(v[u0 + b], xv[b]));
+        }
+      } else {
+        for (int u = 0; u < len; ++u) acc = dadd(acc, dmul(s_val[off + u], ldg(x + s_crd[off + u])));
+        __syncwarp();
+        next_staged = issue_next();
+      }
+    } else {
+      // tile beyond the stage capacity (long rows): the warp takes its rows one
+      // at a time, 32 products in parallel, added in order via shuffles (K2b)
+      next_staged = issue_next();
+      for (int rr = 0; rr < nr; ++rr) {
+        const int32_t b = __shfl_sync(0xffffffffu, pb, rr), e = __shfl_sync(0xffffffffu, pe, rr);
+        double a = 0.0;
+        for (int32_t c0 = b; c0 < e; c0 += 32) {
+          const int32_t q = c0 + lane;
+          const double t = q < e ? dmul(ld_stream(vals + q), ldg(x + ld_stream(crd + q))) : 0.0;
+          const int n = min(32, e - c0);
+          for (int u = 0; u < n; ++u) a = dadd(a, __shfl_sync(0xffffffffu, t, u));
+        }
+        if (lane == rr) acc = a;
+      }
+    }
+    if (lane < nr) y[r0 + lane] = acc;
+    if (nnr == 0) break;
+    tile = next;
+    r0 = nr0;
+    nr = nnr;
+    pb = npb;
+    pe = npe;
+    eb = __shfl_sync(0xffffffffu, pb, 0);
+    a0 = eb & ~3;
+    staged = next_staged;
+  }
+}
+
+template <int kCap, int kMaxRow, int kBatch, int kMinBlocks>
+static void launch_csr_handoff(int64_t nrows, const int32_t* pos, const int32_t* crd,
+                               const double* vals, const double* x, double* y, int blocks_per_sm,
+                               cudaStream_t s) {
+  constexpr size_t smem = 16 + (size_t)kCap * 12;
+  const int64_t ntiles = (nrows + 31) / 32;
+  const int grid = (int)min64(ntiles, (int64_t)sl_host::sm_count() * blocks_per_sm);
+  spmv_csr_handoff_kernel<kCap, kMaxRow, kBatch, kMinBlocks><<<grid, 32, smem, s>>>(
+      nrows, pos, crd, vals, x, y);
+}
+
+// 896-element stage (28 per row), rows of up to 28 nonzeros in registers,
+// gathers in two batches of 14, 12 one-warp blocks per SM (146 registers):
+// 64^3 stencil 22.4 us, D1 19.3 us, against K2f 23.8 / K2a 20.5 us; 14-27
+// element batches, 10-24 blocks/SM and a 32-nonzero register row measured
+// 22.4-27.2 / 19.3-24.4 us (profiles/ab/r1_csr_handoff*.txt)
+constexpr int kCsrHandoffCap = 896;
+constexpr int kCsrHandoffMaxRow = 28;
+constexpr int kCsrHandoffBatch = 14;
+constexpr int kCsrHandoffBlocks = 12;
+
 // K2d: CSR warp row-block.  Each warp owns 32 consecutive rows; their
 // nonzeros (contiguous) are staged in warp-private shared memory in rounds of
 // 256 products (8 coalesced loads per lane), and lane r adds the round's
@@ -789,17 +930,21 @@ static int launch_csr(int64_t nrows, int64_t nnz, const int32_t* pos, const int3
     const double* xd = reinterpret_cast<const XOperand<0>&>(xop).x;
     return sl_host::launch_csr_pipe(nrows, pos, crd, vals, xd, y, s);
   } else if (variant == 0 || variant == 5) {
-    // variant 0 (automatic): rows averaging >= 16 nonzeros take the row-stage
-    // kernel K2f, the rest the row-block kernel K2a (variant 5 forces K2a).
+    // variant 0 (automatic): rows averaging <= 28 nonzeros (aligned crd/vals)
+    // take the register hand-off kernel K2r, longer rows the row-block kernel
+    // K2a, whose staged products keep very long rows parallel (variant 5
+    // forces K2a).
     // K2a: short rows (<= 16 per row on average): 192-row blocks, about one chunk
     // each and more blocks than resident slots, so blocks' load and sum phases
     // interleave (D1 22.8 -> 21.2 us, hashed x 40.7 -> 32.8 us); long rows
     // (the 27-point stencil) keep 256-row blocks (29.0 vs 35.2 us)
     // (nnz < 0: not known to the entry point — the located-x paths, whose
     // per-nonzero locate latency also favours more, smaller blocks)
-    if (variant == 0 && !kHashX && nnz >= 16 * nrows && aligned16(crd) && aligned16(vals)) {
-      launch_csr_stage<kCsrStageRows, kCsrStageCap, kCsrStageBatch, kCsrStageBlocks>(
-          nrows, pos, crd, vals, reinterpret_cast<const XOperand<0>&>(xop).x, y, s);
+    if (variant == 0 && !kHashX && nnz >= 0 && nnz <= (int64_t)kCsrHandoffMaxRow * nrows &&
+        aligned16(crd) && aligned16(vals)) {
+      launch_csr_handoff<kCsrHandoffCap, kCsrHandoffMaxRow, kCsrHandoffBatch, kCsrHandoffBlocks>(
+          nrows, pos, crd, vals, reinterpret_cast<const XOperand<0>&>(xop).x, y,
+          kCsrHandoffBlocks, s);
       return sl_host::launch_status();
     }
     if (nnz <= 16 * nrows) {
@@ -813,6 +958,10 @@ static int launch_csr(int64_t nrows, int64_t nnz, const int32_t* pos, const int3
     if (!aligned16(crd) || !aligned16(vals)) return SL_ERR_INVALID;
     launch_csr_stage<kCsrStageRows, kCsrStageCap, kCsrStageBatch, kCsrStageBlocks>(
         nrows, pos, crd, vals, reinterpret_cast<const XOperand<0>&>(xop).x, y, s);
+  } else if (variant == 6 && !kHashX) {
+    if (!aligned16(crd) || !aligned16(vals)) return SL_ERR_INVALID;
+    launch_csr_handoff<kCsrHandoffCap, kCsrHandoffMaxRow, kCsrHandoffBatch, kCsrHandoffBlocks>(
+        nrows, pos, crd, vals, reinterpret_cast<const XOperand<0>&>(xop).x, y, kCsrHandoffBlocks, s);
   } else if (variant == 3 && !kHashX) {
     const double* xd = reinterpret_cast<const XOperand<0>&>(xop).x;
     spmv_csr_warp_kernel<<<ceil_div(nrows, 256), 256, 0, s>>>(nrows, pos, crd, vals, xd, y);

@@ -43,7 +43,7 @@ def test_spmv_goldens_all_formats(golden):
                            cuda(c["coo_cols"], np.int32), cuda(c["coo_vals"], np.float64), x)
             assert np.array_equal(bits(y), bits(c["coo_y"])), name
         if "csr_y" in c:
-            for variant in (0, 1, 2, 3, 4, 5):
+            for variant in (0, 1, 2, 3, 4, 5, 6):
                 y = K.spmv_csr(nrows, ncols, cuda(c["csr_pos"], np.int32),
                                cuda(c["csr_crd"], np.int32), cuda(c["csr_vals"], np.float64), x,
                                variant=variant)
@@ -85,7 +85,7 @@ def test_spmv_coo_csr_vs_oracle(orc, n, nnz, lam, seed):
     y = K.spmv_coo(n, d["ncols"], cuda(d["rows"]), cuda(d["cols"]), cuda(d["vals"]), x)
     assert np.array_equal(bits(y), bits(ref))
     pos = wl.coo_to_csr_pos(d["rows"], n)
-    for variant in (0, 1, 2, 3, 4, 5):
+    for variant in (0, 1, 2, 3, 4, 5, 6):
         y = K.spmv_csr(n, d["ncols"], cuda(pos), cuda(d["cols"]), cuda(d["vals"]), x,
                        variant=variant)
         assert np.array_equal(bits(y), bits(ref)), variant
@@ -109,8 +109,31 @@ def test_spmv_coo_long_rows_cross_tiles(orc):
     # the same rows through every CSR variant (row-stage: blocks far beyond
     # one staging round, rows cut by rounds)
     pos = wl.coo_to_csr_pos(rows, 8)
-    for variant in (0, 1, 2, 3, 4, 5):
+    for variant in (0, 1, 2, 3, 4, 5, 6):
         y = K.spmv_csr(8, 20000, cuda(pos), cuda(cols), cuda(vals), cuda(x), variant=variant)
+        assert np.array_equal(bits(y), bits(ref)), variant
+
+
+def test_spmv_csr_handoff_paths(orc):
+    # 32-row tiles exercising each path of the register hand-off kernel: rows
+    # <= 28 nonzeros (registers), a longer row inside the stage capacity (the
+    # tile walks the stage), a tile beyond the capacity (warp per row), empty
+    # rows and an empty tile, a partial last tile
+    rng = np.random.default_rng(11)
+    n, m = 230, 5000
+    lens = rng.integers(0, 12, n)
+    lens[3], lens[70], lens[100], lens[150] = 40, 29, 0, 200
+    lens[160:192] = 30                      # 960 nonzeros in one tile: > 896
+    lens[192:224] = 0                       # an empty tile
+    cols = np.concatenate([np.sort(rng.choice(m, k, replace=False)) for k in lens]).astype(np.int32)
+    pos = np.zeros(n + 1, np.int32)
+    pos[1:] = np.cumsum(lens)
+    vals = rng.uniform(-1, 1, len(cols))
+    x = rng.uniform(-1, 1, m)
+    ref, _ = orc.spmv_csr(n, pos, cols, vals, x)
+    for variant in (0, 4, 5, 6):
+        y = cuda(np.full(n, np.nan))
+        K.spmv_csr(n, m, cuda(pos), cuda(cols), cuda(vals), cuda(x), y=y, variant=variant)
         assert np.array_equal(bits(y), bits(ref)), variant
 
 
@@ -134,7 +157,7 @@ def test_spmv_empty_matrix():
     y = K.spmv_coo(9, 5, cuda(np.zeros(0, np.int32)), cuda(np.zeros(0, np.int32)),
                    cuda(np.zeros(0)), x)
     assert np.array_equal(bits(y), bits(np.zeros(9)))
-    for variant in (0, 1, 2, 3, 4, 5):     # y pre-filled with NaN: every row must be written
+    for variant in (0, 1, 2, 3, 4, 5, 6):     # y pre-filled with NaN: every row must be written
         y = cuda(np.full(9, np.nan))
         K.spmv_csr(9, 5, cuda(np.zeros(10, np.int32)), cuda(np.zeros(0, np.int32)),
                    cuda(np.zeros(0)), x, y=y, variant=variant)
@@ -163,7 +186,7 @@ def test_full_size_spmv_bit_exact(orc):
     s = wl.stencil27()
     ref, _ = orc.spmv_csr(s["nrows"], s["pos"], s["crd"], s["vals"], s["x"])
     x = cuda(s["x"])
-    for variant in (0, 1, 2, 3, 4, 5):
+    for variant in (0, 1, 2, 3, 4, 5, 6):
         y = K.spmv_csr(s["nrows"], s["ncols"], cuda(s["pos"]), cuda(s["crd"]), cuda(s["vals"]),
                        x, variant=variant)
         assert np.array_equal(bits(y), bits(ref)), variant
