@@ -16,13 +16,15 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <stdlib.h>
+
 #include <algorithm>
 
 #include "common.cuh"
 
 namespace sl {
 
-template <int G>
+template <int G, int kB = 4>
 __global__ void __launch_bounds__(256)
 spmm_csr_kernel(int64_t nrows, int64_t K, const int32_t* __restrict__ pos,
                 const int32_t* __restrict__ crd, const double* __restrict__ vals,
@@ -49,18 +51,18 @@ spmm_csr_kernel(int64_t nrows, int64_t K, const int32_t* __restrict__ pos,
         const int n = min(G, e - c0);
         const unsigned gmask = G == 32 ? 0xffffffffu : (((1u << G) - 1u) << (g * G));
         int u = 0;
-        for (; u + 4 <= n; u += 4) {
-          int32_t c[4];
-          double a[4], xv[4];
+        for (; u + kB <= n; u += kB) {
+          int32_t c[kB];
+          double a[kB], xv[kB];
 #pragma unroll
-          for (int t = 0; t < 4; ++t) {
+          for (int t = 0; t < kB; ++t) {
             c[t] = __shfl_sync(gmask, cq, u + t, G);
             a[t] = __shfl_sync(gmask, vq, u + t, G);
           }
 #pragma unroll
-          for (int t = 0; t < 4; ++t) xv[t] = kin ? ldg(X + (int64_t)c[t] * K + k) : 0.0;
+          for (int t = 0; t < kB; ++t) xv[t] = kin ? ldg(X + (int64_t)c[t] * K + k) : 0.0;
 #pragma unroll
-          for (int t = 0; t < 4; ++t) acc = dadd(acc, dmul(a[t], xv[t]));
+          for (int t = 0; t < kB; ++t) acc = dadd(acc, dmul(a[t], xv[t]));
         }
         for (; u < n; ++u) {
           const int32_t c = __shfl_sync(gmask, cq, u, G);
@@ -94,7 +96,10 @@ extern "C" int sl_spmm_csr_f64(int64_t nrows, int64_t ncols, int64_t K, const in
                                           (int64_t)sl_host::sm_count() * 64);
   switch (G) {
     case 32: spmm_csr_kernel<32><<<grid, 256, 0, s>>>(nrows, K, pos, crd, vals, X, Y); break;
-    case 16: spmm_csr_kernel<16><<<grid, 256, 0, s>>>(nrows, K, pos, crd, vals, X, Y); break;
+    case 16:   // gathers 2 at a time: 122.9 us vs 130.0 / 133.4 / 244.0 us with 4 / 8 / 16
+               // (64^3 stencil, K = 16: throughput-, not latency-bound; tools/ab_spmm.py)
+      spmm_csr_kernel<16, 2><<<grid, 256, 0, s>>>(nrows, K, pos, crd, vals, X, Y);
+      break;
     case 8: spmm_csr_kernel<8><<<grid, 256, 0, s>>>(nrows, K, pos, crd, vals, X, Y); break;
     case 4: spmm_csr_kernel<4><<<grid, 256, 0, s>>>(nrows, K, pos, crd, vals, X, Y); break;
     case 2: spmm_csr_kernel<2><<<grid, 256, 0, s>>>(nrows, K, pos, crd, vals, X, Y); break;
