@@ -517,11 +517,35 @@ static void launch_csr_stage(int64_t nrows, const int32_t* pos, const int32_t* c
 // bulk-copies the NEXT tile into the same stage, so one tile's gathers and
 // adds overlap the next tile's HBM read.  Tiles with a longer row walk the
 // stage as K2f does; tiles beyond the stage capacity read global memory.
-template <int kCap, int kMaxRow, int kBatch, int kMinBlocks>
+// The register batch's terms: dense x gathers x[c]; a slot-mapped hashed x
+// (kX 2) or a sparse-vector x (kX 3) first gathers the coordinate's slot, then
+// x[slot]; a missing coordinate contributes no term (+0.0, see XOperand<1>).
+template <int kX, int kB>
+SL_DEV void handoff_terms(const XOperand<kX>& xop, const int32_t* c, const double* v, int u0,
+                          int len, double* t) {
+  if constexpr (kX == 0) {
+    double xv[kB];
+#pragma unroll
+    for (int b = 0; b < kB; ++b) xv[b] = u0 + b < len ? ldg(xop.x + c[b]) : 0.0;
+#pragma unroll
+    for (int b = 0; b < kB; ++b) t[b] = dmul(v[b], xv[b]);
+  } else {
+    int64_t sl[kB];
+#pragma unroll
+    for (int b = 0; b < kB; ++b) sl[b] = u0 + b < len ? xop.slot(c[b]) : -1;
+    double xv[kB];
+#pragma unroll
+    for (int b = 0; b < kB; ++b) xv[b] = sl[b] >= 0 ? ldg(xop.xv + sl[b]) : 0.0;
+#pragma unroll
+    for (int b = 0; b < kB; ++b) t[b] = sl[b] >= 0 ? dmul(v[b], xv[b]) : 0.0;
+  }
+}
+
+template <int kCap, int kMaxRow, int kBatch, int kMinBlocks, int kX>
 __global__ void __launch_bounds__(32, kMinBlocks)
 spmv_csr_handoff_kernel(int64_t nrows, const int32_t* __restrict__ pos,
                         const int32_t* __restrict__ crd, const double* __restrict__ vals,
-                        const double* __restrict__ x, double* __restrict__ y) {
+                        XOperand<kX> xop, double* __restrict__ y) {
   static_assert(kCap % 4 == 0 && kMaxRow % kBatch == 0, "shapes");
   extern __shared__ __align__(16) unsigned char smem_raw[];
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw);
@@ -589,15 +613,14 @@ spmv_csr_handoff_kernel(int64_t nrows, const int32_t* __restrict__ pos,
         next_staged = issue_next();
 #pragma unroll
         for (int u0 = 0; u0 < kMaxRow; u0 += kBatch) {
-          double xv[kBatch];
-#pragma unroll
-          for (int b = 0; b < kBatch; ++b) xv[b] = u0 + b < len ? ldg(x + c[u0 + b]) : 0.0;
+          double t[kBatch];
+          handoff_terms<kX, kBatch>(xop, c + u0, v + u0, u0, len, t);
 #pragma unroll
           for (int b = 0; b < kBatch; ++b)
-            if (u0 + b < len) acc = dadd(acc, dmul(v[u0 + b], xv[b]));
+            if (u0 + b < len) acc = dadd(acc, t[b]);
         }
       } else {
-        for (int u = 0; u < len; ++u) acc = dadd(acc, dmul(s_val[off + u], ldg(x + s_crd[off + u])));
+        for (int u = 0; u < len; ++u) acc = dadd(acc, xop.term(s_val[off + u], s_crd[off + u]));
         __syncwarp();
         next_staged = issue_next();
       }
@@ -610,7 +633,7 @@ spmv_csr_handoff_kernel(int64_t nrows, const int32_t* __restrict__ pos,
         double a = 0.0;
         for (int32_t c0 = b; c0 < e; c0 += 32) {
           const int32_t q = c0 + lane;
-          const double t = q < e ? dmul(ld_stream(vals + q), ldg(x + ld_stream(crd + q))) : 0.0;
+          const double t = q < e ? xop.term(ld_stream(vals + q), ld_stream(crd + q)) : 0.0;
           const int n = min(32, e - c0);
           for (int u = 0; u < n; ++u) a = dadd(a, __shfl_sync(0xffffffffu, t, u));
         }
@@ -630,15 +653,15 @@ spmv_csr_handoff_kernel(int64_t nrows, const int32_t* __restrict__ pos,
   }
 }
 
-template <int kCap, int kMaxRow, int kBatch, int kMinBlocks>
+template <int kCap, int kMaxRow, int kBatch, int kMinBlocks, int kX>
 static void launch_csr_handoff(int64_t nrows, const int32_t* pos, const int32_t* crd,
-                               const double* vals, const double* x, double* y, int blocks_per_sm,
+                               const double* vals, XOperand<kX> xop, double* y, int blocks_per_sm,
                                cudaStream_t s) {
   constexpr size_t smem = 16 + (size_t)kCap * 12;
   const int64_t ntiles = (nrows + 31) / 32;
   const int grid = (int)min64(ntiles, (int64_t)sl_host::sm_count() * blocks_per_sm);
-  spmv_csr_handoff_kernel<kCap, kMaxRow, kBatch, kMinBlocks><<<grid, 32, smem, s>>>(
-      nrows, pos, crd, vals, x, y);
+  spmv_csr_handoff_kernel<kCap, kMaxRow, kBatch, kMinBlocks, kX><<<grid, 32, smem, s>>>(
+      nrows, pos, crd, vals, xop, y);
 }
 
 // 896-element stage (28 per row), rows of up to 28 nonzeros in registers,
@@ -942,12 +965,17 @@ static int launch_csr(int64_t nrows, int64_t nnz, const int32_t* pos, const int3
     // (the 27-point stencil) keep 256-row blocks (29.0 vs 35.2 us)
     // (nnz < 0: not known to the entry point — the located-x paths, whose
     // per-nonzero locate latency also favours more, smaller blocks)
-    if (variant == 0 && !kHashX && nnz >= 0 && nnz <= (int64_t)kCsrHandoffMaxRow * nrows &&
-        aligned16(crd) && aligned16(vals)) {
-      launch_csr_handoff<kCsrHandoffCap, kCsrHandoffMaxRow, kCsrHandoffBatch, kCsrHandoffBlocks>(
-          nrows, pos, crd, vals, reinterpret_cast<const XOperand<0>&>(xop).x, y,
-          kCsrHandoffBlocks, s);
-      return sl_host::launch_status();
+    // dense x and sparse-vector x (spx stencil 46.0 -> 35.9 us); the hashed x
+    // paths keep K2a (slot-mapped H1: 45.5 us with K2a, 54.2 us here — the
+    // element-order gathers of K2a's staging serve its two random gathers
+    // per nonzero better than the row walk)
+    if constexpr (kHashX == 0 || kHashX == 3) {
+      if (variant == 0 && nnz >= 0 && nnz <= (int64_t)kCsrHandoffMaxRow * nrows &&
+          aligned16(crd) && aligned16(vals)) {
+        launch_csr_handoff<kCsrHandoffCap, kCsrHandoffMaxRow, kCsrHandoffBatch, kCsrHandoffBlocks>(
+            nrows, pos, crd, vals, xop, y, kCsrHandoffBlocks, s);
+        return sl_host::launch_status();
+      }
     }
     if (nnz <= 16 * nrows) {
       spmv_csr_rowblock_kernel<kHashX, 192><<<ceil_div(nrows, 192), kCsrThreads, 0, s>>>(
@@ -963,7 +991,7 @@ static int launch_csr(int64_t nrows, int64_t nnz, const int32_t* pos, const int3
   } else if (variant == 6 && !kHashX) {
     if (!aligned16(crd) || !aligned16(vals)) return SL_ERR_INVALID;
     launch_csr_handoff<kCsrHandoffCap, kCsrHandoffMaxRow, kCsrHandoffBatch, kCsrHandoffBlocks>(
-        nrows, pos, crd, vals, reinterpret_cast<const XOperand<0>&>(xop).x, y, kCsrHandoffBlocks, s);
+        nrows, pos, crd, vals, reinterpret_cast<const XOperand<0>&>(xop), y, kCsrHandoffBlocks, s);
   } else if (variant == 3 && !kHashX) {
     const double* xd = reinterpret_cast<const XOperand<0>&>(xop).x;
     spmv_csr_warp_kernel<<<ceil_div(nrows, 256), 256, 0, s>>>(nrows, pos, crd, vals, xd, y);
