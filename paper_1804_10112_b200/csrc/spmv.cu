@@ -935,7 +935,9 @@ extern "C" int sl_spmv_coo_f64(int64_t nrows, int64_t ncols, int64_t nnz, const 
   // (measured: 2048-nonzero tiles in one wave 37.0 us, this 26.2 us; 512-tile
   // and 128-thread variants 26.7-42 us; a persistent version prefetching the
   // next tile into registers during the current tile's shared-memory phases
-  // 26.9-34.8 us at 4-8 blocks/SM: profiles/ab/r1_coo_persistent_prefetch.txt)
+  // 26.9-34.8 us at 4-8 blocks/SM: profiles/ab/r1_coo_persistent_prefetch.txt;
+  // a persistent version with a two-stage TMA ring of rows/cols/vals and
+  // in-place products 34.9-36.8 us at 3-5 blocks/SM: r1_coo_tma_ring.txt)
   spmv_coo_kernel<256, 1, 8><<<ceil_div(nnz, 1024), 256, 0, s>>>(nrows, nnz, rows, cols, vals,
                                                                  x, y, vec_ok);
   return sl_host::launch_status();
