@@ -1114,7 +1114,8 @@ extern "C" int sl_spmv_ell_f64(int64_t nrows, int64_t ncols, int32_t nslots, con
     // batch 9 x 256 threads x 4 blocks/SM; batch 7-27 at 64-512 threads per
     // block measured 20.5-24.5 us against 20.8 us here (profiles/ab/r1_ell_configs.txt);
     // issuing the next batch's loads before the current batch's gathers
-    // (register software pipelining) 20.6-24.6 us (profiles/ab/r1_ell_swp.txt)
+    // (register software pipelining) 20.6-24.6 us (profiles/ab/r1_ell_swp.txt);
+    // a grid-stride persistent grid of 2-8 blocks/SM 20.6-25.3 us (r1_ell_persistent.txt)
     spmv_ell_kernel<kEllBatch, 256, 4><<<ceil_div(nrows, 256), 256, 0, s>>>(nrows, nslots, crd, vals, x, y);
   }
   return sl_host::launch_status();
