@@ -668,7 +668,9 @@ static void launch_csr_handoff(int64_t nrows, const int32_t* pos, const int32_t*
 // gathers in two batches of 14, 12 one-warp blocks per SM (146 registers):
 // 64^3 stencil 22.4 us, D1 19.3 us, against K2f 23.8 / K2a 20.5 us; 14-27
 // element batches, 10-24 blocks/SM and a 32-nonzero register row measured
-// 22.4-27.2 / 19.3-24.4 us (profiles/ab/r1_csr_handoff*.txt)
+// 22.4-27.2 / 19.3-24.4 us (profiles/ab/r1_csr_handoff*.txt); two stages per
+// block (tiles t+1 and t+2 in flight, 10 blocks/SM) 25.9-30.7 / 26.7-28.7 us
+// (r1_csr_handoff_2stage.txt)
 constexpr int kCsrHandoffCap = 896;
 constexpr int kCsrHandoffMaxRow = 28;
 constexpr int kCsrHandoffBatch = 14;
