@@ -312,6 +312,17 @@ int sl_mttkrp_csf_f64(int64_t I, int64_t J, int64_t K, int32_t R,
  * row pointer alone (row-sorted COO, unique coordinates) is: */
 int sl_convert_coo_to_csr(int64_t nrows, int64_t nnz, const int32_t* rows, int32_t* pos,
                           void* stream);
+/* COO -> CSR exactly (repeated coordinates summed as (0 + v1) + v2 ..., every
+ * value stored as 0.0 + v; engine.identity_copy, engine.py:775-779) in one
+ * streaming pass when the COO has no repeated coordinate (row pointer, cols
+ * copied, 0.0 + vals), else through the A+B gather-append passes, chosen on
+ * the device (no host round trip).  c_crd / c_vals hold nnz elements;
+ * nnz(C) = c_pos[nrows]. */
+size_t sl_convert_coo_to_csr_exact_workspace_bytes(int64_t nrows, int64_t nnz);
+int sl_convert_coo_to_csr_exact(int64_t nrows, int64_t nnz, const int32_t* rows,
+                                const int32_t* cols, const double* vals, int32_t* c_pos,
+                                int32_t* c_crd, double* c_vals, void* ws, size_t ws_bytes,
+                                void* stream);
 /* CSR -> ELL: nslots = max per-row count of nonzero values (read *out_dev
  * after the stream); entries with value 0.0 are dropped and values stored as
  * 0.0 + v, as the reference's reorder writer + assemble do. */

@@ -74,6 +74,9 @@ SIGNATURES = {
     "sl_mttkrp_csf_f64": ([_i64, _i64, _i64, _i32, _i64, _i64, _i64, _p, _p, _p, _p, _p, _p, _p,
                            _p, _p, _p, _sz, _p], ctypes.c_int),
     "sl_convert_coo_to_csr": ([_i64, _i64, _p, _p, _p], ctypes.c_int),
+    "sl_convert_coo_to_csr_exact_workspace_bytes": ([_i64, _i64], _sz),
+    "sl_convert_coo_to_csr_exact": ([_i64, _i64, _p, _p, _p, _p, _p, _p, _p, _sz, _p],
+                                    ctypes.c_int),
     "sl_csr_max_row_length": ([_i64, _p, _p, _p, _p], ctypes.c_int),
     "sl_convert_csr_to_ell": ([_i64, _i32, _p, _p, _p, _p, _p, _p], ctypes.c_int),
     "sl_convert_coo_to_dia_workspace_bytes": ([_i64, _i64], _sz),

@@ -276,8 +276,10 @@ add_tile_kernel(int64_t nrows, const int32_t* __restrict__ a_pos, const int32_t*
                 const int32_t* __restrict__ b_cols, const double* __restrict__ b_vals,
                 int32_t* __restrict__ c_pos, int32_t* __restrict__ c_crd,
                 double* __restrict__ c_vals, int64_t* __restrict__ tile_tot,
-                int64_t* __restrict__ super_tot, bool staged_ok) {
+                int64_t* __restrict__ super_tot, bool staged_ok,
+                const int32_t* __restrict__ guard = nullptr) {
   constexpr bool kValues = kMode != 0;
+  if (guard != nullptr && ldg(guard) == 0) return;   // nothing to merge (see the exact convert)
   __shared__ int32_t s_apos[kAddRows + 1], s_bpos[kAddRows + 1];
   // unified stages: A's slice at [0, kCS), B's at [kCS, 2 kCS); a value is
   // staged at the same index as its column
@@ -410,6 +412,92 @@ add_tile_kernel(int64_t nrows, const int32_t* __restrict__ a_pos, const int32_t*
       gc[q] = s_ccrd[q];
       gv[q] = s_cval[q];
     }
+  }
+}
+
+// ---- COO -> CSR identity copy (formats.convert), duplicate-free fast path ----
+// The reference's copy into CSR (engine.identity_copy, engine.py:775-779) is
+// the A+B gather-append with an empty A: per row, B's coordinates in order,
+// repeated ones summed, every value stored as 0.0 + v.  Without repeated
+// coordinates that is B's row pointer, cols unchanged and 0.0 + vals, which
+// this single pass writes (16 B read, 12 B written per nonzero); it also
+// flags any repeated coordinate, in which case the guarded A+B passes that
+// follow redo the conversion exactly (they exit at once when the flag is 0).
+constexpr int kCvIpt = 4;
+
+__global__ void __launch_bounds__(256)
+coo_csr_copy_kernel(int64_t nrows, int64_t nnz, const int32_t* __restrict__ rows,
+                    const int32_t* __restrict__ cols, const double* __restrict__ vals,
+                    int32_t* __restrict__ rowptr, int32_t* __restrict__ c_pos,
+                    int32_t* __restrict__ c_crd, double* __restrict__ c_vals,
+                    int32_t* __restrict__ dup_flag, bool vec_ok, int32_t* __restrict__ a_pos,
+                    int64_t* __restrict__ super_tot, int64_t nsuper) {
+  // the guarded fallback's inputs: an all-zero A row pointer, zeroed super-tile totals
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q <= nrows;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    a_pos[q] = 0;
+    if (q < nsuper) super_tot[q] = 0;
+  }
+  const int64_t e0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * kCvIpt;
+  if (e0 > nnz) return;
+  int32_t r[kCvIpt], c[kCvIpt];
+  double v[kCvIpt];
+  const bool vec = vec_ok && e0 + kCvIpt <= nnz;
+  if (vec) {
+    const int4 a = ld_stream(reinterpret_cast<const int4*>(rows + e0));
+    const int4 b = ld_stream(reinterpret_cast<const int4*>(cols + e0));
+    const double2 v0 = ld_stream(reinterpret_cast<const double2*>(vals + e0));
+    const double2 v1 = ld_stream(reinterpret_cast<const double2*>(vals + e0 + 2));
+    r[0] = a.x; r[1] = a.y; r[2] = a.z; r[3] = a.w;
+    c[0] = b.x; c[1] = b.y; c[2] = b.z; c[3] = b.w;
+    v[0] = v0.x; v[1] = v0.y; v[2] = v1.x; v[3] = v1.y;
+  } else {
+#pragma unroll
+    for (int t = 0; t < kCvIpt; ++t) {
+      const bool ok = e0 + t < nnz;
+      r[t] = ok ? ldg(rows + e0 + t) : (int32_t)nrows;
+      c[t] = ok ? ldg(cols + e0 + t) : -1;
+      v[t] = ok ? ldg(vals + e0 + t) : 0.0;
+    }
+  }
+  const int32_t prev_r = e0 == 0 ? -1 : ldg(rows + e0 - 1);
+  const int32_t prev_c = e0 == 0 ? -1 : ldg(cols + e0 - 1);
+  unsigned gaps = 0;
+  bool dup = false;
+#pragma unroll
+  for (int t = 0; t < kCvIpt; ++t) {
+    const int32_t pr = t == 0 ? prev_r : r[t - 1];
+    const int32_t pc = t == 0 ? prev_c : c[t - 1];
+    if (r[t] != pr) {
+      rowptr[r[t]] = (int32_t)(e0 + t);
+      c_pos[r[t]] = (int32_t)(e0 + t);
+    }
+    gaps |= (r[t] - pr > 1 ? 1u : 0u) << t;
+    dup |= e0 + t < nnz && r[t] == pr && c[t] == pc;
+  }
+  if (gaps) {
+#pragma unroll
+    for (int t = 0; t < kCvIpt; ++t)
+      if (gaps >> t & 1u) {
+        const int32_t lo = t == 0 ? prev_r : r[t - 1];
+        for (int32_t q = lo + 1; q < r[t]; ++q) {
+          rowptr[q] = (int32_t)(e0 + t);
+          c_pos[q] = (int32_t)(e0 + t);
+        }
+      }
+  }
+  if (dup) atomicOr(dup_flag, 1);
+  if (vec) {
+    *reinterpret_cast<int4*>(c_crd + e0) = make_int4(c[0], c[1], c[2], c[3]);
+    *reinterpret_cast<double2*>(c_vals + e0) = make_double2(dadd(0.0, v[0]), dadd(0.0, v[1]));
+    *reinterpret_cast<double2*>(c_vals + e0 + 2) = make_double2(dadd(0.0, v[2]), dadd(0.0, v[3]));
+  } else {
+#pragma unroll
+    for (int t = 0; t < kCvIpt; ++t)
+      if (e0 + t < nnz) {
+        c_crd[e0 + t] = c[t];
+        c_vals[e0 + t] = dadd(0.0, v[t]);
+      }
   }
 }
 
@@ -551,5 +639,46 @@ extern "C" int sl_add_csr_f64(int64_t nrows, const int32_t* a_pos, const int32_t
   add_tile_kernel<2><<<(int)add_ntiles(nrows), kAddRows, 0, s>>>(
       nrows, a_pos, a_crd, a_vals, bp, b_cols, b_vals, c_pos, c_crd, c_vals, w.tiles, w.supers,
       add_staged_ok(a_crd, a_vals, b_cols, b_vals));
+  return sl_host::launch_status();
+}
+
+// COO -> CSR exactly as the reference's convert (formats.py:583-587 ->
+// engine.identity_copy): c_crd / c_vals hold nnz elements (the duplicate-free
+// size, an upper bound); nnz(C) = c_pos[nrows].
+extern "C" size_t sl_convert_coo_to_csr_exact_workspace_bytes(int64_t nrows, int64_t nnz) {
+  return sl_add_csr_workspace_bytes(nrows, nnz) + al256((size_t)(nrows + 1) * sizeof(int32_t)) +
+         256;
+}
+
+extern "C" int sl_convert_coo_to_csr_exact(int64_t nrows, int64_t nnz, const int32_t* rows,
+                                           const int32_t* cols, const double* vals,
+                                           int32_t* c_pos, int32_t* c_crd, double* c_vals,
+                                           void* ws, size_t ws_bytes, void* stream) {
+  if (nrows < 0 || nnz < 0) return SL_ERR_INVALID;
+  if (nrows > INT32_MAX || nnz > INT32_MAX) return SL_ERR_RANGE;
+  if (!c_pos || (nnz > 0 && (!rows || !cols || !vals || !c_crd || !c_vals))) return SL_ERR_INVALID;
+  if (!ws || ws_bytes < sl_convert_coo_to_csr_exact_workspace_bytes(nrows, nnz))
+    return SL_ERR_WORKSPACE;
+  cudaStream_t s = as_stream(stream);
+  if (nrows == 0)
+    return cudaMemsetAsync(c_pos, 0, sizeof(int32_t), s) == cudaSuccess ? SL_OK : SL_ERR_CUDA;
+  const AddWs w = add_ws(ws, nrows);
+  char* tail = static_cast<char*>(ws) + sl_add_csr_workspace_bytes(nrows, nnz);
+  int32_t* a_pos = reinterpret_cast<int32_t*>(tail);                 // empty A: all zeros
+  int32_t* flag = reinterpret_cast<int32_t*>(tail + al256((size_t)(nrows + 1) * sizeof(int32_t)));
+  cudaMemsetAsync(flag, 0, sizeof(int32_t), s);
+  const bool vec_ok = sl_host::aligned16(rows) && sl_host::aligned16(cols) &&
+                      sl_host::aligned16(vals) && sl_host::aligned16(c_crd) &&
+                      sl_host::aligned16(c_vals);
+  coo_csr_copy_kernel<<<ceil_div(ceil_div(nnz + 1, kCvIpt), 256), 256, 0, s>>>(
+      nrows, nnz, rows, cols, vals, w.rowptr, c_pos, c_crd, c_vals, flag, vec_ok, a_pos, w.supers,
+      add_nsuper(nrows));
+  // repeated coordinates: the exact gather-append passes (no-ops otherwise)
+  add_tile_kernel<0><<<(int)add_ntiles(nrows), kAddRows, 0, s>>>(
+      nrows, a_pos, nullptr, nullptr, w.rowptr, cols, nullptr, c_pos, nullptr, nullptr, w.tiles,
+      w.supers, true, flag);
+  add_tile_kernel<2><<<(int)add_ntiles(nrows), kAddRows, 0, s>>>(
+      nrows, a_pos, nullptr, nullptr, w.rowptr, cols, vals, c_pos, c_crd, c_vals, w.tiles, w.supers,
+      add_staged_ok(nullptr, nullptr, cols, vals), flag);
   return sl_host::launch_status();
 }

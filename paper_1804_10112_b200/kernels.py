@@ -275,16 +275,36 @@ def add_csr(nrows, a_pos, a_crd, a_vals, b_cols, b_vals, b_rows=None, b_pos=None
 
 # ---- format conversion (formats.convert, formats.py:583-587) -------------------
 
-def coo_to_csr(nrows, rows, cols, vals, sync=True, two_pass=True):
-    """COO-SoA -> CSR exactly as the reference's identity copy: the A+B
-    count -> scan -> fill kernels with an empty A, so duplicates are summed
-    (+0.0 + v1 + v2 ...) and values stored as 0.0 + v (explicit zeros kept)."""
+def coo_to_csr(nrows, rows, cols, vals, sync=True, two_pass=True, path="exact"):
+    """COO-SoA -> CSR exactly as the reference's identity copy: duplicates
+    summed (+0.0 + v1 + v2 ...), values stored as 0.0 + v (explicit zeros
+    kept).  Default: sl_convert_coo_to_csr_exact (one streaming pass when no
+    coordinate repeats, the A+B gather-append passes otherwise, decided on the
+    device).  path="add" routes through the A+B entry points with an empty A
+    (two_pass selecting the two-pass or fused form, as add_csr), for A/B
+    checks."""
     rows = _t(rows, I32, "rows")
-    a_pos = torch.zeros(nrows + 1, dtype=I32, device=rows.device)
-    empty_i = torch.empty(0, dtype=I32, device=rows.device)
-    empty_f = torch.empty(0, dtype=F64, device=rows.device)
-    return add_csr(nrows, a_pos, empty_i, empty_f, cols, vals, b_rows=rows, sync=sync,
-                   two_pass=two_pass)
+    if path == "add":
+        a_pos = torch.zeros(nrows + 1, dtype=I32, device=rows.device)
+        empty_i = torch.empty(0, dtype=I32, device=rows.device)
+        empty_f = torch.empty(0, dtype=F64, device=rows.device)
+        return add_csr(nrows, a_pos, empty_i, empty_f, cols, vals, b_rows=rows, sync=sync,
+                       two_pass=two_pass)
+    cols, vals = _t(cols, I32, "cols"), _t(vals, F64, "vals")
+    nnz = rows.numel()
+    dev = rows.device
+    c_pos = torch.empty(nrows + 1, dtype=I32, device=dev)
+    c_crd = torch.empty(max(nnz, 1), dtype=I32, device=dev)
+    c_vals = torch.empty(max(nnz, 1), dtype=F64, device=dev)
+    ws = _ws(L().sl_convert_coo_to_csr_exact_workspace_bytes(nrows, nnz), vals)
+    _lib.check(L().sl_convert_coo_to_csr_exact(nrows, nnz, P(rows), P(cols), P(vals), P(c_pos),
+                                               P(c_crd), P(c_vals), P(ws),
+                                               0 if ws is None else ws.numel(), S()),
+               "convert_coo_to_csr")
+    if sync:
+        n = int(c_pos[nrows].item())
+        return c_pos, c_crd[:n], c_vals[:n]
+    return c_pos, c_crd, c_vals
 
 
 def csr_rows(nrows, pos, nnz=None):

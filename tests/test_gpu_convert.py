@@ -54,10 +54,37 @@ def test_convert_two_pass_and_fused_agree():
     n = int(c["nrows"])
     args = (n, cuda(c["coo_rows"], np.int32), cuda(c["coo_cols"], np.int32),
             cuda(c["coo_vals"], np.float64))
-    p1, c1, v1 = K.coo_to_csr(*args, two_pass=True)
-    p2, c2, v2 = K.coo_to_csr(*args, two_pass=False)
-    assert torch.equal(p1, p2) and torch.equal(c1, c2)
-    assert np.array_equal(bits(v1), bits(v2))
+    p1, c1, v1 = K.coo_to_csr(*args, path="add", two_pass=True)
+    p2, c2, v2 = K.coo_to_csr(*args, path="add", two_pass=False)
+    p3, c3, v3 = K.coo_to_csr(*args)        # exact path: repeated coordinates -> A+B passes
+    assert torch.equal(p1, p2) and torch.equal(c1, c2) and torch.equal(p1, p3)
+    assert torch.equal(c1, c3)
+    assert np.array_equal(bits(v1), bits(v2)) and np.array_equal(bits(v1), bits(v3))
+
+
+@pytest.mark.parametrize("n,nnz,empty_rows", [(20000, 200000, False), (5000, 7, True),
+                                             (3000, 29999, True)])
+def test_convert_exact_fast_path_unique(orc, n, nnz, empty_rows):
+    # unique coordinates: the single streaming pass (row pointer, cols, 0.0 + v);
+    # signed zeros in the values, empty rows including leading/trailing ones
+    rng = np.random.default_rng(n + nnz)
+    m = 4000
+    key = np.unique(rng.integers(0, n * m, nnz * 2))[:nnz]
+    if empty_rows:
+        key = key[(key // m) % 3 != 0]
+    r, c = (key // m).astype(np.int32), (key % m).astype(np.int32)
+    v = rng.uniform(-1, 1, len(key))
+    v[rng.random(len(key)) < 0.05] = -0.0
+    pos, crd, vals = K.coo_to_csr(n, cuda(r, np.int32), cuda(c, np.int32), cuda(v, np.float64))
+    opos, ocrd, ovals = orc.convert_coo_to_csr(n, r, c, v)
+    assert np.array_equal(host(pos), opos) and np.array_equal(host(crd), ocrd)
+    assert np.array_equal(bits(vals), bits(ovals))
+    # misaligned views take the scalar path of the same pass
+    r2 = cuda(np.concatenate([[0], r]), np.int32)[1:]
+    c2 = cuda(np.concatenate([[0], c]), np.int32)[1:]
+    pos2, crd2, vals2 = K.coo_to_csr(n, r2, c2, cuda(v, np.float64))
+    assert np.array_equal(host(pos2), opos) and np.array_equal(host(crd2), ocrd)
+    assert np.array_equal(bits(vals2), bits(ovals))
 
 
 @pytest.mark.parametrize("seed", [0, 1])
