@@ -130,6 +130,18 @@ int sl_hashed_locate(int64_t nq, const int32_t* parent_pos, const int32_t* coord
 int sl_hashed_insert_init(int64_t size, int32_t* crd, void* stream);
 int sl_hashed_insert(int64_t nq, const int32_t* parent_pos, const int32_t* coord,
                      int64_t w, int32_t* crd, int32_t* err_flag, void* stream);
+/* The same bulk insert with the reference's exact table layout: the result
+ * equals calling insert_coord(parent_pos[q], coord[q]) for q = 0, 1, ... in
+ * order (every coordinate at the first slot from its home free at its turn;
+ * entries already in crd keep their slots; repeated coordinates idempotent).
+ * Priority race: slots hold (q << 32 | coord) updated by atomicMin, so a slot
+ * only passes to earlier queries and displaced ones probe on.  size = the
+ * table length (a multiple of w); workspace from
+ * sl_hashed_insert_ordered_workspace_bytes(nq, size). */
+size_t sl_hashed_insert_ordered_workspace_bytes(int64_t nq, int64_t size);
+int sl_hashed_insert_ordered(int64_t nq, const int32_t* parent_pos, const int32_t* coord,
+                             int64_t w, int64_t size, int32_t* crd, int32_t* err_flag,
+                             void* ws, size_t ws_bytes, void* stream);
 
 /* Slot map of a hash vector: for every coordinate c < n, the answer of
  * locate(c) (first slot in probe order holding c with no empty slot before

@@ -9,6 +9,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
+
 #include "common.cuh"
 #include "levels.cuh"
 
@@ -65,6 +67,150 @@ __global__ void hashed_insert_kernel(int64_t nq, const int32_t* __restrict__ par
   }
   atomicExch(err, SL_ERR_HASH_SEGMENT_FULL);
 }
+
+// ---- ordered bulk insert: the table the sequential insert_coord calls build --
+// insert_coord in query order q = 0, 1, ... (levels.py:312-333) places each new
+// coordinate at the first slot from its home that is empty at that moment;
+// the result depends on the order whenever probe sequences collide.  The
+// bulk insert reproduces it exactly with priorities: a slot holds
+// (order << 32 | coord) and keys race by atomicMin, so a slot can only ever be
+// taken over by a higher-priority (earlier) key; the loser (or the displaced
+// key) continues probing from the next slot.  Every key visits the slots from
+// its home to its final slot, each of which ends up held by an earlier key,
+// so its final slot is the first one from its home not taken by earlier keys
+// — the sequential answer, by induction over the order.  Entries already in
+// the table keep their slots (priority 0), and repeated coordinates are
+// reduced to their first occurrence beforehand (a later copy could otherwise
+// pass the slot the first copy only takes afterwards).
+constexpr unsigned long long kPackEmpty = ~0ull;
+
+SL_DEV unsigned long long dedup_key(int64_t pp, int32_t c) {
+  return ((unsigned long long)pp << 32) | (uint32_t)c;
+}
+SL_DEV uint64_t dedup_home(unsigned long long key, int lg) {
+  return (uint64_t)((key * 0x9E3779B97F4A7C15ull) >> (64 - lg));
+}
+
+__global__ void ordered_seed_kernel(int64_t size, const int32_t* __restrict__ crd,
+                                    unsigned long long* __restrict__ P, int64_t m,
+                                    unsigned long long* __restrict__ dkey,
+                                    uint32_t* __restrict__ dord) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < size; i += stride) {
+    const int32_t v = crd[i];
+    P[i] = v == kEmpty ? kPackEmpty : (unsigned long long)(uint32_t)v;   // order 0
+  }
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += stride) {
+    dkey[i] = kPackEmpty;
+    dord[i] = 0xffffffffu;
+  }
+}
+
+// first occurrence of every (segment, coordinate): min query index per key
+__global__ void ordered_dedup_kernel(int64_t nq, const int32_t* __restrict__ parent_pos,
+                                     const int32_t* __restrict__ coord, int lg,
+                                     unsigned long long* __restrict__ dkey,
+                                     uint32_t* __restrict__ dord) {
+  const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= nq) return;
+  const unsigned long long key = dedup_key(parent_pos ? parent_pos[q] : 0, coord[q]);
+  const uint64_t mask = (1ull << lg) - 1;
+  for (uint64_t h = dedup_home(key, lg);; h = (h + 1) & mask) {
+    const unsigned long long old = atomicCAS(dkey + h, kPackEmpty, key);
+    if (old == kPackEmpty || old == key) {
+      atomicMin(dord + h, (uint32_t)q);
+      return;
+    }
+  }
+}
+
+__global__ void ordered_insert_kernel(int64_t nq, const int32_t* __restrict__ parent_pos,
+                                      const int32_t* __restrict__ coord, int64_t w, int lg,
+                                      const unsigned long long* __restrict__ dkey,
+                                      const uint32_t* __restrict__ dord,
+                                      unsigned long long* __restrict__ P,
+                                      int32_t* __restrict__ err) {
+  const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= nq) return;
+  const int64_t pp = parent_pos ? parent_pos[q] : 0;
+  const int32_t c0 = coord[q];
+  {  // only the first occurrence of a repeated coordinate inserts
+    const unsigned long long key = dedup_key(pp, c0);
+    const uint64_t mask = (1ull << lg) - 1;
+    uint64_t h = dedup_home(key, lg);
+    while (dkey[h] != key) h = (h + 1) & mask;
+    if (dord[h] != (uint32_t)q) return;
+  }
+  unsigned long long* seg = P + pp * w;
+  unsigned long long mine = ((unsigned long long)(q + 1) << 32) | (uint32_t)c0;
+  int64_t s = (int64_t)(c0 % w);
+  int64_t d = 0;                                  // probe distance of the key being placed
+  for (;;) {
+    const unsigned long long old = atomicMin(seg + s, mine);
+    if (old == kPackEmpty) return;                // placed
+    if ((uint32_t)old == (uint32_t)mine) return;  // already present (an earlier entry)
+    if (old > mine) {                             // displaced a later key: it moves on
+      mine = old;
+      const int64_t home = (int64_t)((int32_t)(uint32_t)old % w);
+      d = s >= home ? s - home : s + w - home;
+    }
+    s = s + 1 == w ? 0 : s + 1;
+    if (++d >= w) {                               // probed the whole segment
+      atomicExch(err, SL_ERR_HASH_SEGMENT_FULL);
+      return;
+    }
+  }
+}
+
+__global__ void ordered_unpack_kernel(int64_t size, const unsigned long long* __restrict__ P,
+                                      int32_t* __restrict__ crd) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < size; i += stride)
+    crd[i] = P[i] == kPackEmpty ? kEmpty : (int32_t)(uint32_t)P[i];
+}
+
+static int ordered_lg(int64_t nq) {
+  int lg = 6;
+  while ((1ll << lg) < 2 * nq) ++lg;
+  return lg;
+}
+
+}  // namespace sl
+
+extern "C" size_t sl_hashed_insert_ordered_workspace_bytes(int64_t nq, int64_t size) {
+  const int64_t m = 1ll << sl::ordered_lg(nq);
+  return (size_t)size * 8 + (size_t)m * 12 + 256;
+}
+
+extern "C" int sl_hashed_insert_ordered(int64_t nq, const int32_t* parent_pos,
+                                        const int32_t* coord, int64_t w, int64_t size,
+                                        int32_t* crd, int32_t* err_flag, void* ws,
+                                        size_t ws_bytes, void* stream) {
+  using namespace sl;
+  if (nq < 0 || w <= 0 || size < 0 || size % w != 0) return SL_ERR_INVALID;
+  if (w > INT32_MAX || nq >= INT32_MAX) return SL_ERR_RANGE;
+  if (nq == 0) return SL_OK;
+  if (!coord || !crd || !err_flag) return SL_ERR_INVALID;
+  if (!ws || ws_bytes < sl_hashed_insert_ordered_workspace_bytes(nq, size)) return SL_ERR_WORKSPACE;
+  cudaStream_t s = sl_host::as_stream(stream);
+  const int lg = ordered_lg(nq);
+  const int64_t m = 1ll << lg;
+  char* p = static_cast<char*>(ws);
+  auto* P = reinterpret_cast<unsigned long long*>(p);
+  auto* dkey = reinterpret_cast<unsigned long long*>(p + (size_t)size * 8);
+  auto* dord = reinterpret_cast<uint32_t*>(p + (size_t)size * 8 + (size_t)m * 8);
+  const int grid = (int)std::min<int64_t>(sl_host::ceil_div(std::max(size, m), 256),
+                                          8 * sl_host::sm_count());
+  ordered_seed_kernel<<<grid, 256, 0, s>>>(size, crd, P, m, dkey, dord);
+  ordered_dedup_kernel<<<sl_host::ceil_div(nq, 256), 256, 0, s>>>(nq, parent_pos, coord, lg, dkey,
+                                                                  dord);
+  ordered_insert_kernel<<<sl_host::ceil_div(nq, 256), 256, 0, s>>>(nq, parent_pos, coord, w, lg,
+                                                                   dkey, dord, P, err_flag);
+  ordered_unpack_kernel<<<grid, 256, 0, s>>>(size, P, crd);
+  return sl_host::launch_status();
+}
+
+namespace sl {
 
 // ---- slot map: the answer of locate(c) for every coordinate c < n ------------
 // For a query stream much longer than the table (CSR x hash-vector: one

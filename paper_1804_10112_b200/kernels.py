@@ -222,16 +222,26 @@ def hashed_locate(coords, w, crd, parent=None, group=8):
     return pos, found
 
 
-def hashed_insert(coords, w, nseg=1, parent=None, crd=None):
-    """Bulk hashed insert; returns (crd table, device error flag)."""
+def hashed_insert(coords, w, nseg=1, parent=None, crd=None, ordered=True):
+    """Bulk hashed insert; returns (crd table, device error flag).  ordered:
+    the exact table the sequential insert_coord calls build (default);
+    ordered=False: the concurrent atomicCAS insert (same stored set per
+    segment, layout unspecified where probe sequences collide)."""
     coords = _t(coords, I32, "coords")
     parent = None if parent is None else _t(parent, I32, "parent")
     if crd is None:
         crd = torch.empty(nseg * w, dtype=I32, device=coords.device)
         _lib.check(L().sl_hashed_insert_init(crd.numel(), P(crd), S()), "insert_init")
     err = torch.zeros(1, dtype=I32, device=coords.device)
-    _lib.check(L().sl_hashed_insert(coords.numel(), P(parent), P(coords), w, P(crd), P(err), S()),
-               "hashed_insert")
+    if ordered:
+        ws = _ws(L().sl_hashed_insert_ordered_workspace_bytes(coords.numel(), crd.numel()), crd)
+        _lib.check(L().sl_hashed_insert_ordered(coords.numel(), P(parent), P(coords), w,
+                                                crd.numel(), P(crd), P(err), P(ws),
+                                                0 if ws is None else ws.numel(), S()),
+                   "hashed_insert")
+    else:
+        _lib.check(L().sl_hashed_insert(coords.numel(), P(parent), P(coords), w, P(crd), P(err),
+                                        S()), "hashed_insert")
     return crd, err
 
 

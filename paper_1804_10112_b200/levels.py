@@ -292,8 +292,13 @@ class LevelStorage:
         pp = None if parent_pos is None else torch.as_tensor(
             parent_pos, dtype=torch.int32, device=dev).reshape(-1).contiguous()
         err = torch.zeros(1, dtype=torch.int32, device=dev)
-        _lib.check(_lib.load().sl_hashed_insert(coords.numel(), _lib.ptr(pp), _lib.ptr(coords),
-                                                self.w, _lib.ptr(self.crd), _lib.ptr(err),
+        # the exact table of sequential insert_coord calls in this order
+        lib = _lib.load()
+        nbytes = int(lib.sl_hashed_insert_ordered_workspace_bytes(coords.numel(), self.crd.numel()))
+        ws = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=dev)
+        _lib.check(lib.sl_hashed_insert_ordered(coords.numel(), _lib.ptr(pp), _lib.ptr(coords),
+                                                self.w, self.crd.numel(), _lib.ptr(self.crd),
+                                                _lib.ptr(err), _lib.ptr(ws), ws.numel(),
                                                 _lib.stream_handle()), "insert_coord")
         if int(err.item()) != 0:
             raise HashSegmentFullError(

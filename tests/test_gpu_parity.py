@@ -241,7 +241,7 @@ def test_hashed_insert_set_semantics(orc):
     w, nseg = 64, 50
     parent = rng.integers(0, nseg, 2000).astype(np.int32)
     coords = rng.integers(0, 200, 2000).astype(np.int32)
-    crd, err = K.hashed_insert(cuda(coords), w, nseg=nseg, parent=cuda(parent))
+    crd, err = K.hashed_insert(cuda(coords), w, nseg=nseg, parent=cuda(parent), ordered=False)
     assert int(err.item()) == 0
     table = crd.cpu().numpy()
     ref, st = orc.hashed_insert(coords, w, nseg=nseg, parent=parent)
@@ -257,6 +257,37 @@ def test_hashed_insert_set_semantics(orc):
     # overflow
     crd, err = K.hashed_insert(cuda(np.array([0, 2, 4], np.int32)), 2)
     assert int(err.item()) == 4
+
+
+@pytest.mark.parametrize("w,nseg,n,crange,seed", [
+    (64, 50, 2000, 200, 5),          # multi-segment, many repeats
+    (4096, 1, 3000, 1 << 20, 6),     # one segment, scattered homes
+    (1024, 1, 1000, 1024, 7),        # load ~0.63, heavy primary clustering
+    (97, 3, 282, 10_000, 8),         # odd width, wrap-around probing, 94 per segment
+    (131072, 1, 100_000, 200_000, 9)])  # H1's table (ascending-insert clusters)
+def test_hashed_insert_ordered_exact_layout(orc, w, nseg, n, crange, seed):
+    # the bulk insert builds exactly the table of sequential insert_coord calls
+    rng = np.random.default_rng(seed)
+    parent = rng.permutation(np.repeat(np.arange(nseg), -(-n // nseg))[:n]).astype(np.int32)
+    coords = rng.integers(0, crange, n).astype(np.int32)
+    if seed == 9:
+        coords = np.sort(rng.choice(crange, n, replace=False)).astype(np.int32)
+    half = n // 2
+    # two calls: the second inserts into a table that already has entries
+    crd, err = K.hashed_insert(cuda(coords[:half]), w, nseg=nseg, parent=cuda(parent[:half]))
+    crd, err2 = K.hashed_insert(cuda(coords[half:]), w, nseg=nseg, parent=cuda(parent[half:]),
+                                crd=crd)
+    ref, st = orc.hashed_insert(coords, w, nseg=nseg, parent=parent)
+    assert st == 0 and int(err.item()) == 0 and int(err2.item()) == 0
+    assert np.array_equal(crd.cpu().numpy(), ref)
+
+
+def test_hashed_insert_ordered_overflow():
+    crd, err = K.hashed_insert(cuda(np.array([5, 7, 5, 9], np.int32)), 2)
+    assert int(err.item()) == 4            # SL_ERR_HASH_SEGMENT_FULL: 3 distinct into width 2
+    crd, err = K.hashed_insert(cuda(np.array([5, 7, 5, 7], np.int32)), 2)
+    assert int(err.item()) == 0            # repeats are idempotent: exactly full
+    assert sorted(crd.cpu().numpy().tolist()) == [5, 7]
 
 
 def test_spmv_hashx_full_h1(orc):
