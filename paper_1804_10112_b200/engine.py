@@ -25,7 +25,8 @@ import numpy as np
 import torch
 
 from . import kernels as K
-from .errors import UnsupportedMergeError, UnsupportedOutputError, ValidationError
+from .errors import (HashSegmentFullError, UnsupportedMergeError, UnsupportedOutputError,
+                     ValidationError)
 from .formats import TensorFormat, TensorStorage, preset
 from .levels import LevelKind as LK
 from .levels import LevelStorage
@@ -120,9 +121,9 @@ def plan(checked: CheckedExpr, bindings, out_format: TensorFormat,
             A, x = mat[0], vec[0]
             i, j = A.ivars
             if lhs.ivars == (i,) and x.ivars == (j,) and i != j:
-                if ocls != "dense1":
+                if ocls not in ("dense1", "hash1"):
                     raise UnsupportedOutputError(
-                        f"SpMV output must be a dense vector, got {out_format.describe()}")
+                        f"SpMV output must be a dense or hash vector, got {out_format.describe()}")
                 ca, cx = cls[A.tensor], cls[x.tensor]
                 if cx == "dense1" and ca in ("coo", "csr", "ell", "dia"):
                     return Plan("spmv", f"spmv_{ca}", {"A": A.tensor, "x": x.tensor},
@@ -256,6 +257,36 @@ def _dia_host_offsets(st: TensorStorage):
     return offs
 
 
+def _hashed_spmv_output(p: Plan, A: TensorStorage, y, nrows: int, dev) -> TensorStorage:
+    """SpMV into a hash-vector output, as the reference's scatter writer builds
+    it (engine.py:281-327): the row coordinates are inserted in the order
+    they are first written — every row for CSR / ELL / DIA (the row total is
+    written after the row's loop, empty rows included), the rows present in
+    the coordinates for COO (one write per nonzero) — and each slot holds the
+    row's sum, which is the dense kernel's y[i] (the same additions from
+    +0.0).  Width: the format's pinned width, else next_pow2(max(4, 2 n))."""
+    f = p.out_format
+    w = f.hash_width or _next_pow2(max(4, 2 * nrows))
+    if p.kernel == "spmv_coo":
+        rows = torch.unique_consecutive(A.levels[0].crd)        # sorted: first-write order
+    else:
+        rows = torch.arange(nrows, dtype=torch.int32, device=dev)
+    crd, err = K.hashed_insert(rows, w)
+    if int(err.item()) != 0:
+        raise HashSegmentFullError(f"hashed segment of width {w} is full")
+    slots, _ = K.hashed_locate(rows, w, crd)
+    vals = torch.zeros(w, dtype=torch.float64, device=dev)
+    vals[slots.long()] = y[rows.long()]
+    return TensorStorage(f, (nrows,), [LevelStorage(f.levels[0], w=w, crd=crd, device=dev)], vals)
+
+
+def _next_pow2(v: int) -> int:
+    n = 1
+    while n < v:
+        n <<= 1
+    return n
+
+
 def _run(p: Plan, inputs: Dict[str, TensorStorage], stats: Optional[EvalStats]):
     dev = None
     for st in inputs.values():
@@ -297,8 +328,11 @@ def _run(p: Plan, inputs: Dict[str, TensorStorage], stats: Optional[EvalStats]):
             y = K.spmv_csr_hashx(nrows, A.levels[1].pos, A.levels[1].crd, A.vals, hx.w, hx.crd,
                                  x.vals, n=n_map)
             visits = {"i": nrows, "j": int(A.levels[1].crd.numel())}
-        out = TensorStorage(p.out_format, (nrows,),
-                            [LevelStorage(p.out_format.levels[0], n=nrows, device=dev)], y)
+        if format_class(p.out_format) == "hash1":
+            out = _hashed_spmv_output(p, A, y, nrows, dev)
+        else:
+            out = TensorStorage(p.out_format, (nrows,),
+                                [LevelStorage(p.out_format.levels[0], n=nrows, device=dev)], y)
     elif p.pattern == "add":
         A, B = ops["A"], ops["B"]
         nrows = A.dims[0]

@@ -693,20 +693,85 @@ def check_generator_layouts():
     return {"layouts_checked": np.int32(1)}
 
 
+def hashout_case(name, nrows, ncols, rows, cols, vals, x, width):
+    """SpMV into a hash-vector y (the scatter writer's insert protocol,
+    engine.py:281-327) for COO / CSR / ELL / DIA operands."""
+    out = {"nrows": nrows, "ncols": ncols, "x": f64(x), "width": width}
+    data = coordlist((nrows, ncols), zip(rows, cols), vals)
+    yfmt = sl.preset("hash-vector", width=width)
+    for fmt in ("coo-soa", "csr", "ell", "dia"):
+        st = sl.assemble(sl.preset(fmt), (nrows, ncols), data)
+        key = fmt.split("-")[0]
+        if fmt == "coo-soa":
+            out["coo_rows"] = i32(st.levels[0].crd)
+            out["coo_cols"] = i32(st.levels[1].crd)
+            out["coo_vals"] = f64(st.vals[:len(st.levels[1].crd)] if st.levels[1].crd else [])
+        elif fmt == "csr":
+            out["csr_pos"] = i32(st.levels[1].pos)
+            out["csr_crd"] = i32(st.levels[1].crd)
+            out["csr_vals"] = f64(st.vals[:len(st.levels[1].crd)] if st.levels[1].crd else [])
+        elif fmt == "ell":
+            out["ell_nslots"] = st.levels[0].n
+            out["ell_crd"] = i32(st.levels[2].crd)
+            out["ell_vals"] = f64(st.vals[:st.levels[0].n * nrows] if st.levels[0].n else [])
+        else:
+            out["dia_offsets"] = i32(st.levels[1].offset)
+            nd = len(st.levels[1].offset)
+            out["dia_vals"] = f64(st.vals[:nd * nrows] if nd else [])
+        try:
+            y = sl.evaluate("y(i) = A(i,j) * x(j)", {"A": st, "x": dense_vec(x)}, yfmt)
+        except sl.HashSegmentFullError:
+            out[f"{key}_full"] = 1                      # more rows written than slots
+            continue
+        out[f"{key}_ycrd"] = i32(y.levels[0].crd)
+        out[f"{key}_yw"] = y.levels[0].w
+        out[f"{key}_yvals"] = f64(y.vals)
+    return name, out
+
+
+def hashout_cases():
+    rng = np.random.default_rng(61)
+    cases = []
+    # small: empty rows, an explicit zero, default width (next_pow2(2n))
+    cases.append(hashout_case("ho_small", 8, 6, [0, 0, 2, 2, 5, 6], [1, 3, 0, 2, 4, 1],
+                              [2.0, -1.0, 0.5, 4.0, 1.5, 0.0], [1.0, 2, 3, 4, 5, 6], 0))
+    # COO rows spread over 300 with 60 present: homes r % 64 collide (ordered insert)
+    present = np.sort(rng.choice(300, 60, replace=False))
+    rows = np.repeat(present, rng.integers(1, 4, 60))
+    cols = np.concatenate([np.sort(rng.choice(40, k, replace=False)) for k in
+                           np.bincount(np.searchsorted(present, rows), minlength=60)])
+    vals = rng.uniform(-1, 1, len(rows))
+    cases.append(hashout_case("ho_coo_collide", 300, 40, rows, cols, vals,
+                              rng.uniform(-1, 1, 40), 64))
+    # banded 50 x 50, pinned width 53 (odd; all rows inserted, no wrap)
+    n = 50
+    r = np.repeat(np.arange(n), 3)
+    c = np.clip(r + np.tile([-2, 0, 3], n), 0, n - 1)
+    key = np.unique(r * n + c)
+    cases.append(hashout_case("ho_band_w53", n, n, key // n, key % n, rng.uniform(-1, 1, len(key)),
+                              rng.uniform(-1, 1, n), 53))
+    return cases
+
+
 def main():
     out_dir = HERE
     layouts = check_generator_layouts()
     groups = {
-        "spmv": spmv_cases() + [coo_duplicates_case(), dia_case(4, 21), dia_case(5, 22)],
-        "add": add_cases(),
-        "mttkrp": mttkrp_cases(),
-        "convert": convert_cases(),
-        "widen": widen_cases(),
-        "assembly": assembly_cases(),
-        "io": io_cases(),
-        "addx": addx_cases(),
+        "spmv": lambda: spmv_cases() + [coo_duplicates_case(), dia_case(4, 21), dia_case(5, 22)],
+        "add": add_cases,
+        "mttkrp": mttkrp_cases,
+        "convert": convert_cases,
+        "widen": widen_cases,
+        "assembly": assembly_cases,
+        "io": io_cases,
+        "addx": addx_cases,
+        "hashout": hashout_cases,
     }
-    for group, cases in groups.items():
+    only = set(sys.argv[1:])
+    for group, make in groups.items():
+        if only and group not in only:
+            continue
+        cases = make()
         flat = {}
         names = []
         for name, arrays in cases:
@@ -716,6 +781,8 @@ def main():
         flat["_cases"] = np.array(names)
         np.savez_compressed(out_dir / f"{group}.npz", **flat)
         print(group, len(names), "cases")
+    if only and "levels" not in only:
+        return
     kats = level_kats()
     kats.update(layouts)
     np.savez_compressed(out_dir / "levels.npz", **kats)

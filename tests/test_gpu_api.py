@@ -189,3 +189,33 @@ def test_evaluate_add_and_mttkrp(golden, orc):
         out = slb.evaluate("A(i,r) = X(i,j,k) * B(j,r) * C(k,r)", {"X": X, "B": Bs, "C": Cs})
         ok, err = orc.within_condition(out.vals.cpu().numpy().reshape(I, R), t["A_coo"], absA)
         assert ok, err
+
+
+# ---------------------------------------------------------------------------
+# SpMV into a hash-vector output (the scatter writer's insert protocol)
+
+def test_evaluate_spmv_hashed_output_goldens():
+    import paper_1804_10112_b200 as slb
+    from paper_1804_10112_b200 import formats as F
+    from paper_1804_10112_b200.errors import HashSegmentFullError
+    from conftest import load_cases
+
+    for name, c in load_cases("hashout").items():
+        n, m, w = int(c["nrows"]), int(c["ncols"]), int(c["width"])
+        x = F.dense_storage(np.asarray(c["x"], np.float64))
+        mats = {"coo": F.coo_storage(c["coo_rows"], c["coo_cols"], c["coo_vals"], (n, m)),
+                "csr": F.csr_storage(c["csr_pos"], c["csr_crd"], c["csr_vals"], (n, m)),
+                "ell": F.ell_storage(int(c["ell_nslots"]), c["ell_crd"], c["ell_vals"], (n, m)),
+                "dia": F.dia_storage(c["dia_offsets"], c["dia_vals"], (n, m))}
+        yfmt = F.preset("hash-vector", width=w)
+        for key, A in mats.items():
+            if f"{key}_full" in c:
+                with pytest.raises(HashSegmentFullError):
+                    slb.evaluate("y(i) = A(i,j) * x(j)", {"A": A, "x": x}, yfmt)
+                continue
+            y = slb.evaluate("y(i) = A(i,j) * x(j)", {"A": A, "x": x}, yfmt)
+            assert y.levels[0].w == int(c[f"{key}_yw"]), (name, key)
+            assert np.array_equal(y.levels[0].crd.cpu().numpy(), c[f"{key}_ycrd"]), (name, key)
+            got = y.vals.cpu().numpy().view(np.int64)
+            assert np.array_equal(got, np.asarray(c[f"{key}_yvals"], np.float64).view(np.int64)), \
+                (name, key)
