@@ -228,9 +228,13 @@ constexpr int kMapChunk = 1024;
 // none) and the chunk's last empty slot
 __global__ void __launch_bounds__(kMapChunk)
 hash_runs_kernel(int64_t w, const int32_t* __restrict__ crd, int32_t* __restrict__ last_empty,
-                 int32_t* __restrict__ chunk_last) {
+                 int32_t* __restrict__ chunk_last, unsigned long long* __restrict__ map,
+                 int64_t n) {
   __shared__ int32_t s_warp[kMapChunk / 32];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // the map starts absent (~0) — done here rather than in a launch of its own
+  for (int64_t i = (int64_t)blockIdx.x * kMapChunk + tid; i < n; i += (int64_t)gridDim.x * kMapChunk)
+    map[i] = ~0ull;
   const int64_t s = (int64_t)blockIdx.x * kMapChunk + tid;
   int32_t v = (s < w && ldg(crd + s) == kEmpty) ? (int32_t)s : -1;
 #pragma unroll
@@ -278,11 +282,6 @@ hash_chunk_scan_kernel(int64_t nchunks, const int32_t* __restrict__ chunk_last,
   if (tid == 0) chunk_pre[nchunks] = s_carry;
 }
 
-__global__ void map_init_kernel(unsigned long long* __restrict__ map, int64_t n) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x)
-    map[i] = ~0ull;
-}
 
 __global__ void map_fill_kernel(int64_t w, int64_t n, const int32_t* __restrict__ crd,
                                 const int32_t* __restrict__ last_empty,
@@ -332,8 +331,7 @@ extern "C" int sl_hashed_slot_map(int64_t n, int64_t w, const int32_t* crd, void
   int32_t* chunk_last = last_empty + w;
   int32_t* chunk_pre = chunk_last + nchunks;
   const int sms = sl_host::sm_count();
-  if (n > 0) map_init_kernel<<<min(sl_host::ceil_div(n, 256), 8 * sms), 256, 0, s>>>(map, n);
-  hash_runs_kernel<<<(int)nchunks, kMapChunk, 0, s>>>(w, crd, last_empty, chunk_last);
+  hash_runs_kernel<<<(int)nchunks, kMapChunk, 0, s>>>(w, crd, last_empty, chunk_last, map, n);
   hash_chunk_scan_kernel<<<1, 1024, 0, s>>>(nchunks, chunk_last, chunk_pre);
   map_fill_kernel<<<min(sl_host::ceil_div(w, 256), 8 * sms), 256, 0, s>>>(
       w, n, crd, last_empty, chunk_pre, map, nchunks);
