@@ -256,18 +256,8 @@ struct CooSrc {
 };
 
 // CSF: the batch's fibers and slices come from 32-wide windows of pos2/crd1
-// and pos1/crd0; each lane finds its nonzero's fiber (slice) by a 5-step
-// shuffle binary search over the window of fiber (slice) ends.
-SL_DEV int window_count_le(int32_t w, int32_t key) {
-  // number of window entries <= key (entries sorted across lanes; <= 31)
-  int d = 0;
-#pragma unroll
-  for (int step = 16; step >= 1; step >>= 1) {
-    const int32_t v = __shfl_sync(0xffffffffu, w, d + step - 1);
-    if (v <= key) d += step;
-  }
-  return d;
-}
+// and pos1/crd0; each lane finds its nonzero's fiber (slice) by counting the
+// window's fiber (slice) ends at or before it (warp OR + popcount).
 
 struct CsfSrc {
   const int32_t* crd0;
@@ -304,18 +294,27 @@ struct CsfSrc {
   }
   SL_DEV void next(int64_t base, int lane, int32_t& li, int32_t& lj, int32_t& lk, double& lv) {
     const int32_t fe = wfe, jw = wjw, se = wse, iw = wiw;
-    const int32_t e = (int32_t)(base + lane);
-    const int df = window_count_le(fe, e);
+    // fiber of element base + lane: the number of window fibers ending at or
+    // before it.  Fiber ends inside the batch are distinct positions 1..31,
+    // so one warp OR of (1 << position) and a popcount of the bits up to the
+    // lane give every lane's count (a 5-step shuffle search per lane before:
+    // CSF ran 20% more instructions than COO-3)
+    const unsigned le_mask = 0xffffffffu >> (31 - lane);
+    const int32_t pf = fe - (int32_t)base;
+    const unsigned fbits = __reduce_or_sync(0xffffffffu, pf >= 0 && pf < 32 ? 1u << pf : 0u);
+    const int df = __popc(fbits & le_mask);
     lj = __shfl_sync(0xffffffffu, jw, df);
     const int32_t fib = (int32_t)(f + df);
     // slices average 2000 nonzeros: a batch usually lies in one slice (the
-    // first slice ends after the batch's last fiber) and skips the search
+    // first slice ends after the batch's last fiber) and skips the count
     const int32_t se0 = __shfl_sync(0xffffffffu, se, 0);
     const int32_t fib_last = __shfl_sync(0xffffffffu, fib, 31);
     if (se0 > fib_last) {
       li = __shfl_sync(0xffffffffu, iw, 0);
     } else {
-      const int ds = window_count_le(se, fib);
+      const int32_t ps = se - (int32_t)f;      // slice ends as fiber offsets 1..31
+      const unsigned sbits = __reduce_or_sync(0xffffffffu, ps >= 0 && ps < 32 ? 1u << ps : 0u);
+      const int ds = __popc(sbits & (0xffffffffu >> (31 - df)));
       li = __shfl_sync(0xffffffffu, iw, ds);
     }
     lk = nk;
