@@ -575,6 +575,26 @@ def run_formats(torch, K, wl, dev, timer, peak, steps):
                                      "peak_source": "profiles/l2_calib.json gather256_GBs "
                                                     "(tools/calib_l2.py, 256-B random rows)",
                                      "frac": round(l2b / t / 1e6 / l2_peak, 4) if l2_peak else None}}
+
+    # the paper's other kernels on the same tensor: TTV into a
+    # CSR-over-fibers output (a per-fibre SpMV + the fibre row pointer) and
+    # INNERPROD of the COO-3 tensor with itself (intersection at every level)
+    vt = T(np.random.default_rng(3).uniform(-1.0, 1.0, Kd))
+    zi, zj, zk, zv = ti.clone(), tj.clone(), tk.clone(), tv.clone()
+    tt = timer.run({"ttv": lambda: K.ttv_csf(I, J, Kd, c0, p1, c1, p2, c2, tv, vt, out="csr"),
+                    "inner": lambda: K.inner_coo3(I, J, Kd, (ti, tj, tk, tv), (zi, zj, zk, zv))},
+                   max(3, steps // 3), 2)
+    t = float(np.mean(tt["ttv"]))
+    b_ttv = (4 * (len(csf["crd0"]) + 1) + 4 * len(csf["crd0"]) + 4 * (n1 + 1) + 12 * nnz + 8 * Kd
+             + 4 * (I + 1) + 12 * n1)
+    res["ttv_csf_csr_out_D5"] = {"ms": round(t, 4), "GB/s": round(b_ttv / t / 1e6, 1),
+                                 "frac": round(b_ttv / t / 1e6 / peak, 4), "bytes": b_ttv,
+                                 "nnz/s": round(nnz / t * 1e3, 1), "fibers": n1}
+    t = float(np.mean(tt["inner"]))
+    b_in = 2 * 20 * nnz
+    res["innerprod_coo3_D5"] = {"ms": round(t, 4), "GB/s": round(b_in / t / 1e6, 1),
+                                "frac": round(b_in / t / 1e6 / peak, 4), "bytes": b_in,
+                                "nnz/s": round(nnz / t * 1e3, 1)}
     return res
 
 

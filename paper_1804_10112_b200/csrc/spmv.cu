@@ -577,6 +577,7 @@ spmv_csr_handoff_kernel(int64_t nrows, const int32_t* __restrict__ pos,
   if (staged && lane == 0) issue(a0, ee);
   uint32_t phase = 0;
   for (;;) {
+    ee = __shfl_sync(0xffffffffu, pe, nr - 1);   // this tile's element range [eb, ee)
     // next tile's bounds: in flight during this tile's wait and copy
     const int64_t next = tile + gridDim.x;
     const int64_t nr0 = next * 32;
@@ -595,50 +596,58 @@ spmv_csr_handoff_kernel(int64_t nrows, const int32_t* __restrict__ pos,
       return ns;
     };
     double acc = 0.0;
-    bool next_staged;
+    bool next_staged = false;
     const int len = pe - pb;
+    bool reg = false;
     if (staged) {
       mbar_wait(bar, phase);
       phase ^= 1u;
+      reg = __all_sync(0xffffffffu, len <= kMaxRow);
+    }
+    if (reg) {
       const int off = pb - a0;
-      if (__all_sync(0xffffffffu, len <= kMaxRow)) {
-        int32_t c[kMaxRow];
-        double v[kMaxRow];
+      int32_t c[kMaxRow];
+      double v[kMaxRow];
 #pragma unroll
-        for (int u = 0; u < kMaxRow; ++u) {
-          c[u] = u < len ? s_crd[off + u] : 0;
-          v[u] = u < len ? s_val[off + u] : 0.0;
-        }
-        __syncwarp();                     // every lane's row is in registers
-        next_staged = issue_next();
+      for (int u = 0; u < kMaxRow; ++u) {
+        c[u] = u < len ? s_crd[off + u] : 0;
+        v[u] = u < len ? s_val[off + u] : 0.0;
+      }
+      __syncwarp();                     // every lane's row is in registers
+      next_staged = issue_next();
 #pragma unroll
-        for (int u0 = 0; u0 < kMaxRow; u0 += kBatch) {
-          double t[kBatch];
-          handoff_terms<kX, kBatch>(xop, c + u0, v + u0, u0, len, t);
+      for (int u0 = 0; u0 < kMaxRow; u0 += kBatch) {
+        double t[kBatch];
+        handoff_terms<kX, kBatch>(xop, c + u0, v + u0, u0, len, t);
 #pragma unroll
-          for (int b = 0; b < kBatch; ++b)
-            if (u0 + b < len) acc = dadd(acc, t[b]);
-        }
-      } else {
-        for (int u = 0; u < len; ++u) acc = dadd(acc, xop.term(s_val[off + u], s_crd[off + u]));
-        __syncwarp();
-        next_staged = issue_next();
+        for (int b = 0; b < kBatch; ++b)
+          if (u0 + b < len) acc = dadd(acc, t[b]);
       }
     } else {
-      // tile beyond the stage capacity (long rows): the warp takes its rows one
-      // at a time, 32 products in parallel, added in order via shuffles (K2b)
-      next_staged = issue_next();
-      for (int rr = 0; rr < nr; ++rr) {
-        const int32_t b = __shfl_sync(0xffffffffu, pb, rr), e = __shfl_sync(0xffffffffu, pe, rr);
-        double a = 0.0;
-        for (int32_t c0 = b; c0 < e; c0 += 32) {
-          const int32_t q = c0 + lane;
-          const double t = q < e ? xop.term(ld_stream(vals + q), ld_stream(crd + q)) : 0.0;
-          const int n = min(32, e - c0);
-          for (int u = 0; u < n; ++u) a = dadd(a, __shfl_sync(0xffffffffu, t, u));
+      // a row longer than kMaxRow, or a tile beyond the stage: rounds of kCap
+      // elements through the stage (round 0 already staged if the tile fits),
+      // products formed in place by the whole warp, then every lane adds its
+      // row's part of the round in order (K2a's split of the work: a long row
+      // costs one add per element, not a gather chain per element)
+      const int nch = ee > eb ? (ee - a0 + kCap - 1) / kCap : 0;
+      for (int k = 0; k < nch; ++k) {
+        const int32_t c0 = a0 + k * kCap, c1 = min(c0 + kCap, ee);
+        if (k > 0 || !staged) {
+          if (lane == 0) {
+            fence_proxy_async_smem();
+            issue(c0, c1);
+          }
+          mbar_wait(bar, phase);
+          phase ^= 1u;
         }
-        if (lane == rr) acc = a;
+        for (int q = max(eb, c0) - c0 + lane; q < c1 - c0; q += 32)
+          s_val[q] = xop.term(s_val[q], s_crd[q]);
+        __syncwarp();
+        const int lo = max(pb, c0) - c0, hi = min(pe, c1) - c0;
+        for (int u = lo; u < hi; ++u) acc = dadd(acc, s_val[u]);
+        __syncwarp();
       }
+      next_staged = issue_next();
     }
     if (lane < nr) y[r0 + lane] = acc;
     if (nnr == 0) break;

@@ -137,6 +137,27 @@ def test_spmv_csr_handoff_paths(orc):
         assert np.array_equal(bits(y), bits(ref)), variant
 
 
+def test_spmv_csr_skewed_rows_many_tiles_per_block(orc):
+    # power-law row lengths over enough rows that every persistent hand-off
+    # block walks many tiles (grid = 12 blocks/SM): tiles of short rows, tiles
+    # with a long row inside the stage, tiles far beyond it, empty tiles
+    rng = np.random.default_rng(21)
+    n, m = 200_000, 30_000
+    lens = np.minimum(rng.zipf(1.6, n) - 1, 3000).astype(np.int64)
+    lens[rng.random(n) < 0.01] = 0
+    lens[150_000:150_064] = 0
+    cols = np.concatenate([np.sort(rng.choice(m, k, replace=False)) for k in lens]).astype(np.int32)
+    pos = np.zeros(n + 1, np.int32)
+    pos[1:] = np.cumsum(lens)
+    vals = rng.uniform(-1, 1, len(cols))
+    x = rng.uniform(-1, 1, m)
+    ref, _ = orc.spmv_csr(n, pos, cols, vals, x)
+    for variant in (0, 2, 5, 6):
+        y = cuda(np.full(n, np.nan))
+        K.spmv_csr(n, m, cuda(pos), cuda(cols), cuda(vals), cuda(x), y=y, variant=variant)
+        assert np.array_equal(bits(y), bits(ref)), variant
+
+
 def test_spmv_csr_misaligned_operands(orc):
     # crd/vals views starting one element in: the automatic choice falls back
     # to the row-block kernel; the row-stage kernel refuses (it bulk-copies
