@@ -280,6 +280,24 @@ def _hashed_spmv_output(p: Plan, A: TensorStorage, y, nrows: int, dev) -> Tensor
     return TensorStorage(f, (nrows,), [LevelStorage(f.levels[0], w=w, crd=crd, device=dev)], vals)
 
 
+_SKEW_ROW = 4 * 896   # rows longer than four hand-off stages: merge-path
+
+
+def _csr_variant(lv: LevelStorage) -> int:
+    """CSR SpMV variant for this matrix: the automatic choice (register
+    hand-off for short rows, row-block otherwise), or the merge-path split when
+    some row is far longer than a stage — power-law rows otherwise serialise
+    one warp per heavy tile (D5's fibres: 2.6 ms vs 0.23 ms).  The longest row
+    is measured once per row-pointer array and cached on the level."""
+    cached = lv._sl_max_row
+    if cached is None or cached[0] is not lv.pos:
+        pos = lv.pos
+        mr = int((pos[1:] - pos[:-1]).max().item()) if pos.numel() > 1 else 0
+        cached = (pos, mr)
+        lv._sl_max_row = cached
+    return 2 if cached[1] > _SKEW_ROW else 0
+
+
 def _next_pow2(v: int) -> int:
     n = 1
     while n < v:
@@ -304,7 +322,8 @@ def _run(p: Plan, inputs: Dict[str, TensorStorage], stats: Optional[EvalStats]):
             y = K.spmv_coo(nrows, ncols, A.levels[0].crd, A.levels[1].crd, A.vals, x.vals)
             visits = {"i": int(A.vals.numel())}
         elif p.kernel == "spmv_csr":
-            y = K.spmv_csr(nrows, ncols, A.levels[1].pos, A.levels[1].crd, A.vals, x.vals)
+            y = K.spmv_csr(nrows, ncols, A.levels[1].pos, A.levels[1].crd, A.vals, x.vals,
+                           variant=_csr_variant(A.levels[1]))
             visits = {"i": nrows, "j": int(A.levels[1].crd.numel())}
         elif p.kernel == "spmv_ell":
             S = A.levels[0].n

@@ -166,12 +166,13 @@ class LevelStorage:
     """
 
     __slots__ = ("spec", "n", "m", "w", "pos", "crd", "offset", "crd_stride", "crd_base",
-                 "range_n", "_appended", "_edges", "_last_edge_parent")
+                 "range_n", "_appended", "_edges", "_last_edge_parent", "_sl_max_row")
 
     def __init__(self, spec: LevelSpec, *, n: int = 0, m: int = 0, w: int = 0, pos=None, crd=None,
                  offset=None, crd_stride: int = 1, crd_base: int = 0, range_n: int = 0,
                  device="cuda"):
         self.spec = spec
+        self._sl_max_row = None   # (pos, longest row): engine's CSR variant choice, cached
         self.n, self.m, self.w = int(n), int(m), int(w)
         self.pos = _as_i32(pos, device)
         self.crd = _as_i32(crd, device)

@@ -219,3 +219,25 @@ def test_evaluate_spmv_hashed_output_goldens():
             got = y.vals.cpu().numpy().view(np.int64)
             assert np.array_equal(got, np.asarray(c[f"{key}_yvals"], np.float64).view(np.int64)), \
                 (name, key)
+
+
+def test_evaluate_csr_skewed_rows_takes_merge_path(orc):
+    # one row far longer than the hand-off stages: evaluate picks the
+    # merge-path split (cached per row pointer); results stay bit-exact
+    from paper_1804_10112_b200 import engine as E
+    rng = np.random.default_rng(4)
+    n, m = 5000, 20000
+    lens = rng.integers(0, 6, n)
+    lens[7] = 10000
+    cols = np.concatenate([np.sort(rng.choice(m, k, replace=False)) for k in lens]).astype(np.int32)
+    pos = np.zeros(n + 1, np.int32)
+    pos[1:] = np.cumsum(lens)
+    vals = rng.uniform(-1, 1, len(cols))
+    xv = rng.uniform(-1, 1, m)
+    A = F.csr_storage(pos, cols, vals, (n, m))
+    y = slb.evaluate("y(i) = A(i,j) * x(j)", {"A": A, "x": F.dense_storage(xv)})
+    ref, _ = orc.spmv_csr(n, pos, cols, vals, xv)
+    assert np.array_equal(y.vals.cpu().numpy().view(np.int64), ref.view(np.int64))
+    assert E._csr_variant(A.levels[1]) == 2
+    A2 = F.csr_storage(pos[:8], cols[:pos[7]], vals[:pos[7]], (7, m))
+    assert E._csr_variant(A2.levels[1]) == 0
