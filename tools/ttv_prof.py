@@ -25,3 +25,17 @@ for var in (0, 1, 2, 4, 5, 6):
     e1.record()
     torch.cuda.synchronize()
     print(f"variant {var}: {e0.elapsed_time(e1) / 3 * 1e3:9.1f} us  bit-exact vs K2a {ok}", flush=True)
+
+# the same fibres as a row-sorted COO (rows = fibre index): the COO kernel's
+# cross-tile row continuation on power-law rows
+rows = T(np.repeat(np.arange(nf, dtype=np.int32), np.diff(csf['pos2'])))
+yc = K.spmv_coo(nf, t['K'], rows, c2, tv, v)
+torch.cuda.synchronize()
+okc = torch.equal(yc.view(torch.int64), y0.view(torch.int64))
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+e0.record()
+for _ in range(3):
+    K.spmv_coo(nf, t['K'], rows, c2, tv, v, yc)
+e1.record()
+torch.cuda.synchronize()
+print(f"COO on the fibres: {e0.elapsed_time(e1) / 3 * 1e3:9.1f} us  bit-exact vs K2a {okc}", flush=True)
