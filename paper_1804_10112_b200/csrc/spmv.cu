@@ -57,9 +57,6 @@ spmv_coo_kernel(int64_t nrows, int64_t nnz, const int32_t* __restrict__ rows,
   __shared__ uint16_t s_start[kCooTile];          // row-start items (< kCooTile + kCooHalo)
   __shared__ int32_t s_wcnt[kCooThreads / 32];
   __shared__ unsigned s_mask[kCooThreads / 32][kCooTile / kCooThreads];
-  // a row that runs past the staged halo is finished by the whole block
-  __shared__ int s_cend;
-  __shared__ double s_cacc;
 
   const int tid = threadIdx.x;
   const int64_t e0 = (int64_t)blockIdx.x * kCooTile;
@@ -154,6 +151,8 @@ spmv_coo_kernel(int64_t nrows, int64_t nnz, const int32_t* __restrict__ rows,
 
   // ---- thread per row, lockstep: rows summed in storage order from +0.0
   bool cont = false;   // this thread owns the last row and it runs past the halo
+  int32_t cont_r = 0;
+  double cont_acc = 0.0;
   for (int si = tid; si < nstart; si += kCooThreads) {
     const int q = s_start[si];
     const int32_t r = s_row[4 + q];
@@ -170,9 +169,10 @@ spmv_coo_kernel(int64_t nrows, int64_t nnz, const int32_t* __restrict__ rows,
       for (; u < n_st && s_row[4 + u] == r; ++u) acc = dadd(acc, s_prod[u]);
       g = e0 + u;
       if (u == n_st && g < nnz) {
-        // the row goes on past the halo: the block finishes it (below)
+        // the row goes on past the halo: the owner's warp finishes it (below)
         cont = true;
-        s_cacc = acc;
+        cont_r = r;
+        cont_acc = acc;
         for (int32_t q2 = rp + 1; q2 < r; ++q2) y[q2] = 0.0;
         continue;
       }
@@ -182,30 +182,27 @@ spmv_coo_kernel(int64_t nrows, int64_t nnz, const int32_t* __restrict__ rows,
     if (g == nnz)                                                   // the matrix's last row
       for (int64_t q2 = (int64_t)r + 1; q2 < nrows; ++q2) y[q2] = 0.0;
   }
-  if (!__syncthreads_or(cont)) return;
-  // continuation of a long row: the block forms 256 products per round from
-  // global memory (coalesced), thread 0 adds them in order (a power-law row
-  // no longer costs one dependent global walk per element: 2.7 -> 0.58 ms for
-  // the D5 fibres as COO)
-  const int32_t r = s_row[4 + n_st - 1];
+  // continuation of a long row by the owner's warp (no block barrier on the
+  // common path): 32 coalesced products per round, added in order through
+  // shuffles (a power-law row no longer costs one dependent global walk per
+  // element: D5's fibres as COO 2.67 -> 0.86 ms; a block-wide version, 0.58
+  // ms, put a barrier on every tile and cost D1 0.4-0.8 us)
+  const unsigned wm = __ballot_sync(0xffffffffu, cont);
+  if (!wm) return;
+  const int src = __ffs(wm) - 1;
+  const int32_t r = __shfl_sync(0xffffffffu, cont_r, src);
   int64_t g = e0 + n_st;
-  double acc = s_cacc;
+  double acc = __shfl_sync(0xffffffffu, cont_acc, src);
   for (;;) {
-    if (tid == 0) s_cend = kCooThreads;
-    __syncthreads();
-    const int64_t e = g + tid;
+    const int64_t e = g + lane;
     const bool in = e < nnz && ldg(rows + e) == r;
-    s_prod[tid] = in ? dmul(ldg(vals + e), ldg(x + ldg(cols + e))) : 0.0;
-    if (!in) atomicMin(&s_cend, tid);              // rows are sorted: the first miss ends it
-    __syncthreads();
-    const int cnt = s_cend;
-    if (tid == 0)
-      for (int u = 0; u < cnt; ++u) acc = dadd(acc, s_prod[u]);
+    const double pr = in ? dmul(ldg(vals + e), ldg(x + ldg(cols + e))) : 0.0;
+    const int cnt = __popc(__ballot_sync(0xffffffffu, in));   // rows sorted: a prefix
+    for (int u = 0; u < cnt; ++u) acc = dadd(acc, __shfl_sync(0xffffffffu, pr, u));
     g += cnt;
-    __syncthreads();
-    if (cnt < kCooThreads) break;
+    if (cnt < 32) break;
   }
-  if (tid == 0) {
+  if (lane == src) {
     y[r] = acc;
     if (g == nnz)                                                   // the matrix's last row
       for (int64_t q2 = (int64_t)r + 1; q2 < nrows; ++q2) y[q2] = 0.0;
