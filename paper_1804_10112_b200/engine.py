@@ -280,22 +280,29 @@ def _hashed_spmv_output(p: Plan, A: TensorStorage, y, nrows: int, dev) -> Tensor
     return TensorStorage(f, (nrows,), [LevelStorage(f.levels[0], w=w, crd=crd, device=dev)], vals)
 
 
-_SKEW_ROW = 4 * 896   # rows longer than four hand-off stages: merge-path
+_SKEW_TILE = 4 * 896   # 32-row tiles heavier than four hand-off stages: merge-path
 
 
 def _csr_variant(lv: LevelStorage) -> int:
     """CSR SpMV variant for this matrix: the automatic choice (register
     hand-off for short rows, row-block otherwise), or the merge-path split when
-    some row is far longer than a stage — power-law rows otherwise serialise
-    one warp per heavy tile (D5's fibres: 2.6 ms vs 0.23 ms).  The longest row
-    is measured once per row-pointer array and cached on the level."""
+    some 32-row tile holds more than four hand-off stages of nonzeros —
+    power-law rows otherwise serialise one persistent warp per heavy tile
+    (D5's fibres: 2.6 ms vs 0.23 ms).  The heaviest tile is measured once per
+    row-pointer array and cached on the level."""
     cached = lv._sl_max_row
     if cached is None or cached[0] is not lv.pos:
         pos = lv.pos
-        mr = int((pos[1:] - pos[:-1]).max().item()) if pos.numel() > 1 else 0
-        cached = (pos, mr)
+        n = pos.numel() - 1
+        if n > 0:
+            idx = torch.arange(0, n + 32, 32, device=pos.device).clamp_(max=n)
+            tb = pos[idx].to(torch.int64)
+            heaviest = int((tb[1:] - tb[:-1]).max().item())
+        else:
+            heaviest = 0
+        cached = (pos, heaviest)
         lv._sl_max_row = cached
-    return 2 if cached[1] > _SKEW_ROW else 0
+    return 2 if cached[1] > _SKEW_TILE else 0
 
 
 def _next_pow2(v: int) -> int:

@@ -172,7 +172,7 @@ class LevelStorage:
                  offset=None, crd_stride: int = 1, crd_base: int = 0, range_n: int = 0,
                  device="cuda"):
         self.spec = spec
-        self._sl_max_row = None   # (pos, longest row): engine's CSR variant choice, cached
+        self._sl_max_row = None   # (pos, heaviest 32-row tile): engine's CSR variant choice, cached
         self.n, self.m, self.w = int(n), int(m), int(w)
         self.pos = _as_i32(pos, device)
         self.crd = _as_i32(crd, device)

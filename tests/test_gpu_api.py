@@ -222,8 +222,9 @@ def test_evaluate_spmv_hashed_output_goldens():
 
 
 def test_evaluate_csr_skewed_rows_takes_merge_path(orc):
-    # one row far longer than the hand-off stages: evaluate picks the
-    # merge-path split (cached per row pointer); results stay bit-exact
+    # one row far longer than the hand-off stages (a tile far heavier than
+    # four stages): evaluate picks the merge-path split (cached per row
+    # pointer); results stay bit-exact
     from paper_1804_10112_b200 import engine as E
     rng = np.random.default_rng(4)
     n, m = 5000, 20000
