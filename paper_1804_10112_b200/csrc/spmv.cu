@@ -1061,7 +1061,7 @@ extern "C" int sl_spmv_csr_f64(int64_t nrows, int64_t ncols, int64_t nnz, const 
   if (nrows < 0 || ncols < 0 || nnz < 0) return SL_ERR_INVALID;
   if (nrows > INT32_MAX || ncols > INT32_MAX || nnz > INT32_MAX) return SL_ERR_RANGE;
   if (nrows == 0) return SL_OK;
-  if (!pos || !y || !x) return SL_ERR_INVALID;
+  if (!pos || !y || (nnz > 0 && (!x || !crd || !vals))) return SL_ERR_INVALID;   // x may be empty
   cudaStream_t s = as_stream(stream);
   XOperand<0> xop{x};
   if (variant == 2) {

@@ -588,3 +588,52 @@ def test_mttkrp_heavy_rows_span_many_chunks(orc, monkeypatch):
         for A in (A1, A2):
             ok, err = orc.within_condition(A, ref, absA, RTOL)
             assert ok, err
+
+
+# ---------------------------------------------------------------------------
+# degenerate shapes: no rows, no columns, no slots / diagonals, all-empty rows
+
+def test_spmv_degenerate_shapes(orc):
+    e_i, e_f = cuda(np.zeros(0, np.int32)), cuda(np.zeros(0))
+    # zero rows: nothing to write, no error
+    y = K.spmv_coo(0, 5, e_i, e_i, e_f, cuda(np.ones(5)))
+    assert y.numel() == 0
+    for variant in (0, 1, 2, 3, 4, 5, 6):
+        y = K.spmv_csr(0, 5, cuda(np.zeros(1, np.int32)), e_i, e_f, cuda(np.ones(5)),
+                       variant=variant)
+        assert y.numel() == 0
+    # zero columns: every row empty -> +0.0 everywhere
+    n = 1000
+    x0 = cuda(np.zeros(0))
+    for variant in (0, 1, 2, 3, 4, 5, 6):
+        y = cuda(np.full(n, np.nan))
+        K.spmv_csr(n, 0, cuda(np.zeros(n + 1, np.int32)), e_i, e_f, x0, y=y, variant=variant)
+        assert np.array_equal(bits(y), bits(np.zeros(n))), variant
+    y = cuda(np.full(n, np.nan))
+    K.spmv_coo(n, 0, e_i, e_i, e_f, x0, y)
+    assert np.array_equal(bits(y), bits(np.zeros(n)))
+    # ELL with zero slots, DIA with zero diagonals
+    y = cuda(np.full(n, np.nan))
+    K.spmv_ell(n, 7, 0, e_i, e_f, cuda(np.ones(7)), y)
+    assert np.array_equal(bits(y), bits(np.zeros(n)))
+    y = cuda(np.full(n, np.nan))
+    K.spmv_dia(n, 7, np.zeros(0, np.int32), e_f, cuda(np.ones(7)), y)
+    assert np.array_equal(bits(y), bits(np.zeros(n)))
+    # DIA whose diagonals are all out of range for some rows (tall matrix)
+    offs = np.array([5, 9], np.int32)
+    vals = np.random.default_rng(1).uniform(-1, 1, 2 * n)
+    xx = np.random.default_rng(2).uniform(-1, 1, 12)
+    ref, _ = orc.spmv_dia(n, 12, offs, vals, xx)
+    y = cuda(np.full(n, np.nan))
+    K.spmv_dia(n, 12, offs, cuda(vals), cuda(xx), y)
+    assert np.array_equal(bits(y), bits(ref))
+    # COO whose only nonzeros sit in the last row (every earlier row zeroed
+    # by the owner of the last row's start)
+    rows = np.full(3, n - 1, np.int32)
+    cols = np.array([0, 3, 6], np.int32)
+    v = np.array([1.5, -2.0, 0.25])
+    xs = np.random.default_rng(3).uniform(-1, 1, 7)
+    ref, _ = orc.spmv_coo(n, rows, cols, v, xs)
+    y = cuda(np.full(n, np.nan))
+    K.spmv_coo(n, 7, cuda(rows), cuda(cols), cuda(v), cuda(xs), y)
+    assert np.array_equal(bits(y), bits(ref))
