@@ -637,3 +637,28 @@ def test_spmv_degenerate_shapes(orc):
     y = cuda(np.full(n, np.nan))
     K.spmv_coo(n, 7, cuda(rows), cuda(cols), cuda(v), cuda(xs), y)
     assert np.array_equal(bits(y), bits(ref))
+
+
+def test_mttkrp_degenerate_and_small_rank(orc):
+    # no nonzeros: A is all +0.0; ranks 1 and 3 (scalar path); slices with no
+    # nonzeros at both ends of I
+    for R in (1, 3, 32):
+        I, J, Kd = 50, 20, 10
+        z = cuda(np.zeros(0, np.int32))
+        A = K.mttkrp_coo3(I, J, Kd, z, z, z, cuda(np.zeros(0)), cuda(np.ones((J, R))),
+                          cuda(np.ones((Kd, R))))
+        assert np.array_equal(bits(A), bits(np.zeros((I, R)))), R
+        rng = np.random.default_rng(R)
+        nnz = 500
+        key = np.unique(rng.integers(5 * J * Kd, 40 * J * Kd, nnz))     # slices 5..39 only
+        i = (key // (J * Kd)).astype(np.int32)
+        j = ((key // Kd) % J).astype(np.int32)
+        k = (key % Kd).astype(np.int32)
+        v = 1.0 - rng.random(len(key))
+        Bm, Cm = rng.uniform(-1, 1, (J, R)), rng.uniform(-1, 1, (Kd, R))
+        ref, absA = orc.mttkrp_coo3(I, i, j, k, v, Bm, Cm)
+        A = K.mttkrp_coo3(I, J, Kd, cuda(i), cuda(j), cuda(k), cuda(v), cuda(Bm), cuda(Cm))
+        ok, err = orc.within_condition(A.cpu().numpy(), ref, absA, RTOL)
+        assert ok, (R, err)
+        assert np.array_equal(bits(A.cpu().numpy()[:5]), bits(np.zeros((5, R))))
+        assert np.array_equal(bits(A.cpu().numpy()[40:]), bits(np.zeros((10, R))))
