@@ -343,6 +343,62 @@ add_tile_kernel(int64_t nrows, const int32_t* __restrict__ a_pos, const int32_t*
     __syncthreads();
     mbar_wait(&bar, 0);
   }
+  // ---- tiles beyond the stage (denser or power-law rows): consecutive row
+  // groups whose A and B slices fit are staged and merged one after another
+  // (a group of one oversized row merges from global memory)
+  __shared__ int s_g1;
+  uint32_t gphase = 0;
+  auto oversized = [&](int r) {            // one row alone beyond the stage
+    return s_apos[r + 1] - s_apos[r] > kAddCap || s_bpos[r + 1] - s_bpos[r] > kAddCap;
+  };
+  auto group_end = [&](int g0) {           // block-uniform: last row bound that still fits
+    if (tid == 0) {
+      int lo = g0 + 1, hi = nr;
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (s_apos[mid] - s_apos[g0] <= kAddCap && s_bpos[mid] - s_bpos[g0] <= kAddCap) lo = mid;
+        else hi = mid - 1;
+      }
+      s_g1 = lo;
+    }
+    __syncthreads();
+    return s_g1;
+  };
+  // stage the slices of rows [g0, g1); returns the stage index offsets of A and B
+  auto stage_group = [&](int g0, int g1, int32_t& oa, int32_t& ob) {
+    const int32_t alo = s_apos[g0], ahi = s_apos[g1], blo = s_bpos[g0], bhi = s_bpos[g1];
+    const BulkRange<int32_t> ga = plan_range(a_crd, alo, ahi), gb = plan_range(b_cols, blo, bhi);
+    BulkRange<double> gav{}, gbv{};
+    if (kValues) {
+      gav = plan_range(a_vals, alo, ahi);
+      gbv = plan_range(b_vals, blo, bhi);
+    }
+    double* sav = s_val + (int32_t)(gav.lo0 - ga.lo0);
+    double* sbv = kValues ? s_val + kCS + (int32_t)(gbv.lo0 - gb.lo0) : s_val;
+    if (tid == 0) {
+      fence_proxy_async_smem();          // the previous group's reads precede these writes
+      mbar_arrive_expect_tx(&bar, ga.tx_bytes + gb.tx_bytes + gav.tx_bytes + gbv.tx_bytes);
+      issue_range(a_crd, ga, s_col, &bar);
+      issue_range(b_cols, gb, s_col + kCS, &bar);
+      if (kValues) {
+        issue_range(a_vals, gav, sav, &bar);
+        issue_range(b_vals, gbv, sbv, &bar);
+      }
+    }
+    edge_loads_small(a_crd, ga, alo, ahi, s_col, tid);
+    edge_loads_small(b_cols, gb, blo, bhi, s_col + kCS, tid);
+    if (kValues) {
+      edge_loads_small(a_vals, gav, alo, ahi, sav, tid);
+      edge_loads_small(b_vals, gbv, blo, bhi, sbv, tid);
+    }
+    __syncthreads();
+    mbar_wait(&bar, gphase);
+    gphase ^= 1u;
+    oa = (int32_t)ga.lo0;
+    ob = (int32_t)gb.lo0;
+  };
+  const bool grouped = !fits && staged_ok;   // block-uniform
+
   const bool mine = tid < nr;
   // this row's slices as stage indices
   const int ia = mine ? s_apos[tid] - (int32_t)ra.lo0 : 0;
@@ -353,7 +409,28 @@ add_tile_kernel(int64_t nrows, const int32_t* __restrict__ a_pos, const int32_t*
   // ---- per-row counts (count mode) / row bases (fill modes)
   if (kMode == 0) {
     int cnt = 0;
-    if (mine) {
+    if (grouped) {
+      for (int g0 = 0; g0 < nr;) {
+        if (oversized(g0)) {               // merged by its own thread below, in parallel
+          ++g0;
+          continue;
+        }
+        const int g1 = group_end(g0);
+        int32_t oa, ob;
+        stage_group(g0, g1, oa, ob);
+        const int row = g0 + tid;
+        if (row < g1)
+          s_rbase[row] = count_row_idx(s_apos[row] - oa, s_apos[row + 1] - oa,
+                                       kCS + s_bpos[row] - ob, kCS + s_bpos[row + 1] - ob, s_col);
+        __syncthreads();                   // counts written, stage free
+        g0 = g1;
+      }
+      if (mine && oversized(tid))
+        s_rbase[tid] = merge_row<false>(s_apos[tid], s_apos[tid + 1], s_bpos[tid], s_bpos[tid + 1],
+                                        gacc, NoEmit{});
+      __syncthreads();
+      cnt = mine ? s_rbase[tid] : 0;
+    } else if (mine) {
       if (fits) {
         cnt = count_row_idx(ia, iah, ib, ibh, s_col);
       } else {
@@ -393,6 +470,39 @@ add_tile_kernel(int64_t nrows, const int32_t* __restrict__ a_pos, const int32_t*
     if (r0 + tid == 0) c_pos[0] = 0;
   }
   __syncthreads();
+  if (grouped) {
+    for (int g0 = 0; g0 < nr;) {
+      if (oversized(g0)) {                 // merged by its own thread below, in parallel
+        ++g0;
+        continue;
+      }
+      const int g1 = group_end(g0);
+      const int32_t ob0 = s_rbase[g0];                       // group's first output (tile-local)
+      const int32_t ob1 = g1 < nr ? s_rbase[g1] : (int32_t)n_out;
+      {
+        int32_t oa, ob;
+        stage_group(g0, g1, oa, ob);
+        const int row = g0 + tid;
+        if (row < g1)
+          fill_row_idx(s_apos[row] - oa, s_apos[row + 1] - oa, kCS + s_bpos[row] - ob,
+                       kCS + s_bpos[row + 1] - ob, s_col, s_val, s_ccrd + (s_rbase[row] - ob0),
+                       s_cval + (s_rbase[row] - ob0));
+        __syncthreads();
+        int32_t* gc = c_crd + tile_out + ob0;              // the group's outputs, coalesced
+        double* gv = c_vals + tile_out + ob0;
+        for (int q = tid; q < ob1 - ob0; q += kAddRows) {
+          gc[q] = s_ccrd[q];
+          gv[q] = s_cval[q];
+        }
+      }
+      __syncthreads();                     // stages free for the next group
+      g0 = g1;
+    }
+    if (mine && oversized(tid))
+      merge_row<true>(s_apos[tid], s_apos[tid + 1], s_bpos[tid], s_bpos[tid + 1], gacc,
+                      FillEmit{c_crd + tile_out + s_rbase[tid], c_vals + tile_out + s_rbase[tid]});
+    return;
+  }
   const bool staged_out = n_out <= 2 * kAddCap;
   int32_t* oc = staged_out ? s_ccrd : c_crd + tile_out;
   double* ov = staged_out ? s_cval : c_vals + tile_out;

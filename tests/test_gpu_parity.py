@@ -662,3 +662,36 @@ def test_mttkrp_degenerate_and_small_rank(orc):
         assert ok, (R, err)
         assert np.array_equal(bits(A.cpu().numpy()[:5]), bits(np.zeros((5, R))))
         assert np.array_equal(bits(A.cpu().numpy()[40:]), bits(np.zeros((10, R))))
+
+
+@pytest.mark.parametrize("lam,zipf,seed", [(28.0, None, 1), (None, 1.7, 2)])
+def test_add_dense_and_power_law_rows(orc, lam, zipf, seed):
+    # tiles far beyond the 768-element stage: the grouped path (consecutive
+    # row groups that fit) and single oversized rows (global merge)
+    rng = np.random.default_rng(seed)
+    n, m = 20_000, 40_000
+
+    def rows_of(lens):
+        cols = [np.sort(rng.choice(m, int(k), replace=False)) for k in lens]
+        pos = np.zeros(n + 1, np.int64)
+        pos[1:] = np.cumsum(lens)
+        return pos.astype(np.int32), np.concatenate(cols).astype(np.int32)
+
+    if zipf:
+        la = np.minimum(rng.zipf(zipf, n) - 1, 3000)
+        lb = np.minimum(rng.zipf(zipf, n) - 1, 3000)
+    else:
+        la, lb = rng.poisson(lam, n), rng.poisson(lam, n)
+    a_pos, a_crd = rows_of(la)
+    b_pos, b_cols = rows_of(lb)
+    # make ~10% of B's coordinates coincide with A's (matches)
+    b_rows = np.repeat(np.arange(n, dtype=np.int32), lb)
+    a_vals = rng.uniform(-1, 1, len(a_crd))
+    b_vals = rng.uniform(-1, 1, len(b_cols))
+    rp, rc, rv = orc.add_csr(n, a_pos, a_crd, a_vals, b_cols, b_vals, b_rows=b_rows)
+    for two_pass in (False, True):
+        pos, crd, vals = K.add_csr(n, cuda(a_pos), cuda(a_crd), cuda(a_vals), cuda(b_cols),
+                                   cuda(b_vals), b_rows=cuda(b_rows), two_pass=two_pass)
+        assert np.array_equal(pos.cpu().numpy(), rp), two_pass
+        assert np.array_equal(crd.cpu().numpy(), rc), two_pass
+        assert np.array_equal(bits(vals), bits(rv)), two_pass
