@@ -197,6 +197,15 @@ SL_DEV int fill_row_idx(int ia, int iah, int ib, int ibh, const int32_t* s_col,
   return n + 1;
 }
 
+// first index in [lo, hi) of a sorted global int32 range whose value is >= c
+SL_DEV int32_t lower_bound_g(const int32_t* __restrict__ a, int32_t lo, int32_t hi, int32_t c) {
+  while (lo < hi) {
+    const int32_t mid = (lo + hi) >> 1;
+    if (ldg(a + mid) < c) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
 struct NoEmit {
   SL_DEV void operator()(int, int32_t, double) const {}
 };
@@ -425,10 +434,29 @@ add_tile_kernel(int64_t nrows, const int32_t* __restrict__ a_pos, const int32_t*
         __syncthreads();                   // counts written, stage free
         g0 = g1;
       }
-      if (mine && oversized(tid))
-        s_rbase[tid] = merge_row<false>(s_apos[tid], s_apos[tid + 1], s_bpos[tid], s_bpos[tid + 1],
-                                        gacc, NoEmit{});
-      __syncthreads();
+      // rows alone beyond the stage: the block counts each one element-parallel
+      // (a B entry adds a coordinate unless it repeats its predecessor or is
+      // found in A's row by binary search)
+      const bool any_big = __syncthreads_or(mine && oversized(tid));
+      for (int r = 0; any_big && r < nr; ++r) {
+        if (!oversized(r)) continue;
+        const int32_t a0 = s_apos[r], a1 = s_apos[r + 1], b0 = s_bpos[r], b1 = s_bpos[r + 1];
+        if (tid == 0) s_g1 = 0;
+        __syncthreads();
+        int fresh = 0;
+        for (int32_t j = b0 + tid; j < b1; j += kAddRows) {
+          const int32_t c = ldg(b_cols + j);
+          const bool dup = j > b0 && ldg(b_cols + j - 1) == c;
+          if (!dup) {
+            const int32_t p = lower_bound_g(a_crd, a0, a1, c);
+            fresh += !(p < a1 && ldg(a_crd + p) == c);
+          }
+        }
+        if (fresh) atomicAdd(&s_g1, fresh);
+        __syncthreads();
+        if (tid == 0) s_rbase[r] = (a1 - a0) + s_g1;
+        __syncthreads();
+      }
       cnt = mine ? s_rbase[tid] : 0;
     } else if (mine) {
       if (fits) {
@@ -498,9 +526,62 @@ add_tile_kernel(int64_t nrows, const int32_t* __restrict__ a_pos, const int32_t*
       __syncthreads();                     // stages free for the next group
       g0 = g1;
     }
-    if (mine && oversized(tid))
-      merge_row<true>(s_apos[tid], s_apos[tid + 1], s_bpos[tid], s_bpos[tid + 1], gacc,
-                      FillEmit{c_crd + tile_out + s_rbase[tid], c_vals + tile_out + s_rbase[tid]});
+    // rows alone beyond the stage: element-parallel by the block when B's row
+    // has no repeated coordinate (a match is emitted once, by A's entry, as
+    // 0 + (a + b)), else merged by one thread from global memory
+    const bool any_big = __syncthreads_or(mine && oversized(tid));
+    for (int r = 0; any_big && r < nr; ++r) {
+      if (!oversized(r)) continue;
+      const int32_t a0 = s_apos[r], a1 = s_apos[r + 1], b0 = s_bpos[r], b1 = s_bpos[r + 1];
+      int32_t* oc = c_crd + tile_out + s_rbase[r];
+      double* ov = c_vals + tile_out + s_rbase[r];
+      bool dup = false;
+      for (int32_t j = b0 + 1 + tid; j < b1; j += kAddRows)
+        dup |= ldg(b_cols + j) == ldg(b_cols + j - 1);
+      if (__syncthreads_or(dup)) {
+        if (tid == 0)
+          merge_row<true>(a0, a1, b0, b1, gacc, FillEmit{oc, ov});
+        continue;
+      }
+      // slot of an entry = (its rank in its row) + (the other row's entries
+      // below it) - (matched pairs below it); the matched pairs below an entry
+      // are the matched entries before it in its own row: a running block scan
+      int carry = 0;
+      for (int32_t i0 = a0; i0 < a1; i0 += kAddRows) {
+        const int32_t i = i0 + tid;
+        const bool in = i < a1;
+        const int32_t c = in ? ldg(a_crd + i) : 0;
+        const int32_t lb = in ? lower_bound_g(b_cols, b0, b1, c) : b0;
+        const bool m = in && lb < b1 && ldg(b_cols + lb) == c;
+        int tot;
+        const int before = carry + block_incl_scan(m ? 1 : 0, s_warp, &tot) - (m ? 1 : 0);
+        if (in) {
+          const int32_t q = (i - a0) + (lb - b0) - before;
+          const double a = ldg(a_vals + i);
+          oc[q] = c;
+          ov[q] = dadd(0.0, m ? dadd(a, ldg(b_vals + lb)) : a);
+        }
+        carry += tot;
+        __syncthreads();                   // s_warp reused by the next round's scan
+      }
+      carry = 0;
+      for (int32_t j0 = b0; j0 < b1; j0 += kAddRows) {
+        const int32_t j = j0 + tid;
+        const bool in = j < b1;
+        const int32_t c = in ? ldg(b_cols + j) : 0;
+        const int32_t la = in ? lower_bound_g(a_crd, a0, a1, c) : a0;
+        const bool m = in && la < a1 && ldg(a_crd + la) == c;
+        int tot;
+        const int before = carry + block_incl_scan(m ? 1 : 0, s_warp, &tot) - (m ? 1 : 0);
+        if (in && !m) {                    // a matched entry was emitted with A's
+          const int32_t q = (la - a0) + (j - b0) - before;
+          oc[q] = c;
+          ov[q] = dadd(0.0, ldg(b_vals + j));
+        }
+        carry += tot;
+        __syncthreads();
+      }
+    }
     return;
   }
   const bool staged_out = n_out <= 2 * kAddCap;
