@@ -391,10 +391,27 @@ def _mttkrp_ws(nnz, R, like, ws):
     return _ws(need, like)
 
 
+_MT_MAX_R = 128   # ranks per launch (sl_mttkrp_*: SL_ERR_RANGE above)
+
+
+def _mttkrp_rank_blocks(fn, I, B, C, A):
+    """A(i, r) depends on column r of B and C alone, so ranks beyond one
+    launch's limit are computed in column blocks (identical results)."""
+    R = B.shape[-1]
+    A = torch.empty((I, R), dtype=F64, device=B.device) if A is None else A
+    for r0 in range(0, R, _MT_MAX_R):
+        r1 = min(R, r0 + _MT_MAX_R)
+        A[:, r0:r1] = fn(B[:, r0:r1].contiguous(), C[:, r0:r1].contiguous())
+    return A
+
+
 def mttkrp_coo3(I, J, K, i, j, k, vals, B, C, A=None, ws=None):
     i, j, k = _t(i, I32, "i"), _t(j, I32, "j"), _t(k, I32, "k")
     vals, B, C = _t(vals, F64, "vals"), _t(B, F64, "B"), _t(C, F64, "C")
     R = B.shape[-1]
+    if R > _MT_MAX_R:
+        return _mttkrp_rank_blocks(lambda b, c: mttkrp_coo3(I, J, K, i, j, k, vals, b, c),
+                                   I, B, C, A)
     A = _out(A, I * R, F64, vals, "A").view(I, R) if A is None else _t(A, F64, "A")
     ws = _mttkrp_ws(i.numel(), R, vals, ws)
     _lib.check(L().sl_mttkrp_coo3_f64(I, J, K, R, i.numel(), P(i), P(j), P(k), P(vals), P(B),
@@ -408,6 +425,9 @@ def mttkrp_csf(I, J, K, crd0, pos1, crd1, pos2, crd2, vals, B, C, A=None, ws=Non
     pos2, crd2 = _t(pos2, I32, "pos2"), _t(crd2, I32, "crd2")
     vals, B, C = _t(vals, F64, "vals"), _t(B, F64, "B"), _t(C, F64, "C")
     R = B.shape[-1]
+    if R > _MT_MAX_R:
+        return _mttkrp_rank_blocks(
+            lambda b, c: mttkrp_csf(I, J, K, crd0, pos1, crd1, pos2, crd2, vals, b, c), I, B, C, A)
     A = _out(A, I * R, F64, vals, "A").view(I, R) if A is None else _t(A, F64, "A")
     ws = _mttkrp_ws(vals.numel(), R, vals, ws)
     _lib.check(L().sl_mttkrp_csf_f64(I, J, K, R, crd0.numel(), crd1.numel(), vals.numel(),

@@ -466,7 +466,7 @@ def test_mttkrp_goldens(golden, orc):
 @pytest.mark.parametrize("I,J,Kd,nnz,R,seed", [
     (2000, 1500, 1000, 400_000, 32, 1), (300, 200, 100, 50_000, 16, 2),
     (50, 40, 30, 20_000, 64, 3), (5000, 100, 100, 3000, 32, 4), (20, 3000, 3000, 200_000, 32, 5),
-    (400, 300, 200, 60_000, 8, 6), (100, 90, 80, 30_000, 100, 7)])
+    (400, 300, 200, 60_000, 8, 6), (100, 90, 80, 30_000, 100, 7), (60, 50, 40, 8_000, 200, 8)])
 def test_mttkrp_vs_oracle(orc, I, J, Kd, nnz, R, seed):
     m = wl.mttkrp(I=I, J=J, K=Kd, nnz=nnz, R=R, seed=seed)
     csf = wl.coo3_to_csf(m["i"], m["j"], m["k"], None)
