@@ -319,14 +319,13 @@ add_tile_kernel(int64_t nrows, const int32_t* __restrict__ a_pos, const int32_t*
   const int32_t ea1 = s_apos[nr], eb1 = s_bpos[nr];
   const int na = ea1 - ea0, nb = eb1 - eb0;
   const bool fits = staged_ok && na <= kAddCap && nb <= kAddCap;   // block-uniform
-  BulkRange<int32_t> ra{}, rb{};
-  BulkRange<double> rav{}, rbv{};
+  BulkRange32 ra{}, rb{}, rav{}, rbv{};
   if (fits) {
-    ra = plan_range(a_crd, ea0, ea1);
-    rb = plan_range(b_cols, eb0, eb1);
+    ra = plan_range32(a_crd, ea0, ea1);
+    rb = plan_range32(b_cols, eb0, eb1);
     if (kValues) {
-      rav = plan_range(a_vals, ea0, ea1);
-      rbv = plan_range(b_vals, eb0, eb1);
+      rav = plan_range32(a_vals, ea0, ea1);
+      rbv = plan_range32(b_vals, eb0, eb1);
     }
     // element p of A lands at s_col[p - ra.lo0] and s_val[p - ra.lo0] (B: + kCS);
     // with 16-byte-aligned operands (staged_ok) the value copies stay aligned
@@ -336,18 +335,18 @@ add_tile_kernel(int64_t nrows, const int32_t* __restrict__ a_pos, const int32_t*
     double* sbv = kValues ? s_val + kCS + (int32_t)(rbv.lo0 - rb.lo0) : s_val;
     if (tid == 0) {
       mbar_arrive_expect_tx(&bar, ra.tx_bytes + rb.tx_bytes + rav.tx_bytes + rbv.tx_bytes);
-      issue_range(a_crd, ra, sa, &bar);
-      issue_range(b_cols, rb, sb, &bar);
+      issue_range32(a_crd, ra, sa, &bar);
+      issue_range32(b_cols, rb, sb, &bar);
       if (kValues) {
-        issue_range(a_vals, rav, sav, &bar);
-        issue_range(b_vals, rbv, sbv, &bar);
+        issue_range32(a_vals, rav, sav, &bar);
+        issue_range32(b_vals, rbv, sbv, &bar);
       }
     }
-    edge_loads_small(a_crd, ra, ea0, ea1, sa, tid);
-    edge_loads_small(b_cols, rb, eb0, eb1, sb, tid);
+    edge_loads_small32(a_crd, ra, ea0, ea1, sa, tid);
+    edge_loads_small32(b_cols, rb, eb0, eb1, sb, tid);
     if (kValues) {
-      edge_loads_small(a_vals, rav, ea0, ea1, sav, tid);
-      edge_loads_small(b_vals, rbv, eb0, eb1, sbv, tid);
+      edge_loads_small32(a_vals, rav, ea0, ea1, sav, tid);
+      edge_loads_small32(b_vals, rbv, eb0, eb1, sbv, tid);
     }
     __syncthreads();
     mbar_wait(&bar, 0);
@@ -376,29 +375,29 @@ add_tile_kernel(int64_t nrows, const int32_t* __restrict__ a_pos, const int32_t*
   // stage the slices of rows [g0, g1); returns the stage index offsets of A and B
   auto stage_group = [&](int g0, int g1, int32_t& oa, int32_t& ob) {
     const int32_t alo = s_apos[g0], ahi = s_apos[g1], blo = s_bpos[g0], bhi = s_bpos[g1];
-    const BulkRange<int32_t> ga = plan_range(a_crd, alo, ahi), gb = plan_range(b_cols, blo, bhi);
-    BulkRange<double> gav{}, gbv{};
+    const BulkRange32 ga = plan_range32(a_crd, alo, ahi), gb = plan_range32(b_cols, blo, bhi);
+    BulkRange32 gav{}, gbv{};
     if (kValues) {
-      gav = plan_range(a_vals, alo, ahi);
-      gbv = plan_range(b_vals, blo, bhi);
+      gav = plan_range32(a_vals, alo, ahi);
+      gbv = plan_range32(b_vals, blo, bhi);
     }
     double* sav = s_val + (int32_t)(gav.lo0 - ga.lo0);
     double* sbv = kValues ? s_val + kCS + (int32_t)(gbv.lo0 - gb.lo0) : s_val;
     if (tid == 0) {
       fence_proxy_async_smem();          // the previous group's reads precede these writes
       mbar_arrive_expect_tx(&bar, ga.tx_bytes + gb.tx_bytes + gav.tx_bytes + gbv.tx_bytes);
-      issue_range(a_crd, ga, s_col, &bar);
-      issue_range(b_cols, gb, s_col + kCS, &bar);
+      issue_range32(a_crd, ga, s_col, &bar);
+      issue_range32(b_cols, gb, s_col + kCS, &bar);
       if (kValues) {
-        issue_range(a_vals, gav, sav, &bar);
-        issue_range(b_vals, gbv, sbv, &bar);
+        issue_range32(a_vals, gav, sav, &bar);
+        issue_range32(b_vals, gbv, sbv, &bar);
       }
     }
-    edge_loads_small(a_crd, ga, alo, ahi, s_col, tid);
-    edge_loads_small(b_cols, gb, blo, bhi, s_col + kCS, tid);
+    edge_loads_small32(a_crd, ga, alo, ahi, s_col, tid);
+    edge_loads_small32(b_cols, gb, blo, bhi, s_col + kCS, tid);
     if (kValues) {
-      edge_loads_small(a_vals, gav, alo, ahi, sav, tid);
-      edge_loads_small(b_vals, gbv, blo, bhi, sbv, tid);
+      edge_loads_small32(a_vals, gav, alo, ahi, sav, tid);
+      edge_loads_small32(b_vals, gbv, blo, bhi, sbv, tid);
     }
     __syncthreads();
     mbar_wait(&bar, gphase);
