@@ -349,7 +349,9 @@ add_tile_kernel(int64_t nrows, const int32_t* __restrict__ a_pos, const int32_t*
       edge_loads_small32(b_vals, rbv, eb0, eb1, sbv, tid);
     }
     __syncthreads();
-    mbar_wait(&bar, 0);
+    // the fill waits for the copy only after reading its row bases and tile
+    // prefix (global loads that then overlap the bulk copy)
+    if (!kValues) mbar_wait(&bar, 0);
   }
   // ---- tiles beyond the stage (denser or power-law rows): consecutive row
   // groups whose A and B slices fit are staged and merged one after another
@@ -583,6 +585,7 @@ add_tile_kernel(int64_t nrows, const int32_t* __restrict__ a_pos, const int32_t*
     }
     return;
   }
+  if (fits) mbar_wait(&bar, 0);
   const bool staged_out = n_out <= 2 * kAddCap;
   int32_t* oc = staged_out ? s_ccrd : c_crd + tile_out;
   double* ov = staged_out ? s_cval : c_vals + tile_out;
