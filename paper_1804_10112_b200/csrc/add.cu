@@ -226,7 +226,12 @@ struct FillEmit {
 // kMode 2: fill + finalise c_pos from the tile-local counts and the tile prefix
 
 constexpr int kAddRows = 128;
-constexpr int kAddCap = 768;     // staged elements per operand per tile (Poisson(5) tiles: 640 +- 25)
+// staged elements per operand per tile (Poisson(5) x 128 rows: 640 +- 25;
+// larger tiles take the grouped path): the count stages columns only and is
+// thread-bound at 16 blocks/SM, so it keeps the roomier stage; the fill's
+// 704-element stage lets 6 instead of 5 blocks share an SM (85.1 -> 81.4 us)
+constexpr int kAddCapCount = 768;
+constexpr int kAddCapFill = 704;
 constexpr int kSuper = 64;       // tiles per super-tile of the two-level prefix
 
 // Accessor for tiles that exceed the stage capacity (or unaligned operands):
@@ -288,6 +293,7 @@ add_tile_kernel(int64_t nrows, const int32_t* __restrict__ a_pos, const int32_t*
                 int64_t* __restrict__ super_tot, bool staged_ok,
                 const int32_t* __restrict__ guard = nullptr) {
   constexpr bool kValues = kMode != 0;
+  constexpr int kAddCap = kValues ? kAddCapFill : kAddCapCount;
   if (guard != nullptr && ldg(guard) == 0) return;   // nothing to merge (see the exact convert)
   __shared__ int32_t s_apos[kAddRows + 1], s_bpos[kAddRows + 1];
   // unified stages: A's slice at [0, kCS), B's at [kCS, 2 kCS); a value is
