@@ -162,6 +162,36 @@ SL_DEV int count_row_idx(int ia, int iah, int ib, int ibh, const int32_t* s_col)
 // rewrites the run's output slot; the slot's last write, at the run's last
 // element, is the final value 0 + (a + bgroup | a | bgroup) (engine.py:404,
 // 413, 524-531, 625-631).  No divergent branches.
+// The fill merge for a tile whose B slice repeats no coordinate (the usual
+// case; checked per tile): a run is one entry, or an A entry followed by the
+// B entry it matches, so the value is v, or a + b for the match — stored as
+// 0 + value like the general form, without its repeat-group state.
+SL_DEV void fill_row_idx_unique(int ia, int iah, int ib, int ibh, const int32_t* s_col,
+                                const double* s_val, int32_t* oc, double* ov) {
+  int n = -1;
+  int32_t last = -1;
+  double prev = 0.0;
+  int32_t ca = ia < iah ? s_col[ia] : INT32_MAX;
+  int32_t cb = ib < ibh ? s_col[ib] : INT32_MAX;
+  for (int it = (iah - ia) + (ibh - ib); it > 0; --it) {
+    const bool ta = ca <= cb;
+    const int32_t c = ta ? ca : cb;
+    const double v = s_val[ta ? ia : ib];
+    const bool fresh = c != last;
+    n += fresh;
+    last = c;
+    oc[n] = c;
+    ov[n] = dadd(0.0, fresh ? v : dadd(prev, v));   // not fresh: B matching the A before it
+    prev = v;
+    ia += ta;
+    ib += !ta;
+    const int idx = ta ? ia : ib;
+    const int32_t nx = idx < (ta ? iah : ibh) ? s_col[idx] : INT32_MAX;
+    ca = ta ? nx : ca;
+    cb = ta ? cb : nx;
+  }
+}
+
 SL_DEV int fill_row_idx(int ia, int iah, int ib, int ibh, const int32_t* s_col,
                         const double* s_val, int32_t* oc, double* ov) {
   int n = -1;
@@ -592,13 +622,24 @@ add_tile_kernel(int64_t nrows, const int32_t* __restrict__ a_pos, const int32_t*
     return;
   }
   if (fits) mbar_wait(&bar, 0);
+  // does the staged B slice repeat a coordinate?  (adjacent equal columns;
+  // across a row boundary this only makes the check conservative)
+  bool b_rep = false;
+  if (fits) {
+    const int boff = kCS + eb0 - (int32_t)rb.lo0;
+    for (int q = 1 + tid; q < nb; q += kAddRows) b_rep |= s_col[boff + q] == s_col[boff + q - 1];
+  }
+  const bool b_unique = fits && !__syncthreads_or(b_rep);
   const bool staged_out = n_out <= 2 * kAddCap;
   int32_t* oc = staged_out ? s_ccrd : c_crd + tile_out;
   double* ov = staged_out ? s_cval : c_vals + tile_out;
   if (mine) {
     const int32_t lo = s_rbase[tid];
     if (fits)
-      fill_row_idx(ia, iah, ib, ibh, s_col, s_val, oc + lo, ov + lo);
+      if (b_unique)
+        fill_row_idx_unique(ia, iah, ib, ibh, s_col, s_val, oc + lo, ov + lo);
+      else
+        fill_row_idx(ia, iah, ib, ibh, s_col, s_val, oc + lo, ov + lo);
     else
       merge_row<true>(s_apos[tid], s_apos[tid + 1], s_bpos[tid], s_bpos[tid + 1], gacc,
                       FillEmit{oc + lo, ov + lo});
