@@ -357,11 +357,11 @@ add_tile_kernel(int64_t nrows, const int32_t* __restrict__ a_pos, const int32_t*
   const bool fits = staged_ok && na <= kAddCap && nb <= kAddCap;   // block-uniform
   BulkRange32 ra{}, rb{}, rav{}, rbv{};
   if (fits) {
-    ra = plan_range32(a_crd, ea0, ea1);
-    rb = plan_range32(b_cols, eb0, eb1);
+    ra = plan_granules32(a_crd, ea0, ea1);
+    rb = plan_granules32(b_cols, eb0, eb1);
     if (kValues) {
-      rav = plan_range32(a_vals, ea0, ea1);
-      rbv = plan_range32(b_vals, eb0, eb1);
+      rav = plan_granules32(a_vals, ea0, ea1);
+      rbv = plan_granules32(b_vals, eb0, eb1);
     }
     // element p of A lands at s_col[p - ra.lo0] and s_val[p - ra.lo0] (B: + kCS);
     // with 16-byte-aligned operands (staged_ok) the value copies stay aligned
@@ -377,12 +377,6 @@ add_tile_kernel(int64_t nrows, const int32_t* __restrict__ a_pos, const int32_t*
         issue_range32(a_vals, rav, sav, &bar);
         issue_range32(b_vals, rbv, sbv, &bar);
       }
-    }
-    edge_loads_small32(a_crd, ra, ea0, ea1, sa, tid);
-    edge_loads_small32(b_cols, rb, eb0, eb1, sb, tid);
-    if (kValues) {
-      edge_loads_small32(a_vals, rav, ea0, ea1, sav, tid);
-      edge_loads_small32(b_vals, rbv, eb0, eb1, sbv, tid);
     }
     __syncthreads();
     // the fill waits for the copy only after reading its row bases and tile
@@ -413,11 +407,11 @@ add_tile_kernel(int64_t nrows, const int32_t* __restrict__ a_pos, const int32_t*
   // stage the slices of rows [g0, g1); returns the stage index offsets of A and B
   auto stage_group = [&](int g0, int g1, int32_t& oa, int32_t& ob) {
     const int32_t alo = s_apos[g0], ahi = s_apos[g1], blo = s_bpos[g0], bhi = s_bpos[g1];
-    const BulkRange32 ga = plan_range32(a_crd, alo, ahi), gb = plan_range32(b_cols, blo, bhi);
+    const BulkRange32 ga = plan_granules32(a_crd, alo, ahi), gb = plan_granules32(b_cols, blo, bhi);
     BulkRange32 gav{}, gbv{};
     if (kValues) {
-      gav = plan_range32(a_vals, alo, ahi);
-      gbv = plan_range32(b_vals, blo, bhi);
+      gav = plan_granules32(a_vals, alo, ahi);
+      gbv = plan_granules32(b_vals, blo, bhi);
     }
     double* sav = s_val + (int32_t)(gav.lo0 - ga.lo0);
     double* sbv = kValues ? s_val + kCS + (int32_t)(gbv.lo0 - gb.lo0) : s_val;
@@ -430,12 +424,6 @@ add_tile_kernel(int64_t nrows, const int32_t* __restrict__ a_pos, const int32_t*
         issue_range32(a_vals, gav, sav, &bar);
         issue_range32(b_vals, gbv, sbv, &bar);
       }
-    }
-    edge_loads_small32(a_crd, ga, alo, ahi, s_col, tid);
-    edge_loads_small32(b_cols, gb, blo, bhi, s_col + kCS, tid);
-    if (kValues) {
-      edge_loads_small32(a_vals, gav, alo, ahi, sav, tid);
-      edge_loads_small32(b_vals, gbv, blo, bhi, sbv, tid);
     }
     __syncthreads();
     mbar_wait(&bar, gphase);

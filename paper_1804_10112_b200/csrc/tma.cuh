@@ -154,6 +154,22 @@ SL_DEV BulkRange32 plan_range32(const T* g, int32_t lo, int32_t hi) {
   return r;
 }
 
+// Whole 16-byte granules covering [lo, hi): no plain edge loads at all.  The
+// granules at the ends hold elements outside the range (garbage in the
+// stage, never read); each granule holds at least one element of the range,
+// so no read leaves the array's pages.
+template <typename T>
+SL_DEV BulkRange32 plan_granules32(const T* g, int32_t lo, int32_t hi) {
+  constexpr int32_t per16 = 16 / sizeof(T);
+  const int32_t mis = (int32_t)((reinterpret_cast<uintptr_t>(g) / sizeof(T)) & (per16 - 1));
+  BulkRange32 r;
+  r.lo0 = ((lo + mis) & ~(per16 - 1)) - mis;
+  r.blo = r.lo0;
+  r.bhi = hi > lo ? ((hi + mis + per16 - 1) & ~(per16 - 1)) - mis : r.lo0;
+  r.tx_bytes = (uint32_t)(r.bhi - r.blo) * (uint32_t)sizeof(T);
+  return r;
+}
+
 template <typename T>
 SL_DEV void issue_range32(const T* g, const BulkRange32& r, T* s, uint64_t* bar) {
   if (r.tx_bytes) bulk_g2s(s + (r.blo - r.lo0), g + r.blo, r.tx_bytes, bar);
