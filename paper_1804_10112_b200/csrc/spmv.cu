@@ -976,7 +976,9 @@ extern "C" int sl_spmv_coo_f64(int64_t nrows, int64_t ncols, int64_t nnz, const 
   if (vec_ok && spmv_path() == 2) return sl_host::launch_coo_pipe(nrows, nnz, rows, cols, vals, x, y, s);
   // 1024-nonzero tiles, 8 blocks/SM: on D1 (2M nonzeros) the grid is 1.65x the
   // resident slots, so later tiles' loads overlap earlier tiles' sum phases
-  // (measured: 2048-nonzero tiles in one wave 37.0 us, this 26.2 us; 512-tile
+  // (measured: 2048-nonzero tiles in one wave 37.0 us, this 26.2 us; dropping
+  // the start compaction for per-thread walks from each staged item's start
+  // bit: 29.4 vs 24.8 us, the walks imbalance the lanes; 512-tile
   // and 128-thread variants 26.7-42 us; a persistent version prefetching the
   // next tile into registers during the current tile's shared-memory phases
   // 26.9-34.8 us at 4-8 blocks/SM: profiles/ab/r1_coo_persistent_prefetch.txt;
