@@ -41,6 +41,7 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 METRIC = "SpMV effective HBM GB/s (% of peak) per format; MTTKRP nnz/s"
+E2E_STREAMS = 4                         # e2e pipelining depth (tools/e2e_probe.py: 4 beats 3, 6 no better)
 WORKLOAD = "ELL vs CSR SpMV fp64, 27-point stencil 64^3 (BASELINE configs[1])"
 G = 64
 
@@ -264,20 +265,21 @@ def run_ours(args, rank, world, local_rank):
 
     # ---- e2e through the public API: x from pinned host memory each step,
     # the matrix resident on the device (like weights), y read back.  Steps
-    # alternate between two streams (and two pinned x / y buffers), so step
-    # k+1's host->device copy overlaps step k's kernel and device->host copy —
+    # rotate over E2E_STREAMS streams (each with its own pinned x / y buffers),
+    # so step k+1's host->device copy overlaps step k's kernel and device->host copy —
     # a serving loop's pipelining; every step still moves its own x in and y out.
     A_st = F.csr_storage(pos, crd, vals, (nrows, ncols), device=dev)
-    x_hosts = [torch.as_tensor(st["x"]).pin_memory() for _ in range(3)]
+    ns = E2E_STREAMS
+    x_hosts = [torch.as_tensor(st["x"]).pin_memory() for _ in range(ns)]
     xs = [F.dense_storage(xh, device=None) for xh in x_hosts]
-    y_hosts = [torch.empty(nrows, dtype=torch.float64).pin_memory() for _ in range(3)]
-    streams = [torch.cuda.Stream(device=dev) for _ in range(3)]
+    y_hosts = [torch.empty(nrows, dtype=torch.float64).pin_memory() for _ in range(ns)]
+    streams = [torch.cuda.Stream(device=dev) for _ in range(ns)]
     expr = "y(i) = A(i,j) * x(j)"
 
     def e2e_step(k):
-        with torch.cuda.stream(streams[k % 3]):
-            y_dev = evaluate(expr, {"A": A_st, "x": xs[k % 3]}).vals
-            y_hosts[k % 3].copy_(y_dev, non_blocking=True)
+        with torch.cuda.stream(streams[k % ns]):
+            y_dev = evaluate(expr, {"A": A_st, "x": xs[k % ns]}).vals
+            y_hosts[k % ns].copy_(y_dev, non_blocking=True)
 
     for k in range(max(args.warmup, 3)):
         e2e_step(k)
@@ -325,7 +327,7 @@ def run_ours(args, rank, world, local_rank):
                 "d2h_bytes_per_step": int(nrows * 8),
                 "ms_per_step": round(t_e2e * 1e3, 4),
                 "path": "evaluate('y(i) = A(i,j) * x(j)') CSR, pinned host x in, y out every "
-                        "step; matrix resident in HBM; steps rotate over 3 streams"},
+                        f"step; matrix resident in HBM; steps rotate over {ns} streams"},
         "gpu_launches": launches,
         "gpu_launches_note": (f"{launches} SpMV kernel launches inside the timed events "
                               f"(CSR + ELL per step); plus {timer.flush_launches} L2-sweep "

@@ -162,7 +162,11 @@ def ptr(t):
 
 
 def stream_handle(stream=None):
+    """cudaStream_t of `stream`, else of the current device's current stream
+    (the raw query: torch.cuda.current_stream() costs several microseconds of
+    Python per launch, which the e2e step pays on every call)."""
     import torch
 
-    s = stream if stream is not None else torch.cuda.current_stream()
-    return s.cuda_stream
+    if stream is not None:
+        return stream.cuda_stream
+    return torch._C._cuda_getCurrentRawStream(torch._C._cuda_getDevice())

@@ -454,6 +454,13 @@ def _run(p: Plan, inputs: Dict[str, TensorStorage], stats: Optional[EvalStats]):
 
 _PLAN_CACHE: Dict[tuple, Plan] = {}
 _PLAN_CACHE_MAX = 256
+_FAST_CACHE: Dict[tuple, tuple] = {}
+
+
+def _remember(fkey, inputs, out_format, p: Plan) -> None:
+    if len(_FAST_CACHE) >= _PLAN_CACHE_MAX:
+        _FAST_CACHE.clear()
+    _FAST_CACHE[fkey] = (tuple(s.format for s in inputs.values()), out_format, p)
 
 
 def evaluate(expr, inputs: Dict[str, TensorStorage], out_format: Optional[TensorFormat] = None,
@@ -471,6 +478,15 @@ def evaluate(expr, inputs: Dict[str, TensorStorage], out_format: Optional[Tensor
     """
     key = None
     if isinstance(expr, str):
+        # identity fast path: the same format objects as a cached call skip
+        # hashing the (recursive, frozen-dataclass) formats; the entry holds the
+        # format objects, so their ids cannot be reused while it is cached
+        fkey = (expr, tuple((n, id(s.format), s.dims) for n, s in inputs.items()),
+                id(out_format), None if out_dims is None else tuple(out_dims))
+        hit = _FAST_CACHE.get(fkey)
+        if hit is not None and all(s.format is f for s, f in zip(inputs.values(), hit[0])) \
+                and hit[1] is out_format:
+            return _run(hit[2], inputs, stats)
         try:
             key = (expr, tuple(sorted((n, s.format, s.dims) for n, s in inputs.items())),
                    out_format, None if out_dims is None else tuple(out_dims))
@@ -478,6 +494,7 @@ def evaluate(expr, inputs: Dict[str, TensorStorage], out_format: Optional[Tensor
         except TypeError:            # an unhashable format: plan every time
             key, p = None, None
         if p is not None:
+            _remember(fkey, inputs, out_format, p)
             return _run(p, inputs, stats)
     assignment = parse(expr) if isinstance(expr, str) else expr
     bindings = {name: (s.format, s.dims) for name, s in inputs.items()}
@@ -493,6 +510,7 @@ def evaluate(expr, inputs: Dict[str, TensorStorage], out_format: Optional[Tensor
         if len(_PLAN_CACHE) >= _PLAN_CACHE_MAX:
             _PLAN_CACHE.clear()
         _PLAN_CACHE[key] = p
+        _remember(fkey, inputs, out_format, p)
     return _run(p, inputs, stats)
 
 

@@ -1,7 +1,7 @@
 #!/usr/bin/env python
 """Where the end-to-end SpMV step's time goes (bench.py's `e2e` leg): host
 cost of one evaluate() call, pinned H2D / D2H copy times of x and y, and the
-full step loop over 1, 2 and 3 streams.
+full step loop over 2, 3, 4 and 6 streams.
 
     python tools/e2e_probe.py [--steps 200]
 """
@@ -40,13 +40,13 @@ def main():
     n = st["nrows"]
     pos, crd, vals = (torch.as_tensor(a, device=dev) for a in (st["pos"], st["crd"], st["vals"]))
     A = F.csr_storage(pos, crd, vals, (n, n), device=dev)
-    xh = [torch.as_tensor(st["x"]).pin_memory() for _ in range(3)]
-    yh = [torch.empty(n, dtype=torch.float64).pin_memory() for _ in range(3)]
-    xd = [torch.empty(n, dtype=torch.float64, device=dev) for _ in range(3)]
-    yd = [torch.empty(n, dtype=torch.float64, device=dev) for _ in range(3)]
+    xh = [torch.as_tensor(st["x"]).pin_memory() for _ in range(6)]
+    yh = [torch.empty(n, dtype=torch.float64).pin_memory() for _ in range(6)]
+    xd = [torch.empty(n, dtype=torch.float64, device=dev) for _ in range(6)]
+    yd = [torch.empty(n, dtype=torch.float64, device=dev) for _ in range(6)]
     xs_host = [F.dense_storage(x, device=None) for x in xh]
     xs_dev = [F.dense_storage(x, device=dev) for x in xd]
-    streams = [torch.cuda.Stream(device=dev) for _ in range(3)]
+    streams = [torch.cuda.Stream(device=dev) for _ in range(6)]
     expr = "y(i) = A(i,j) * x(j)"
     for k in range(5):
         evaluate(expr, {"A": A, "x": xs_host[0]})
@@ -75,7 +75,7 @@ def main():
             yh[1].copy_(yd[1], non_blocking=True)
     print(f"H2D + D2H on two streams: {wall(h2d_d2h, args.steps):.1f} us/step")
 
-    for ns in (1, 2, 3):
+    for ns in (2, 3, 4, 6):
         def step(k, ns=ns):
             with torch.cuda.stream(streams[k % ns]):
                 y = evaluate(expr, {"A": A, "x": xs_host[k % ns]}).vals
