@@ -253,6 +253,16 @@ int sl_spmv_csr_spx_f64(int64_t nrows, int64_t n, int64_t nnz, const int32_t* po
 int sl_spmm_csr_f64(int64_t nrows, int64_t ncols, int64_t K, const int32_t* pos,
                     const int32_t* crd, const double* vals, const double* X, double* Y,
                     void* stream);
+/* The same product with rows longer than long_min split out (power-law
+ * rows): a device pass lists them (workspace: a counter and the list), the
+ * group kernel skips them, and one CTA per listed row gathers its X rows with
+ * all warps while one warp adds the products in storage order — bit-identical
+ * to sl_spmm_csr_f64.  Same reference loop nest as above. */
+int64_t sl_spmm_csr_split_workspace_bytes(int64_t nrows, int64_t nnz, int32_t long_min);
+int sl_spmm_csr_split_f64(int64_t nrows, int64_t ncols, int64_t K, int64_t nnz,
+                          const int32_t* pos, const int32_t* crd, const double* vals,
+                          const double* X, double* Y, int32_t long_min, void* ws,
+                          int64_t ws_bytes, void* stream);
 
 /* ---- 3-tensor kernels beyond MTTKRP (X CSF) ----------
  * TTV Y(i,j) = X(i,j,k) v(k) and TTM Y(i,j,r) = X(i,j,k) U(k,r) reduce over k

@@ -28,7 +28,8 @@ template <int G, int kB = 4>
 __global__ void __launch_bounds__(256)
 spmm_csr_kernel(int64_t nrows, int64_t K, const int32_t* __restrict__ pos,
                 const int32_t* __restrict__ crd, const double* __restrict__ vals,
-                const double* __restrict__ X, double* __restrict__ Y) {
+                const double* __restrict__ X, double* __restrict__ Y,
+                int32_t long_min = INT32_MAX) {
   constexpr int kRowsPerWarp = 32 / G;
   const int lane = threadIdx.x & 31;
   const int g = lane / G, gl = lane % G;
@@ -36,8 +37,11 @@ spmm_csr_kernel(int64_t nrows, int64_t K, const int32_t* __restrict__ pos,
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t w = warp; w * kRowsPerWarp < nrows; w += nwarps) {
     const int64_t row = w * kRowsPerWarp + g;
-    const bool live = row < nrows;
-    const int32_t b = live ? ldg(pos + row) : 0, e = live ? ldg(pos + row + 1) : 0;
+    const int32_t b = row < nrows ? ldg(pos + row) : 0;
+    int32_t e = row < nrows ? ldg(pos + row + 1) : 0;
+    // rows longer than long_min belong to spmm_long_rows_kernel
+    const bool live = row < nrows && e - b <= long_min;
+    if (!live) e = b;
     for (int64_t k0 = 0; k0 < K; k0 += G) {
       const int64_t k = k0 + gl;
       const bool kin = live && k < K;
@@ -76,34 +80,157 @@ spmm_csr_kernel(int64_t nrows, int64_t K, const int32_t* __restrict__ pos,
   }
 }
 
+// Rows longer than long_min, listed by spmm_mark_long_kernel: one CTA per
+// row.  A lone group walking a power-law row keeps only kB gathers in flight
+// per lane, so a 10^5-nonzero row costs ~10^5/kB dependent gather latencies.
+// Here all eight warps gather a chunk of the row's X rows — a warp covers
+// 32/G nonzeros x G columns per step, kPer steps with every load issued
+// before the first use — and form the products A(i,j)*X(j,k) in shared
+// memory; then warp 0 (lane l < G owning column k0 + l) adds them in storage
+// order.  dadd(acc, dmul(a, x)) in the same order as the group kernel:
+// bit-identical.  The add chain (one dependent dadd per nonzero per column)
+// is the floor the ordered sum imposes.
+template <int G>
+__global__ void __launch_bounds__(256)
+spmm_long_rows_kernel(int64_t K, const int32_t* __restrict__ pos, const int32_t* __restrict__ crd,
+                      const double* __restrict__ vals, const double* __restrict__ X,
+                      double* __restrict__ Y, const int32_t* __restrict__ list,
+                      const int32_t* __restrict__ count) {
+  constexpr int kPer = 16, kRows = 32 / G, kChunk = 8 * kRows * kPer;
+  __shared__ double P[kChunk][G + 1];   // +1: conflict-free column reads by warp 0
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int gl = lane % G, gr = lane / G;
+  const int n = *count;
+  for (int li = blockIdx.x; li < n; li += gridDim.x) {
+    const int64_t row = list[li];
+    const int32_t b = ldg(pos + row), e = ldg(pos + row + 1);
+    for (int64_t k0 = 0; k0 < K; k0 += G) {
+      const int64_t k = k0 + gl;
+      const int64_t kc = k < K ? k : K - 1;          // in-bounds column for idle lanes
+      double acc = 0.0;
+      for (int32_t c0 = b; c0 < e; c0 += kChunk) {
+        const int nc = min(kChunk, e - c0);
+        int32_t c[kPer];
+        double a[kPer], xv[kPer];
+#pragma unroll
+        for (int u = 0; u < kPer; ++u) {
+          const int t = (warp + 8 * u) * kRows + gr;
+          const int tt = min(t, nc - 1);
+          c[u] = ldg(crd + c0 + tt);
+          a[u] = ldg(vals + c0 + tt);
+        }
+#pragma unroll
+        for (int u = 0; u < kPer; ++u) xv[u] = ldg(X + (int64_t)c[u] * K + kc);
+#pragma unroll
+        for (int u = 0; u < kPer; ++u) P[(warp + 8 * u) * kRows + gr][gl] = dmul(a[u], xv[u]);
+        __syncthreads();
+        if (warp == 0 && lane < G) {
+          int t = 0;
+          for (; t + 4 <= nc; t += 4) {
+            const double p0 = P[t][lane], p1 = P[t + 1][lane], p2 = P[t + 2][lane],
+                         p3 = P[t + 3][lane];
+            acc = dadd(dadd(dadd(dadd(acc, p0), p1), p2), p3);
+          }
+          for (; t < nc; ++t) acc = dadd(acc, P[t][lane]);
+        }
+        __syncthreads();
+      }
+      if (warp == 0 && lane < G && k < K) Y[row * K + k] = acc;
+    }
+  }
+}
+
+__global__ void spmm_mark_long_kernel(int64_t nrows, const int32_t* __restrict__ pos,
+                                      int32_t long_min, int32_t* __restrict__ list,
+                                      int32_t* __restrict__ count) {
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < nrows;
+       r += (int64_t)gridDim.x * blockDim.x)
+    if (ldg(pos + r + 1) - ldg(pos + r) > long_min) list[atomicAdd(count, 1)] = (int32_t)r;
+}
+
 }  // namespace sl
 
 using namespace sl;
 using sl_host::as_stream;
 using sl_host::ceil_div;
 
-extern "C" int sl_spmm_csr_f64(int64_t nrows, int64_t ncols, int64_t K, const int32_t* pos,
-                               const int32_t* crd, const double* vals, const double* X, double* Y,
-                               void* stream) {
-  if (nrows < 0 || ncols < 0 || K < 0) return SL_ERR_INVALID;
-  if (nrows > INT32_MAX || ncols > INT32_MAX || K > INT32_MAX) return SL_ERR_RANGE;
-  if (nrows == 0 || K == 0) return SL_OK;
-  if (!pos || !Y || (ncols > 0 && !X)) return SL_ERR_INVALID;
-  cudaStream_t s = as_stream(stream);
+namespace {
+
+int spmm_launch(int64_t nrows, int64_t ncols, int64_t K, const int32_t* pos, const int32_t* crd,
+                const double* vals, const double* X, double* Y, int32_t long_min,
+                cudaStream_t s) {
   const int G = K >= 32 ? 32 : (K > 8 ? 16 : (K > 4 ? 8 : (K > 2 ? 4 : (K > 1 ? 2 : 1))));
   const int64_t rows_per_block = 8 * (32 / G);
   const int grid = (int)std::min<int64_t>(ceil_div(nrows, rows_per_block),
                                           (int64_t)sl_host::sm_count() * 64);
   switch (G) {
-    case 32: spmm_csr_kernel<32><<<grid, 256, 0, s>>>(nrows, K, pos, crd, vals, X, Y); break;
+    case 32: spmm_csr_kernel<32><<<grid, 256, 0, s>>>(nrows, K, pos, crd, vals, X, Y, long_min); break;
     case 16:   // gathers 2 at a time: 122.9 us vs 130.0 / 133.4 / 244.0 us with 4 / 8 / 16
                // (64^3 stencil, K = 16: throughput-, not latency-bound; tools/ab_spmm.py)
-      spmm_csr_kernel<16, 2><<<grid, 256, 0, s>>>(nrows, K, pos, crd, vals, X, Y);
+      spmm_csr_kernel<16, 2><<<grid, 256, 0, s>>>(nrows, K, pos, crd, vals, X, Y, long_min);
       break;
-    case 8: spmm_csr_kernel<8><<<grid, 256, 0, s>>>(nrows, K, pos, crd, vals, X, Y); break;
-    case 4: spmm_csr_kernel<4><<<grid, 256, 0, s>>>(nrows, K, pos, crd, vals, X, Y); break;
-    case 2: spmm_csr_kernel<2><<<grid, 256, 0, s>>>(nrows, K, pos, crd, vals, X, Y); break;
-    default: spmm_csr_kernel<1><<<grid, 256, 0, s>>>(nrows, K, pos, crd, vals, X, Y); break;
+    case 8: spmm_csr_kernel<8><<<grid, 256, 0, s>>>(nrows, K, pos, crd, vals, X, Y, long_min); break;
+    case 4: spmm_csr_kernel<4><<<grid, 256, 0, s>>>(nrows, K, pos, crd, vals, X, Y, long_min); break;
+    case 2: spmm_csr_kernel<2><<<grid, 256, 0, s>>>(nrows, K, pos, crd, vals, X, Y, long_min); break;
+    default: spmm_csr_kernel<1><<<grid, 256, 0, s>>>(nrows, K, pos, crd, vals, X, Y, long_min); break;
   }
+  return sl_host::launch_status();
+}
+
+int spmm_check(int64_t nrows, int64_t ncols, int64_t K, const int32_t* pos, const double* X,
+               double* Y) {
+  if (nrows < 0 || ncols < 0 || K < 0) return SL_ERR_INVALID;
+  if (nrows > INT32_MAX || ncols > INT32_MAX || K > INT32_MAX) return SL_ERR_RANGE;
+  if (nrows == 0 || K == 0) return SL_OK;
+  if (!pos || !Y || (ncols > 0 && !X)) return SL_ERR_INVALID;
+  return -1;
+}
+
+}  // namespace
+
+extern "C" int sl_spmm_csr_f64(int64_t nrows, int64_t ncols, int64_t K, const int32_t* pos,
+                               const int32_t* crd, const double* vals, const double* X, double* Y,
+                               void* stream) {
+  const int st = spmm_check(nrows, ncols, K, pos, X, Y);
+  if (st >= 0) return st;
+  return spmm_launch(nrows, ncols, K, pos, crd, vals, X, Y, INT32_MAX, as_stream(stream));
+}
+
+extern "C" int64_t sl_spmm_csr_split_workspace_bytes(int64_t nrows, int64_t nnz,
+                                                     int32_t long_min) {
+  if (nrows <= 0 || long_min < 0) return 0;
+  const int64_t nlong = std::min<int64_t>(nrows, nnz / ((int64_t)long_min + 1) + 1);
+  return 16 + 4 * nlong;
+}
+
+extern "C" int sl_spmm_csr_split_f64(int64_t nrows, int64_t ncols, int64_t K, int64_t nnz,
+                                     const int32_t* pos, const int32_t* crd, const double* vals,
+                                     const double* X, double* Y, int32_t long_min, void* ws,
+                                     int64_t ws_bytes, void* stream) {
+  const int st = spmm_check(nrows, ncols, K, pos, X, Y);
+  if (st >= 0) return st;
+  if (long_min < 0) return SL_ERR_INVALID;
+  if (!ws || ws_bytes < sl_spmm_csr_split_workspace_bytes(nrows, nnz, long_min))
+    return SL_ERR_WORKSPACE;
+  cudaStream_t s = as_stream(stream);
+  int32_t* count = static_cast<int32_t*>(ws);
+  int32_t* list = reinterpret_cast<int32_t*>(static_cast<char*>(ws) + 16);
+  if (cudaMemsetAsync(count, 0, sizeof(int32_t), s) != cudaSuccess) return SL_ERR_CUDA;
+  spmm_mark_long_kernel<<<std::min<int64_t>(ceil_div(nrows, 256), 8LL * sl_host::sm_count()), 256,
+                          0, s>>>(nrows, pos, long_min, list, count);
+  int rc = sl_host::launch_status();
+  if (rc != SL_OK) return rc;
+  rc = spmm_launch(nrows, ncols, K, pos, crd, vals, X, Y, long_min, s);
+  if (rc != SL_OK) return rc;
+  const int64_t nlong = std::min<int64_t>(nrows, nnz / ((int64_t)long_min + 1) + 1);
+  const int lgrid = (int)std::min<int64_t>(nlong, 4LL * sl_host::sm_count());
+  if (K > 16)
+    spmm_long_rows_kernel<32><<<lgrid, 256, 0, s>>>(K, pos, crd, vals, X, Y, list, count);
+  else if (K > 8)
+    spmm_long_rows_kernel<16><<<lgrid, 256, 0, s>>>(K, pos, crd, vals, X, Y, list, count);
+  else if (K > 4)
+    spmm_long_rows_kernel<8><<<lgrid, 256, 0, s>>>(K, pos, crd, vals, X, Y, list, count);
+  else
+    spmm_long_rows_kernel<4><<<lgrid, 256, 0, s>>>(K, pos, crd, vals, X, Y, list, count);
   return sl_host::launch_status();
 }

@@ -290,6 +290,12 @@ def _csr_variant(lv: LevelStorage) -> int:
     power-law rows otherwise serialise one persistent warp per heavy tile
     (D5's fibres: 2.6 ms vs 0.23 ms).  The heaviest tile is measured once per
     row-pointer array and cached on the level."""
+    return 2 if _row_stats(lv)[0] > _SKEW_TILE else 0
+
+
+def _row_stats(lv: LevelStorage):
+    """(heaviest 32-row tile, longest row) of a compressed level, measured once
+    per row-pointer array and cached on the level."""
     cached = lv._sl_max_row
     if cached is None or cached[0] is not lv.pos:
         pos = lv.pos
@@ -297,12 +303,16 @@ def _csr_variant(lv: LevelStorage) -> int:
         if n > 0:
             idx = torch.arange(0, n + 32, 32, device=pos.device).clamp_(max=n)
             tb = pos[idx].to(torch.int64)
-            heaviest = int((tb[1:] - tb[:-1]).max().item())
+            both = torch.stack([(tb[1:] - tb[:-1]).max(), (pos[1:] - pos[:-1]).max().long()])
+            heaviest, longest = (int(v) for v in both.tolist())
         else:
-            heaviest = 0
-        cached = (pos, heaviest)
+            heaviest = longest = 0
+        cached = (pos, heaviest, longest)
         lv._sl_max_row = cached
-    return 2 if cached[1] > _SKEW_TILE else 0
+    return cached[1], cached[2]
+
+
+_SPMM_LONG_ROW = 1024  # SpMM rows longer than this: one CTA per row (power-law rows)
 
 
 def _next_pow2(v: int) -> int:
@@ -390,8 +400,9 @@ def _run(p: Plan, inputs: Dict[str, TensorStorage], stats: Optional[EvalStats]):
         A, X = ops["A"], ops["X"]
         nrows, ncols = A.dims
         Kc = X.dims[1]
+        long_min = _SPMM_LONG_ROW if _row_stats(A.levels[1])[1] > _SPMM_LONG_ROW else None
         Y = K.spmm_csr(nrows, ncols, A.levels[1].pos, A.levels[1].crd, A.vals,
-                       X.vals.view(ncols, Kc))
+                       X.vals.view(ncols, Kc), long_min=long_min)
         f = p.out_format
         out = TensorStorage(f, (nrows, Kc), [LevelStorage(f.levels[0], n=nrows, device=dev),
                                              LevelStorage(f.levels[1], n=Kc, device=dev)],

@@ -134,14 +134,23 @@ def spmv_csr_spx(nrows, n, pos, crd, vals, x_crd, x_vals, y=None, ws=None):
     return y
 
 
-def spmm_csr(nrows, ncols, pos, crd, vals, X, Y=None):
-    """Y = A X, A CSR (nrows x ncols), X dense (ncols x K) row-major."""
+def spmm_csr(nrows, ncols, pos, crd, vals, X, Y=None, long_min=None):
+    """Y = A X, A CSR (nrows x ncols), X dense (ncols x K) row-major.  With
+    `long_min`, rows longer than it run one CTA per row
+    (sl_spmm_csr_split_f64); same results."""
     pos, crd, vals = _t(pos, I32, "pos"), _t(crd, I32, "crd"), _t(vals, F64, "vals")
     X = _t(X, F64, "X")
     K = X.shape[-1] if X.dim() == 2 else X.numel() // max(ncols, 1)
     Y = _out(Y, nrows * K, F64, vals, "Y").view(nrows, K) if Y is None else _t(Y, F64, "Y")
-    _lib.check(L().sl_spmm_csr_f64(nrows, ncols, K, P(pos), P(crd), P(vals), P(X), P(Y), S()),
-               "spmm_csr")
+    if long_min is None:
+        _lib.check(L().sl_spmm_csr_f64(nrows, ncols, K, P(pos), P(crd), P(vals), P(X), P(Y),
+                                       S()), "spmm_csr")
+        return Y
+    nnz = crd.numel()
+    ws = _ws(L().sl_spmm_csr_split_workspace_bytes(nrows, nnz, long_min), vals)
+    _lib.check(L().sl_spmm_csr_split_f64(nrows, ncols, K, nnz, P(pos), P(crd), P(vals), P(X),
+                                         P(Y), long_min, P(ws), 0 if ws is None else ws.numel(),
+                                         S()), "spmm_csr")
     return Y
 
 

@@ -84,6 +84,31 @@ def test_spmm_ragged_rows_vs_oracle(orc):
     assert np.array_equal(bits(Y), bits(ref))
 
 
+@pytest.mark.parametrize("Kc", [1, 12, 32, 45])
+def test_spmm_long_row_split_vs_oracle(orc, Kc):
+    """power-law rows (up to ~20k nonzeros, empty rows) through the split path
+    (one CTA per row longer than long_min) for several thresholds, and
+    through evaluate(), which takes it when a row exceeds 1024 nonzeros"""
+    rng = np.random.default_rng(30 + Kc)
+    n, m = 3000, 40_000
+    lens = np.minimum((rng.pareto(1.1, n) * 20).astype(np.int64), 20_000)
+    lens[::11] = 0
+    lens[5] = 20_000
+    pos = np.zeros(n + 1, np.int64)
+    np.cumsum(lens, out=pos[1:])
+    crd = np.concatenate([np.sort(rng.choice(m, k, replace=False)) for k in lens]).astype(np.int32)
+    vals = rng.uniform(-1, 1, len(crd))
+    X = rng.uniform(-1, 1, (m, Kc))
+    ref = orc.spmm_csr(n, Kc, pos.astype(np.int32), crd, vals, X, threads=0)
+    args = (cuda(pos, np.int32), cuda(crd, np.int32), cuda(vals, np.float64), cuda(X, np.float64))
+    for long_min in (0, 1, 7, 200, 1024, 10**9):
+        Y = K.spmm_csr(n, m, *args, long_min=long_min)
+        assert np.array_equal(bits(Y), bits(ref)), long_min
+    A = F.csr_storage(pos.astype(np.int32), crd, vals, (n, m))
+    Y2 = sl.evaluate("Y(i,k) = A(i,j) * X(j,k)", {"A": A, "X": F.dense_storage(X)})
+    assert np.array_equal(bits(Y2.vals), bits(ref))
+
+
 @pytest.mark.parametrize("frac", [0.0, 0.01, 0.3, 1.0])
 def test_spmv_spx_vs_oracle(orc, frac):
     d = wl.coo_spmv(n=50_000, nnz=500_000, seed=12)
