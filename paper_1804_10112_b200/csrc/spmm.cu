@@ -84,20 +84,20 @@ spmm_csr_kernel(int64_t nrows, int64_t K, const int32_t* __restrict__ pos,
 // row.  A lone group walking a power-law row keeps only kB gathers in flight
 // per lane, so a 10^5-nonzero row costs ~10^5/kB dependent gather latencies.
 // Here all eight warps gather a chunk of the row's X rows — a warp covers
-// 32/G nonzeros x G columns per step, kPer steps with every load issued
-// before the first use — and form the products A(i,j)*X(j,k) in shared
+// 32/G nonzeros x G columns per step, kPer steps — and form the products A(i,j)*X(j,k) in shared
 // memory; then warp 0 (lane l < G owning column k0 + l) adds them in storage
 // order.  dadd(acc, dmul(a, x)) in the same order as the group kernel:
 // bit-identical.  The add chain (one dependent dadd per nonzero per column)
 // is the floor the ordered sum imposes.
-template <int G>
+template <int G, int kPer>
 __global__ void __launch_bounds__(256)
 spmm_long_rows_kernel(int64_t K, const int32_t* __restrict__ pos, const int32_t* __restrict__ crd,
                       const double* __restrict__ vals, const double* __restrict__ X,
                       double* __restrict__ Y, const int32_t* __restrict__ list,
                       const int32_t* __restrict__ count) {
-  constexpr int kPer = 16, kRows = 32 / G, kChunk = 8 * kRows * kPer;
-  __shared__ double P[kChunk][G + 1];   // +1: conflict-free column reads by warp 0
+  constexpr int kRows = 32 / G, kChunk = 8 * kRows * kPer;
+  extern __shared__ double smem_p[];
+  double(*P)[G + 1] = reinterpret_cast<double(*)[G + 1]>(smem_p);  // +1: conflict-free columns
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int gl = lane % G, gr = lane / G;
   const int n = *count;
@@ -224,13 +224,20 @@ extern "C" int sl_spmm_csr_split_f64(int64_t nrows, int64_t ncols, int64_t K, in
   if (rc != SL_OK) return rc;
   const int64_t nlong = std::min<int64_t>(nrows, nnz / ((int64_t)long_min + 1) + 1);
   const int lgrid = (int)std::min<int64_t>(nlong, 4LL * sl_host::sm_count());
-  if (K > 16)
-    spmm_long_rows_kernel<32><<<lgrid, 256, 0, s>>>(K, pos, crd, vals, X, Y, list, count);
-  else if (K > 8)
-    spmm_long_rows_kernel<16><<<lgrid, 256, 0, s>>>(K, pos, crd, vals, X, Y, list, count);
-  else if (K > 4)
-    spmm_long_rows_kernel<8><<<lgrid, 256, 0, s>>>(K, pos, crd, vals, X, Y, list, count);
-  else
-    spmm_long_rows_kernel<4><<<lgrid, 256, 0, s>>>(K, pos, crd, vals, X, Y, list, count);
+  // chunk depth: 32 loads per lane for G <= 16, 24 for G = 32 (the giant-row
+  // time is per-chunk gather latency; tools/spmm_skew_prof.py,
+  // profiles/ab/r1_spmm_skew_split.txt)
+  auto go = [&](auto kern, int g, int per) {
+    const size_t smem = (size_t)8 * (32 / g) * per * (g + 1) * sizeof(double);
+    if (smem > 48 * 1024 &&
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+            cudaSuccess)
+      return;
+    kern<<<lgrid, 256, smem, s>>>(K, pos, crd, vals, X, Y, list, count);
+  };
+  if (K > 16) go(spmm_long_rows_kernel<32, 24>, 32, 24);
+  else if (K > 8) go(spmm_long_rows_kernel<16, 32>, 16, 32);
+  else if (K > 4) go(spmm_long_rows_kernel<8, 32>, 8, 32);
+  else go(spmm_long_rows_kernel<4, 32>, 4, 32);
   return sl_host::launch_status();
 }
