@@ -427,7 +427,8 @@ def _run(p: Plan, inputs: Dict[str, TensorStorage], stats: Optional[EvalStats]):
         else:
             U = ops["U"]
             R = U.dims[1]
-            Y = K.ttm_csf(*args, U.vals.view(Kd, R))
+            long_min = _SPMM_LONG_ROW if _row_stats(lv[2])[1] > _SPMM_LONG_ROW else None
+            Y = K.ttm_csf(*args, U.vals.view(Kd, R), long_min=long_min)
             out = TensorStorage(f, (I, J, R), [LevelStorage(f.levels[0], n=I, device=dev),
                                                LevelStorage(f.levels[1], n=J, device=dev),
                                                LevelStorage(f.levels[2], n=R, device=dev)],

@@ -184,15 +184,16 @@ def ttv_csf(I, J, K, crd0, pos1, crd1, pos2, crd2, vals, v, out="dense"):
     return Y
 
 
-def ttm_csf(I, J, K, crd0, pos1, crd1, pos2, crd2, vals, U):
-    """TTM over a CSF tensor: Y (I, J, R) dense."""
+def ttm_csf(I, J, K, crd0, pos1, crd1, pos2, crd2, vals, U, long_min=None):
+    """TTM over a CSF tensor: Y (I, J, R) dense.  `long_min`: fibres longer
+    than it take the SpMM long-row split (same results)."""
     crd0, pos1, crd1, pos2, crd2, vals = _fibers(crd0, pos1, crd1, pos2, crd2, vals)
     U = _t(U, F64, "U")
     R = U.shape[-1]
     nf = crd1.numel()
     rows = torch.empty((nf, R), dtype=F64, device=vals.device)
     if nf:
-        spmm_csr(nf, K, pos2, crd2, vals, U.view(K, R), rows)
+        spmm_csr(nf, K, pos2, crd2, vals, U.view(K, R), rows, long_min=long_min)
     Y = torch.empty((I, J, R), dtype=F64, device=vals.device)
     _lib.check(L().sl_csf_fiber_scatter_f64(I, J, R, crd0.numel(), nf, P(crd0), P(pos1), P(crd1),
                                             P(rows), P(Y), S()), "csf_fiber_scatter")

@@ -189,6 +189,9 @@ def test_tensor3_full_vs_oracle(orc):
     rows = orc.ttm_csf(csf, t["vals"], U)
     Y3 = K.ttm_csf(*args, cuda(U, np.float64)).cpu().numpy().reshape(I * J, 16)
     assert np.array_equal(bits(Y3[fi * J + fj]), bits(rows))
+    for long_min in (0, 2):        # every / most fibres through the SpMM long-row split
+        Y4 = K.ttm_csf(*args, cuda(U, np.float64), long_min=long_min).cpu().numpy()
+        assert np.array_equal(bits(Y4.reshape(I * J, 16)[fi * J + fj]), bits(rows)), long_min
     # inner product with a perturbed copy of the pattern
     keep = rng.random(len(t["i"])) < 0.5
     z = {"i": t["i"][keep], "j": t["j"][keep], "k": t["k"][keep],
