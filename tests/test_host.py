@@ -257,3 +257,28 @@ def test_generators_hit_exact_sizes():
     m = wl.mttkrp(I=100, J=80, K=60, nnz=5000, R=4, seed=3)
     key = (m["i"].astype(np.int64) * 80 + m["j"]) * 60 + m["k"]
     assert len(key) == 5000 and (np.diff(key) > 0).all() and (m["vals"] > 0).all()
+
+
+def test_plan_cache_identity_fast_path(monkeypatch):
+    """evaluate()'s identity plan cache: a repeated call with the same format
+    objects reuses the plan; other dims, other formats (equal or not) and an
+    explicit out_format plan correctly (no GPU: _run is stubbed to return the
+    plan)."""
+    monkeypatch.setattr(Eng, "_run", lambda p, inputs, stats: p)
+    Eng._FAST_CACHE.clear()
+    pos, crd, vals = np.array([0, 1, 2], np.int32), np.array([0, 1], np.int32), np.ones(2)
+    A = F.csr_storage(pos, crd, vals, (2, 2), device=None)
+    x = F.dense_storage(np.ones(2), device=None)
+    expr = "y(i) = A(i,j) * x(j)"
+    p1 = Eng.evaluate(expr, {"A": A, "x": x})
+    assert p1.kernel == "spmv_csr" and len(Eng._FAST_CACHE) == 1
+    assert Eng.evaluate(expr, {"A": A, "x": x}) is p1             # identity hit
+    A3 = F.csr_storage(np.array([0, 1, 2, 2], np.int32), crd, vals, (3, 2), device=None)
+    p3 = Eng.evaluate(expr, {"A": A3, "x": x})
+    assert p3 is not p1 and p3.out_dims == (3,)                 # dims are part of the key
+    C = F.coo_storage(np.array([0, 1], np.int32), crd, vals, (2, 2), device=None)
+    assert Eng.evaluate(expr, {"A": C, "x": x}).kernel == "spmv_coo"
+    hv = F.preset("hash-vector")
+    ph = Eng.evaluate(expr, {"A": A, "x": x}, out_format=hv)
+    assert ph.out_format is hv and ph is not p1
+    assert Eng.evaluate(expr, {"A": A, "x": x}) is p1
