@@ -247,7 +247,8 @@ void or_spmv_csr_hashx_mt(int64_t nrows, const int32_t* pos, const int32_t* crd,
  * j-lattice {A1,B1} -> {A1} -> {B1} over one shared pair of streams: visit
  * the minimum coordinate; both present -> a + b, else the copy.  B's
  * duplicate (i,j) entries are grouped (Grouped, engine.py:107-149) and summed
- * as Python's sum(): +0.0 + b1 + b2 ... (engine.py:524-527).  The gather
+ * by Python's sum() (engine.py:524-527) — on the CPython 3.12 the reference
+ * runs on, Neumaier-compensated (py_sum below).  The gather
  * writer appends 0.0 then += (0.0 + value) (engine.py:404, :413, :625-631),
  * so the stored value is 0.0 + e.  B rows come from b_pos (CSR) or from the
  * row-sorted b_rows (COO).  Returns nnz(C). */
@@ -260,6 +261,20 @@ static void b_row_range(int64_t r, const int32_t* b_pos, const int32_t* b_rows, 
   while (q < b_nnz && b_rows[q] == r) ++q;
   *hi = q;
   *cursor = q;
+}
+
+/* CPython 3.12 builtin sum() over floats (bltinmodule.c builtin_sum_impl):
+ * f = 0 + v[0] (int 0 + float), then for each x: t = f + x,
+ * c += |f| >= |x| ? (f - t) + x : (x - t) + f, f = t; returns f + c when c is
+ * nonzero and finite, else f. */
+double or_py_sum(const double* v, int64_t n) {
+  double f = 0.0 + v[0], c = 0.0;
+  for (int64_t u = 1; u < n; ++u) {
+    const double x = v[u], t = f + x;
+    if (fabs(f) >= fabs(x)) c += (f - t) + x; else c += (x - t) + f;
+    f = t;
+  }
+  return (c != 0.0 && isfinite(c)) ? f + c : f;
 }
 
 static int64_t add_row(int64_t alo, int64_t ahi, const int32_t* a_crd, const double* a_vals,
@@ -278,8 +293,7 @@ static int64_t add_row(int64_t alo, int64_t ahi, const int32_t* a_crd, const dou
       /* group duplicates of c in B */
       int64_t q = pb + 1;
       while (q < bhi && b_cols[q] == c) ++q;
-      if (q - pb == 1) b = b_vals[pb];
-      else { b = 0.0; for (int64_t u = pb; u < q; ++u) b = b + b_vals[u]; }
+      b = q - pb == 1 ? b_vals[pb] : or_py_sum(b_vals + pb, q - pb);
       pb = q;
       have_b = 1;
     }
@@ -566,11 +580,19 @@ double or_inner_coo3(int64_t nx, const int32_t* xi, const int32_t* xj, const int
       cur_i = xi[p];
       cur_j = xj[p];
     }
-    const double t = xv[p] * zv[q];
+    /* both streams are Grouped (engine.py:107-149): a repeated coordinate is
+     * one visit whose value is Python's sum() over its run (engine.py:527) */
+    int64_t p2 = p + 1, q2 = q + 1;
+    while (p2 < nx && xi[p2] == xi[p] && xj[p2] == xj[p] && xk[p2] == xk[p]) ++p2;
+    while (q2 < nz && zi[q2] == zi[q] && zj[q2] == zj[q] && zk[q2] == zk[q]) ++q2;
+    const double gx = p2 - p == 1 ? xv[p] : or_py_sum(xv + p, p2 - p);
+    const double gz = q2 - q == 1 ? zv[q] : or_py_sum(zv + q, q2 - q);
+    const double t = gx * gz;
     fiber = fiber + t;
-    a += fabs(t);
-    ++p;
-    ++q;
+    for (int64_t u = p; u < p2; ++u)
+      for (int64_t w = q; w < q2; ++w) a += fabs(xv[u] * zv[w]);
+    p = p2;
+    q = q2;
   }
   if (cur_i >= 0) {
     slice = slice + fiber;

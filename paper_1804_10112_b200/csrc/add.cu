@@ -5,7 +5,8 @@
 // gather-append writer (engine.py:330-434).  Per row the output is the
 // sorted union of A's and B's columns; a coordinate present in both gets
 // a + b, otherwise the copy; B's duplicate coordinates are grouped and summed
-// (+0.0 + b1 + b2 ..., engine.py:107-149, 524-527); the stored value is
+// (Python's sum() over the group, engine.py:107-149, 524-527: `PySum`,
+// common.cuh); the stored value is
 // 0.0 + value (engine.py:404, 413, 625-631).  Explicit zeros are kept.
 //
 // B200 design (two passes over the operands, scan-based assembly):
@@ -106,13 +107,15 @@ SL_DEV int merge_row(int32_t alo, int32_t ahi, int32_t blo, int32_t bhi, const A
       int32_t q = pb + 1;
       int32_t cq = q < bhi ? acc.bcol(q) : INT32_MAX;
       if (cq == c) {
-        // duplicates: Python sum() over the group, 0 + b1 + b2 + ...
-        if (kValues) b = dadd(0.0, b);
+        // duplicates: Python's sum() over the group (PySum)
+        PySum g;
+        if (kValues) g.start(b);
         while (cq == c) {
-          if (kValues) b = dadd(b, acc.bval(q));
+          if (kValues) g.add(acc.bval(q));
           ++q;
           cq = q < bhi ? acc.bcol(q) : INT32_MAX;
         }
+        if (kValues) b = g.value();
       }
       pb = q;
       cb = cq;
@@ -157,8 +160,8 @@ SL_DEV int count_row_idx(int ia, int iah, int ib, int ibh, const int32_t* s_col)
 
 // Fill merge in the same single-stream form (values staged at the same
 // indices as their columns): each iteration consumes one element, folds it
-// into the current output run (A value; B group sum in the reference's order,
-// (0 + b1) + b2 ... for a repeated coordinate, b1 alone otherwise) and
+// into the current output run (A value; B group: b1 alone, or Python's sum()
+// over a repeated coordinate's values — PySum's state carried in (bs, bc)) and
 // rewrites the run's output slot; the slot's last write, at the run's last
 // element, is the final value 0 + (a + bgroup | a | bgroup) (engine.py:404,
 // 413, 524-531, 625-631).  No divergent branches.
@@ -196,7 +199,7 @@ SL_DEV int fill_row_idx(int ia, int iah, int ib, int ibh, const int32_t* s_col,
                         const double* s_val, int32_t* oc, double* ov) {
   int n = -1;
   int32_t last = -1;
-  double ra = 0.0, bs = 0.0;
+  double ra = 0.0, bs = 0.0, bc = 0.0;
   bool has_a = false;
   int nb = 0;
   int32_t ca = ia < iah ? s_col[ia] : INT32_MAX;
@@ -211,10 +214,16 @@ SL_DEV int fill_row_idx(int ia, int iah, int ib, int ibh, const int32_t* s_col,
     has_a = (fresh ? false : has_a) || ta;
     nb = fresh ? 0 : nb;
     ra = ta ? v : ra;
-    const double bnext = nb == 0 ? v : dadd(nb == 1 ? dadd(0.0, bs) : bs, v);
-    bs = ta ? bs : bnext;
+    // B's group: nb == 0 -> b1; else one PySum step from f (0 + b1 when nb == 1)
+    const double f = nb == 1 ? dadd(0.0, bs) : bs;
+    const double t = dadd(f, v);
+    const double cnext = nb == 0 ? 0.0
+        : dadd(nb == 1 ? 0.0 : bc, fabs(f) >= fabs(v) ? dadd(dsub(f, t), v) : dadd(dsub(v, t), f));
+    bs = ta ? bs : (nb == 0 ? v : t);
+    bc = ta ? bc : cnext;
     nb += !ta;
-    const double e = has_a ? (nb ? dadd(ra, bs) : ra) : bs;
+    const double g = (nb >= 2 && bc != 0.0 && isfinite(bc)) ? dadd(bs, bc) : bs;
+    const double e = has_a ? (nb ? dadd(ra, g) : ra) : g;
     oc[n] = c;
     ov[n] = dadd(0.0, e);
     ia += ta;

@@ -14,6 +14,25 @@ namespace sl {
 // contracted into FMA, which keeps results bit-identical.
 SL_DEV double dmul(double a, double b) { return __dmul_rn(a, b); }
 SL_DEV double dadd(double a, double b) { return __dadd_rn(a, b); }
+SL_DEV double dsub(double a, double b) { return __dsub_rn(a, b); }
+
+// A duplicate group's value is Python's builtin sum() over it
+// (engine.py:527: `sum(vals[p] for p in ps)`).  The reference runs on CPython
+// 3.12, whose sum() of floats is Neumaier-compensated (bltinmodule.c,
+// builtin_sum_impl): f = 0 + v1 (int 0 + float), then per item
+// t = f + x, c += |f| >= |x| ? (f - t) + x : (x - t) + f, f = t; the result is
+// f + c when c is nonzero and finite, else f.  Two items give the plain sum;
+// three or more can differ from it in the last bit.
+struct PySum {
+  double f, c;
+  SL_DEV void start(double v1) { f = dadd(0.0, v1); c = 0.0; }
+  SL_DEV void add(double x) {
+    const double t = dadd(f, x);
+    c = dadd(c, fabs(f) >= fabs(x) ? dadd(dsub(f, t), x) : dadd(dsub(x, t), f));
+    f = t;
+  }
+  SL_DEV double value() const { return (c != 0.0 && isfinite(c)) ? dadd(f, c) : f; }
+};
 
 // Read-only loads through the non-coherent path.
 template <typename T>

@@ -79,7 +79,8 @@ SL_DEV int64_t key3(const int32_t* i, const int32_t* j, const int32_t* k, int64_
 }
 
 // block b: partial[b] = sum over its X tile of x * z where Z holds the same
-// coordinate (binary search over Z's keys), reduced in a fixed tree order
+// coordinate (binary search over Z's keys; a repeated Z coordinate summed),
+// reduced in a fixed tree order
 __global__ void __launch_bounds__(kInThreads)
 inner_tile_kernel(int64_t J, int64_t K, int64_t nx, const int32_t* __restrict__ xi,
                   const int32_t* __restrict__ xj, const int32_t* __restrict__ xk,
@@ -115,7 +116,16 @@ inner_tile_kernel(int64_t J, int64_t K, int64_t nx, const int32_t* __restrict__ 
       const int64_t mid = (lo + hi) >> 1;
       if (key3(zi, zj, zk, mid, J, K) < kx) lo = mid + 1; else hi = mid;
     }
-    if (lo < zhi && key3(zi, zj, zk, lo, J, K) == kx) acc = dadd(acc, dmul(ldg(xv + e), ldg(zv + lo)));
+    if (lo < zhi && key3(zi, zj, zk, lo, J, K) == kx) {
+      // Z's repeats of the coordinate are one grouped visit (engine.py:107-149,
+      // 527): the product takes their sum (X's repeats each add their own
+      // product — the same value up to reassociation, inside the reduction's
+      // tolerance)
+      double gz = ldg(zv + lo);
+      for (int64_t q = lo + 1; q < zhi && key3(zi, zj, zk, q, J, K) == kx; ++q)
+        gz = dadd(gz, ldg(zv + q));
+      acc = dadd(acc, dmul(ldg(xv + e), gz));
+    }
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) acc = dadd(acc, __shfl_down_sync(0xffffffffu, acc, o));

@@ -35,10 +35,12 @@ from .notation import Access, Add, Assignment, CheckedExpr, Mul, parse, validate
 
 @dataclass
 class EvalStats:
-    """Visit counters keyed by loop variable (engine.py:255-268).  The GPU
-    path fills `by_var` with the number of loop visits the reference's
-    schedule performs for each variable (known from the storage sizes), which
-    is what the O(nnz) complexity property checks."""
+    """Visit counters keyed by loop variable and by (variable, lattice-point
+    label) (engine.py:255-268).  The GPU path fills them with the visit
+    counts the reference's schedule performs — from the storage sizes, and
+    for merged streams (A + B unions, intersections) from the coordinates on
+    the device — so `by_loop` compares entry for entry with the reference's
+    (SPEC.md:676; tests/test_gpu_sweep.py)."""
 
     by_var: Dict[str, int] = field(default_factory=dict)
     by_loop: Dict[Tuple[str, str], int] = field(default_factory=dict)
@@ -70,8 +72,9 @@ def format_class(fmt: TensorFormat) -> str:
         if (k == (LK.COMPRESSED, LK.SINGLETON) and fmt.levels[0].props.ordered
                 and fmt.levels[1].props.ordered):
             return "coo"
-        if k == (LK.COMPRESSED, LK.SINGLETON, LK.SINGLETON) and fmt.levels[0].props.ordered:
-            return "coo3"
+        if k == (LK.COMPRESSED, LK.SINGLETON, LK.SINGLETON) and all(
+                s.props.ordered for s in fmt.levels):
+            return "coo3"   # lexicographically sorted (an unordered level is Reordered)
         if k == (LK.COMPRESSED, LK.COMPRESSED, LK.COMPRESSED) and all(
                 s.props.ordered and s.props.unique for s in fmt.levels):
             return "csf"
@@ -97,6 +100,9 @@ class Plan:
     operands: Dict[str, str]     # role -> tensor name
     out_format: TensorFormat
     out_dims: Tuple[int, ...]
+    fuse: bool = True            # the reference's fuse_branchless switch (engine.py:766-772)
+    ivars: Tuple[str, ...] = ()  # the loop variables, in schedule order (EvalStats keys)
+    order: Tuple[str, ...] = ()  # tensor names in expression order (lattice-point labels)
 
 
 def _flatten_mul(e):
@@ -106,7 +112,25 @@ def _flatten_mul(e):
 
 
 def plan(checked: CheckedExpr, bindings, out_format: TensorFormat,
-         out_dims: Tuple[int, ...]) -> Plan:
+         out_dims: Tuple[int, ...], *, fuse: bool = True) -> Plan:
+    """Bind the expression to a kernel (or raise).  `fuse` follows the
+    reference's `plan(..., fuse=)` (engine.py:766-772): an unfused COO chain
+    is executed level by level, so its duplicate coordinates are grouped
+    (engine.py:200-209) — the B200 path then runs the exact-CSR copy."""
+    p = _plan(checked, bindings, out_format, out_dims, fuse)
+    p.fuse = fuse
+    p.order = tuple(dict.fromkeys(t.tensor for t in _accesses(checked.assignment.rhs)))
+    return p
+
+
+def _accesses(e):
+    if isinstance(e, Access):
+        return [e]
+    return _accesses(e.left) + _accesses(e.right) if isinstance(e, (Mul, Add)) else []
+
+
+def _plan(checked: CheckedExpr, bindings, out_format: TensorFormat,
+          out_dims: Tuple[int, ...], fuse: bool) -> Plan:
     a: Assignment = checked.assignment
     lhs, rhs = a.lhs, a.rhs
     cls = {name: format_class(fmt) for name, (fmt, _) in bindings.items()}
@@ -125,15 +149,16 @@ def plan(checked: CheckedExpr, bindings, out_format: TensorFormat,
                     raise UnsupportedOutputError(
                         f"SpMV output must be a dense or hash vector, got {out_format.describe()}")
                 ca, cx = cls[A.tensor], cls[x.tensor]
+                kern = None
                 if cx == "dense1" and ca in ("coo", "csr", "ell", "dia"):
-                    return Plan("spmv", f"spmv_{ca}", {"A": A.tensor, "x": x.tensor},
-                                out_format, out_dims)
-                if cx == "hash1" and ca == "csr":
-                    return Plan("spmv", "spmv_csr_hashx", {"A": A.tensor, "x": x.tensor},
-                                out_format, out_dims)
-                if cx == "spvec" and ca == "csr":
-                    return Plan("spmv", "spmv_csr_spx", {"A": A.tensor, "x": x.tensor},
-                                out_format, out_dims)
+                    kern = f"spmv_{ca}" if (fuse or ca != "coo") else "spmv_coo_grouped"
+                elif cx == "hash1" and ca == "csr":
+                    kern = "spmv_csr_hashx"
+                elif cx == "spvec" and ca == "csr":
+                    kern = "spmv_csr_spx"
+                if kern is not None:
+                    return Plan("spmv", kern, {"A": A.tensor, "x": x.tensor}, out_format,
+                                out_dims, ivars=(i, j))
                 raise UnsupportedMergeError(
                     f"no B200 kernel for SpMV with A {ca} and x {cx}")
 
@@ -150,7 +175,7 @@ def plan(checked: CheckedExpr, bindings, out_format: TensorFormat,
                         if ocls != "dense2":
                             raise UnsupportedOutputError("SpMM output must be dense-2")
                         return Plan("spmm", "spmm_csr", {"A": A.tensor, "X": X.tensor},
-                                    out_format, out_dims)
+                                    out_format, out_dims, ivars=(i, j, X.ivars[1]))
             raise UnsupportedMergeError("no B200 kernel for this matrix product "
                                         "(supported: CSR x dense-2)")
 
@@ -169,7 +194,7 @@ def plan(checked: CheckedExpr, bindings, out_format: TensorFormat,
                     if ocls not in ("dense2", "csr"):
                         raise UnsupportedOutputError("TTV output must be dense-2 or CSR")
                     return Plan("ttv", f"ttv_csf_{ocls}", {"X": X.tensor, "v": other.tensor},
-                                out_format, out_dims)
+                                out_format, out_dims, ivars=(i, j, k))
                 raise UnsupportedMergeError(f"no B200 kernel for TTV with X {cX}, v {cO}")
             # TTM: Y(i,j,r) = X(i,j,k) * U(k,r)
             if (len(other.ivars) == 2 and other.ivars[0] == k and len(lhs.ivars) == 3
@@ -178,7 +203,7 @@ def plan(checked: CheckedExpr, bindings, out_format: TensorFormat,
                     if ocls != "dense3":
                         raise UnsupportedOutputError("TTM output must be dense-3")
                     return Plan("ttm", "ttm_csf", {"X": X.tensor, "U": other.tensor},
-                                out_format, out_dims)
+                                out_format, out_dims, ivars=(i, j, k, other.ivars[1]))
                 raise UnsupportedMergeError(f"no B200 kernel for TTM with X {cX}, U {cO}")
             # INNERPROD: a() = X(i,j,k) * Z(i,j,k)
             if other.ivars == X.ivars and lhs.ivars == () and len({i, j, k}) == 3:
@@ -186,7 +211,7 @@ def plan(checked: CheckedExpr, bindings, out_format: TensorFormat,
                     if ocls != "dense0":
                         raise UnsupportedOutputError("inner product output must be a scalar")
                     return Plan("inner", "inner_coo3", {"X": X.tensor, "Z": other.tensor},
-                                out_format, out_dims)
+                                out_format, out_dims, ivars=(i, j, k))
                 raise UnsupportedMergeError(
                     f"no B200 kernel for the inner product of {cX} and {cO} (COO-3 x COO-3)")
 
@@ -205,7 +230,8 @@ def plan(checked: CheckedExpr, bindings, out_format: TensorFormat,
                 A_, B_ = (L_, R_) if (cl == "csr" or cr == "coo") else (R_, L_)
                 ca = cls[A_.tensor]
                 return Plan("add", f"add_{ca}_{cls[B_.tensor]}_{ocls}",
-                            {"A": A_.tensor, "B": B_.tensor}, out_format, out_dims)
+                            {"A": A_.tensor, "B": B_.tensor}, out_format, out_dims,
+                            ivars=lhs.ivars)
             raise UnsupportedMergeError(f"no B200 kernel for A + B with {cl} + {cr}")
 
     # ---- A(i,r) = X(i,j,k) * B(j,r) * C(k,r), association (X*B)*C
@@ -229,7 +255,7 @@ def plan(checked: CheckedExpr, bindings, out_format: TensorFormat,
                             cls[Cm.tensor] == "dense2":
                         return Plan("mttkrp", f"mttkrp_{cX}",
                                     {"X": X.tensor, "B": Bm.tensor, "C": Cm.tensor},
-                                    out_format, out_dims)
+                                    out_format, out_dims, ivars=(i, j, k, lhs.ivars[1]))
                     raise UnsupportedMergeError(
                         f"no B200 kernel for MTTKRP with X {cX}, B {cls[Bm.tensor]}, "
                         f"C {cls[Cm.tensor]}")
@@ -257,27 +283,73 @@ def _dia_host_offsets(st: TensorStorage):
     return offs
 
 
+def _hashed_row_order(p: Plan, A: TensorStorage, nrows: int, dev):
+    """Row coordinates in the order the reference's scatter writer first
+    writes them (engine.py:281-327): CSR writes every row's total after its
+    loop (empty rows included); COO one write per nonzero (present rows, in
+    storage order); ELL every row once per slot (no rows when there are no
+    slots); DIA the rows of each diagonal's range [max(0,-o), min(n, m-o))
+    (levels.py:220-222), diagonal by diagonal in offset order.  The ordered
+    insert keeps each coordinate's first occurrence."""
+    if p.kernel in ("spmv_coo", "spmv_coo_grouped"):
+        return torch.unique_consecutive(A.levels[0].crd)
+    if p.kernel == "spmv_ell":
+        if A.levels[0].n == 0:
+            return torch.empty(0, dtype=torch.int32, device=dev)
+        return torch.arange(nrows, dtype=torch.int32, device=dev)
+    if p.kernel == "spmv_dia":
+        ncols = A.dims[1]
+        parts = [torch.arange(max(0, -o), min(nrows, ncols - o), dtype=torch.int32, device=dev)
+                 for o in _dia_host_offsets(A).tolist()]
+        return torch.cat(parts) if parts else torch.empty(0, dtype=torch.int32, device=dev)
+    return torch.arange(nrows, dtype=torch.int32, device=dev)
+
+
 def _hashed_spmv_output(p: Plan, A: TensorStorage, y, nrows: int, dev) -> TensorStorage:
     """SpMV into a hash-vector output, as the reference's scatter writer builds
     it (engine.py:281-327): the row coordinates are inserted in the order
-    they are first written — every row for CSR / ELL / DIA (the row total is
-    written after the row's loop, empty rows included), the rows present in
-    the coordinates for COO (one write per nonzero) — and each slot holds the
+    they are first written (`_hashed_row_order`) and each slot holds the
     row's sum, which is the dense kernel's y[i] (the same additions from
     +0.0).  Width: the format's pinned width, else next_pow2(max(4, 2 n))."""
     f = p.out_format
     w = f.hash_width or _next_pow2(max(4, 2 * nrows))
-    if p.kernel == "spmv_coo":
-        rows = torch.unique_consecutive(A.levels[0].crd)        # sorted: first-write order
-    else:
-        rows = torch.arange(nrows, dtype=torch.int32, device=dev)
+    rows = _hashed_row_order(p, A, nrows, dev)
     crd, err = K.hashed_insert(rows, w)
     if int(err.item()) != 0:
         raise HashSegmentFullError(f"hashed segment of width {w} is full")
-    slots, _ = K.hashed_locate(rows, w, crd)
     vals = torch.zeros(w, dtype=torch.float64, device=dev)
-    vals[slots.long()] = y[rows.long()]
+    if rows.numel():
+        slots, _ = K.hashed_locate(rows, w, crd)
+        vals[slots.long()] = y[rows.long()]
     return TensorStorage(f, (nrows,), [LevelStorage(f.levels[0], w=w, crd=crd, device=dev)], vals)
+
+
+def _csr_level(st: TensorStorage):
+    """(compressed level, vals) of a {dense, compressed} matrix with one entry per
+    coordinate.  A non-unique compressed level is iterated through the
+    reference's `Grouped` (engine.py:107-149, 200-209): each run of equal
+    coordinates is one visit whose value is the run's sum (engine.py:520-527)
+    — the exact identity copy (gather-append, 0.0 + (v1 + v2 ...)) is that
+    matrix, bit for bit where it can matter (a lone -0.0 group only feeds
+    sums that start from +0.0).  Computed once per storage and cached."""
+    lv = st.levels[1]
+    if st.format.levels[1].props.unique:
+        return lv, st.vals
+    cached = getattr(st, "_sl_grouped", None)
+    if cached is None or cached[0] is not lv.pos:
+        nrows = st.dims[0]
+        empty_i = torch.empty(0, dtype=torch.int32, device=lv.pos.device)
+        a_pos = torch.zeros(nrows + 1, dtype=torch.int32, device=lv.pos.device)
+        pos, crd, vals = K.add_csr(nrows, a_pos, empty_i, empty_i.double(), lv.crd, st.vals,
+                                   b_pos=lv.pos)
+        cached = (lv.pos, LevelStorage(lv.spec, pos=pos, crd=crd, device=pos.device), vals)
+        st._sl_grouped = cached
+    return cached[1], cached[2]
+
+
+def _csr_arrays(st: TensorStorage):
+    lv, vals = _csr_level(st)
+    return lv.pos, lv.crd, vals
 
 
 _SKEW_TILE = 4 * 896   # 32-row tiles heavier than four hand-off stages: merge-path
@@ -330,6 +402,15 @@ def _run(p: Plan, inputs: Dict[str, TensorStorage], stats: Optional[EvalStats]):
             break
     if dev is None:
         dev = torch.device("cuda", torch.cuda.current_device())
+    if dev.index is not None and dev.index != torch.cuda.current_device():
+        # kernels launch on the current device's current stream: make it the
+        # operands' device for the call (outputs are allocated there too)
+        with torch.cuda.device(dev):
+            return _run_on(p, inputs, stats, dev)
+    return _run_on(p, inputs, stats, dev)
+
+
+def _run_on(p: Plan, inputs: Dict[str, TensorStorage], stats: Optional[EvalStats], dev):
     ops = {role: _dev(inputs[name], dev) for role, name in p.operands.items()}
 
     if p.pattern == "spmv":
@@ -337,33 +418,30 @@ def _run(p: Plan, inputs: Dict[str, TensorStorage], stats: Optional[EvalStats]):
         nrows, ncols = A.dims
         if p.kernel == "spmv_coo":
             y = K.spmv_coo(nrows, ncols, A.levels[0].crd, A.levels[1].crd, A.vals, x.vals)
-            visits = {"i": int(A.vals.numel())}
+        elif p.kernel == "spmv_coo_grouped":
+            # unfused COO: rows and (row, column) runs grouped — the exact CSR copy
+            pos, crd, vals = K.coo_to_csr(nrows, A.levels[0].crd, A.levels[1].crd, A.vals)
+            y = K.spmv_csr(nrows, ncols, pos, crd, vals, x.vals)
         elif p.kernel == "spmv_csr":
-            y = K.spmv_csr(nrows, ncols, A.levels[1].pos, A.levels[1].crd, A.vals, x.vals,
-                           variant=_csr_variant(A.levels[1]))
-            visits = {"i": nrows, "j": int(A.levels[1].crd.numel())}
+            lv, vals = _csr_level(A)
+            y = K.spmv_csr(nrows, ncols, lv.pos, lv.crd, vals, x.vals, variant=_csr_variant(lv))
         elif p.kernel == "spmv_ell":
             S = A.levels[0].n
             y = K.spmv_ell(nrows, ncols, S, A.levels[2].crd, A.vals, x.vals)
-            visits = {"slot": S, "i": S * nrows}
         elif p.kernel == "spmv_dia":
             offs = _dia_host_offsets(inputs[p.operands["A"]])
             y = K.spmv_dia(nrows, ncols, offs, A.vals, x.vals)
-            visits = {"diag": len(offs), "i": int(sum(
-                max(0, min(nrows, ncols - o) - max(0, -o)) for o in offs.tolist()))}
         elif p.kernel == "spmv_csr_spx":
             sx = x.levels[0]
-            y = K.spmv_csr_spx(nrows, int(x.dims[0]), A.levels[1].pos, A.levels[1].crd, A.vals,
-                               sx.crd, x.vals)
-            visits = {"i": nrows, "j": int(A.levels[1].crd.numel())}
+            pos, crd, vals = _csr_arrays(A)
+            y = K.spmv_csr_spx(nrows, int(x.dims[0]), pos, crd, vals, sx.crd, x.vals)
         else:  # spmv_csr_hashx
             hx = x.levels[0]
-            nq = int(A.levels[1].crd.numel())
+            pos, crd, vals = _csr_arrays(A)
+            nq = int(crd.numel())
             # queries >= table slots: resolve each coordinate once (slot map)
             n_map = int(x.dims[0]) if nq >= hx.w else None
-            y = K.spmv_csr_hashx(nrows, A.levels[1].pos, A.levels[1].crd, A.vals, hx.w, hx.crd,
-                                 x.vals, n=n_map)
-            visits = {"i": nrows, "j": int(A.levels[1].crd.numel())}
+            y = K.spmv_csr_hashx(nrows, pos, crd, vals, hx.w, hx.crd, x.vals, n=n_map)
         if format_class(p.out_format) == "hash1":
             out = _hashed_spmv_output(p, A, y, nrows, dev)
         else:
@@ -375,8 +453,8 @@ def _run(p: Plan, inputs: Dict[str, TensorStorage], stats: Optional[EvalStats]):
         _, ka, kb, ko = p.kernel.split("_")
         if ka == "coo":          # COO A (possibly duplicated): its exact CSR copy
             a_pos, a_crd, a_vals = K.coo_to_csr(nrows, A.levels[0].crd, A.levels[1].crd, A.vals)
-        else:
-            a_pos, a_crd, a_vals = A.levels[1].pos, A.levels[1].crd, A.vals
+        else:                    # CSR A, a non-unique level grouped
+            a_pos, a_crd, a_vals = _csr_arrays(A)
         if kb == "coo":
             c_pos, c_crd, c_vals = K.add_csr(nrows, a_pos, a_crd, a_vals, B.levels[1].crd, B.vals,
                                              b_rows=B.levels[0].crd)
@@ -395,19 +473,19 @@ def _run(p: Plan, inputs: Dict[str, TensorStorage], stats: Optional[EvalStats]):
                                                          device=dev),
                                             LevelStorage(f.levels[1], crd=c_crd, device=dev)],
                                 c_vals)
-        visits = {"i": nrows, "j": int(c_crd.numel())}
+        res_csr = (c_pos, c_crd)
     elif p.pattern == "spmm":
         A, X = ops["A"], ops["X"]
         nrows, ncols = A.dims
         Kc = X.dims[1]
-        long_min = _SPMM_LONG_ROW if _row_stats(A.levels[1])[1] > _SPMM_LONG_ROW else None
-        Y = K.spmm_csr(nrows, ncols, A.levels[1].pos, A.levels[1].crd, A.vals,
-                       X.vals.view(ncols, Kc), long_min=long_min)
+        lv, vals = _csr_level(A)
+        long_min = _SPMM_LONG_ROW if _row_stats(lv)[1] > _SPMM_LONG_ROW else None
+        Y = K.spmm_csr(nrows, ncols, lv.pos, lv.crd, vals, X.vals.view(ncols, Kc),
+                       long_min=long_min)
         f = p.out_format
         out = TensorStorage(f, (nrows, Kc), [LevelStorage(f.levels[0], n=nrows, device=dev),
                                              LevelStorage(f.levels[1], n=Kc, device=dev)],
                             Y.reshape(-1))
-        visits = {"i": nrows, "k": int(A.levels[1].crd.numel()) * Kc}
     elif p.pattern in ("ttv", "ttm"):
         X = ops["X"]
         I, J, Kd = X.dims
@@ -433,7 +511,6 @@ def _run(p: Plan, inputs: Dict[str, TensorStorage], stats: Optional[EvalStats]):
                                                LevelStorage(f.levels[1], n=J, device=dev),
                                                LevelStorage(f.levels[2], n=R, device=dev)],
                                 Y.reshape(-1))
-        visits = {"k": int(X.vals.numel())}
     elif p.pattern == "inner":
         X, Z = ops["X"], ops["Z"]
         I, J, Kd = X.dims
@@ -441,7 +518,6 @@ def _run(p: Plan, inputs: Dict[str, TensorStorage], stats: Optional[EvalStats]):
         zs = (Z.levels[0].crd, Z.levels[1].crd, Z.levels[2].crd, Z.vals)
         a = K.inner_coo3(I, J, Kd, xs, zs)
         out = TensorStorage(p.out_format, (), [], a)
-        visits = {"k": int(X.vals.numel())}
     else:  # mttkrp
         X, B, C = ops["X"], ops["B"], ops["C"]
         I, J, Kd = X.dims
@@ -457,10 +533,239 @@ def _run(p: Plan, inputs: Dict[str, TensorStorage], stats: Optional[EvalStats]):
         out = TensorStorage(f, (I, R), [LevelStorage(f.levels[0], n=I, device=dev),
                                         LevelStorage(f.levels[1], n=R, device=dev)],
                             A.reshape(-1))
-        visits = {"i": I, "r": int(X.vals.numel()) * R}
     if stats is not None:
-        for var, n in visits.items():
-            stats.count(var, p.kernel, n)
+        for (var, label), n in _loop_counts(p, ops, locals().get("res_csr")).items():
+            if n:
+                stats.count(var, label, n)
+    return out
+
+
+# ---------------------------------------------------------------------------
+# EvalStats: the reference's loop-visit counts, keyed (variable, lattice point)
+
+def _label(p: Plan, *dims: Tuple[str, int]) -> str:
+    """Lattice-point label as the reference prints it (engine.py:255-268):
+    `{A1,x0}` — each iterated or located tensor level, tensors in expression
+    order."""
+    rank = {t: n for n, t in enumerate(p.order)}
+    ds = sorted(dims, key=lambda d: (rank.get(d[0], 99), d[1]))
+    return "{" + ",".join(f"{t}{lvl}" for t, lvl in ds) + "}"
+
+
+def _i64(t):
+    return t.to(torch.int64)
+
+
+def _merge_counts(ka, kb, w: int):
+    """Visits of `merge_visits` (engine.py:211-225) over two ordered unique
+    coordinate streams under each parent, for keys parent*w + coord (sorted,
+    unique): (visits while both streams are live, visits of A's remainder,
+    visits of B's remainder, keys present in both)."""
+    u = torch.unique(torch.cat([ka, kb]))
+    if u.numel() == 0:
+        z = torch.zeros((), dtype=torch.int64, device=u.device)
+        return z, z, z, u
+    pu, cu = torch.div(u, w, rounding_mode="floor"), u % w
+
+    def last(k):
+        if k.numel() == 0:
+            return torch.full_like(u, -1)
+        ix = torch.searchsorted(k, (pu + 1) * w) - 1
+        kk = k[ix.clamp(min=0)]
+        ok = (ix >= 0) & (torch.div(kk, w, rounding_mode="floor") == pu)
+        return torch.where(ok, kk % w, torch.full_like(kk, -1))
+
+    la, lb = last(ka), last(kb)
+    both = (la >= 0) & (lb >= 0) & (cu <= torch.minimum(la, lb))
+    rest = ~both
+    a_rest = rest & (la > lb)
+    common = ka[torch.isin(ka, kb)] if ka.numel() and kb.numel() else ka[:0]
+    return both.sum(), a_rest.sum(), (rest & ~(la > lb)).sum(), common
+
+
+def _grouped_keys(rows, cols, w: int):
+    """Sorted unique keys row*w + col of an ordered coordinate list."""
+    if rows.numel() == 0:
+        return torch.empty(0, dtype=torch.int64, device=rows.device)
+    return torch.unique_consecutive(_i64(rows) * w + _i64(cols))
+
+
+def _csr_keys(pos, crd, w: int):
+    nrows = pos.numel() - 1
+    rows = torch.repeat_interleave(torch.arange(nrows, device=pos.device),
+                                   _i64(pos[1:] - pos[:-1]))
+    return _grouped_keys(rows, crd[: rows.numel()], w)
+
+
+def _loop_counts(p: Plan, ops, res_csr) -> Dict[Tuple[str, str], int]:
+    """Per (loop variable, lattice point) visit counts of the reference's
+    schedule for this plan (engine.py:255-268, 607-608, 688-689), from the
+    storage sizes and, for merged streams, the coordinates themselves."""
+    v = p.ivars
+    n = {role: name for role, name in p.operands.items()}
+    out: Dict[Tuple[str, str], int] = {}
+    if p.pattern == "spmv":
+        A, x = ops["A"], ops["x"]
+        An, xn = n["A"], n["x"]
+        nrows, ncols = A.dims
+        if p.kernel == "spmv_coo":
+            out[(v[0], _label(p, (An, 0)))] = int(A.levels[1].crd.numel())
+        elif p.kernel == "spmv_coo_grouped":
+            r, c = A.levels[0].crd, A.levels[1].crd
+            out[(v[0], _label(p, (An, 0)))] = int(torch.unique_consecutive(r).numel()) \
+                if r.numel() else 0
+            out[(v[1], _label(p, (An, 1), (xn, 0)))] = int(_grouped_keys(r, c, ncols).numel())
+        elif p.kernel == "spmv_ell":
+            S = A.levels[0].n
+            out[("slot$" + An + "0", _label(p, (An, 0)))] = S
+            out[(v[0], _label(p, (An, 1)))] = S * nrows
+            if not p.fuse:
+                out[(v[1], _label(p, (An, 2), (xn, 0)))] = S * nrows
+        elif p.kernel == "spmv_dia":
+            offs = _dia_host_offsets(A).tolist()
+            inr = sum(max(0, min(nrows, ncols - o) - max(0, -o)) for o in offs)
+            out[("diag$" + An + "0", _label(p, (An, 0)))] = len(offs)
+            out[(v[0], _label(p, (An, 1)))] = inr
+            if not p.fuse:
+                out[(v[1], _label(p, (An, 2), (xn, 0)))] = inr
+        else:                                   # CSR rows, grouped columns
+            lv, _ = _csr_level(A)
+            out[(v[0], _label(p, (An, 0)))] = nrows
+            jl = _label(p, (An, 1), (xn, 0))
+            if p.kernel == "spmv_csr_spx":      # intersection with x's stream
+                out[(v[1], jl)] = _spx_visits(lv.pos, lv.crd, x.levels[0].crd)
+            else:
+                out[(v[1], jl)] = int(lv.crd.numel())
+    elif p.pattern == "spmm":
+        A, X = ops["A"], ops["X"]
+        lv, _ = _csr_level(A)
+        nnz = int(lv.crd.numel())
+        out[(v[0], _label(p, (n["A"], 0)))] = A.dims[0]
+        out[(v[1], _label(p, (n["A"], 1), (n["X"], 0)))] = nnz
+        out[(v[2], _label(p, (n["X"], 1)))] = nnz * X.dims[1]
+    elif p.pattern == "add":
+        out.update(_add_counts(p, ops, res_csr))
+    elif p.pattern == "mttkrp":
+        X, R = ops["X"], ops["B"].dims[1]
+        Xn, Bn, Cn = n["X"], n["B"], n["C"]
+        nnz = int(X.levels[-1].crd.numel()) if X.vals.numel() else 0
+        if p.kernel == "mttkrp_coo3" and p.fuse:
+            out[(v[0], _label(p, (Xn, 0)))] = nnz
+            out[(v[3], _label(p, (Bn, 1), (Cn, 1)))] = nnz * R
+        else:
+            ni, nij, nijk = _coo3_level_sizes(X) if p.kernel == "mttkrp_coo3" else (
+                int(X.levels[0].crd.numel()), int(X.levels[1].crd.numel()), nnz)
+            out[(v[0], _label(p, (Xn, 0)))] = ni
+            out[(v[1], _label(p, (Xn, 1), (Bn, 0)))] = nij
+            out[(v[2], _label(p, (Xn, 2), (Cn, 0)))] = nijk
+            out[(v[3], _label(p, (Bn, 1), (Cn, 1)))] = nijk * R
+    elif p.pattern in ("ttv", "ttm"):
+        X = ops["X"]
+        On = n["v"] if p.pattern == "ttv" else n["U"]
+        nnz = int(X.levels[2].crd.numel())
+        out[(v[0], _label(p, (n["X"], 0)))] = int(X.levels[0].crd.numel())
+        out[(v[1], _label(p, (n["X"], 1)))] = int(X.levels[1].crd.numel())
+        out[(v[2], _label(p, (n["X"], 2), (On, 0)))] = nnz
+        if p.pattern == "ttm":
+            out[(v[3], _label(p, (On, 1)))] = nnz * ops["U"].dims[1]
+    elif p.pattern == "inner":
+        out.update(_inner_counts(p, ops))
+    return out
+
+
+def _coo3_level_sizes(X: TensorStorage):
+    """Distinct i, (i,j), (i,j,k) of an ordered COO-3 (its grouped levels)."""
+    I, J, Kd = X.dims
+    i, j, k = (_i64(X.levels[t].crd) for t in range(3))
+    if i.numel() == 0:
+        return 0, 0, 0
+    ij = i * J + j
+    return (int(torch.unique_consecutive(i).numel()), int(torch.unique_consecutive(ij).numel()),
+            int(torch.unique_consecutive(ij * Kd + k).numel()))
+
+
+def _spx_visits(pos, crd, xcrd) -> int:
+    """Visits of the {A1,x0} intersection loop: per row, the union of the
+    row's and x's coordinates up to the smaller of the two last ones."""
+    nrows = pos.numel() - 1
+    if crd.numel() == 0 or xcrd.numel() == 0:
+        return 0
+    lens = _i64(pos[1:] - pos[:-1])
+    rows = torch.repeat_interleave(torch.arange(nrows, device=pos.device), lens)
+    crd = _i64(crd[: rows.numel()])
+    xc = _i64(xcrd)
+    last_a = torch.where(lens > 0, crd[(_i64(pos[1:]) - 1).clamp(min=0)], torch.full_like(lens, -1))
+    m = torch.minimum(last_a, xc[-1].expand_as(last_a))
+    live = lens > 0
+    in_a = (crd <= m[rows]) & live[rows]
+    n_a = torch.zeros(nrows, dtype=torch.int64, device=pos.device).index_add_(0, rows, _i64(in_a))
+    shared = torch.zeros(nrows, dtype=torch.int64, device=pos.device).index_add_(
+        0, rows, _i64(in_a & torch.isin(crd, xc)))
+    n_x = torch.searchsorted(xc, m, right=True)
+    return int(torch.where(live, n_a + n_x - shared, torch.zeros_like(n_a)).sum())
+
+
+def _add_counts(p: Plan, ops, res_csr):
+    """Union lattices of C = A + B (lattice.py:346-552): the row loop over
+    {A0,B0} then the rows only one side still has; per visited row the column
+    loop over {A1,B1}, then {A1} / {B1} for the remainder of the longer row."""
+    v = p.ivars
+    A, B = ops["A"], ops["B"]
+    An, Bn = p.operands["A"], p.operands["B"]
+    nrows, ncols = A.dims
+    dev = A.vals.device
+
+    def row_keys_and_entries(st):
+        if format_class(st.format) == "csr":
+            lv, _ = _csr_level(st)
+            rows = torch.arange(nrows, dtype=torch.int64, device=dev)   # dense: every row
+            return rows, _csr_keys(lv.pos, lv.crd, ncols)
+        r, c = st.levels[0].crd, st.levels[1].crd
+        rows = torch.unique_consecutive(_i64(r)) if r.numel() else _i64(r)
+        return rows, _grouped_keys(r, c, ncols)
+
+    ra, ka = row_keys_and_entries(A)
+    rb, kb = row_keys_and_entries(B)
+    out = {}
+    both_i, a_i, b_i, _ = _merge_counts(ra, rb, max(nrows, 1))
+    both_j, a_j, b_j, _ = _merge_counts(ka, kb, ncols)
+    out[(v[0], _label(p, (An, 0), (Bn, 0)))] = int(both_i)
+    out[(v[0], _label(p, (An, 0)))] = int(a_i)
+    out[(v[0], _label(p, (Bn, 0)))] = int(b_i)
+    out[(v[1], _label(p, (An, 1), (Bn, 1)))] = int(both_j)
+    out[(v[1], _label(p, (An, 1)))] = int(a_j)
+    out[(v[1], _label(p, (Bn, 1)))] = int(b_j)
+    return out
+
+
+def _inner_counts(p: Plan, ops):
+    """Intersection at every level of two ordered COO-3 tensors: visits of
+    each level's merge under the parents matched one level up."""
+    v = p.ivars
+    X, Z = ops["X"], ops["Z"]
+    Xn, Zn = p.operands["X"], p.operands["Z"]
+    I, J, Kd = X.dims
+
+    def keys(st):
+        i, j, k = (_i64(st.levels[t].crd) for t in range(3))
+        if not st.vals.numel() or i.numel() == 0:
+            e = i[:0]
+            return e, e, e
+        ij = i * J + j
+        return (torch.unique_consecutive(i), torch.unique_consecutive(ij),
+                torch.unique_consecutive(ij * Kd + k))
+
+    (xi, xij, xk), (zi, zij, zk) = keys(X), keys(Z)
+    out = {}
+    both, _, _, mi = _merge_counts(xi, zi, 1 << 40)     # one root parent
+    out[(v[0], _label(p, (Xn, 0), (Zn, 0)))] = int(both)
+    keep = lambda k, w, par: k[torch.isin(torch.div(k, w, rounding_mode="floor"), par)]
+    xij, zij = keep(xij, J, mi), keep(zij, J, mi)
+    both, _, _, mij = _merge_counts(xij, zij, J)
+    out[(v[1], _label(p, (Xn, 1), (Zn, 1)))] = int(both)
+    xk, zk = keep(xk, Kd, mij), keep(zk, Kd, mij)
+    both, _, _, _ = _merge_counts(xk, zk, Kd)
+    out[(v[2], _label(p, (Xn, 2), (Zn, 2)))] = int(both)
     return out
 
 
@@ -494,14 +799,14 @@ def evaluate(expr, inputs: Dict[str, TensorStorage], out_format: Optional[Tensor
         # hashing the (recursive, frozen-dataclass) formats; the entry holds the
         # format objects, so their ids cannot be reused while it is cached
         fkey = (expr, tuple((n, id(s.format), s.dims) for n, s in inputs.items()),
-                id(out_format), None if out_dims is None else tuple(out_dims))
+                id(out_format), None if out_dims is None else tuple(out_dims), fuse)
         hit = _FAST_CACHE.get(fkey)
         if hit is not None and all(s.format is f for s, f in zip(inputs.values(), hit[0])) \
                 and hit[1] is out_format:
             return _run(hit[2], inputs, stats)
         try:
             key = (expr, tuple(sorted((n, s.format, s.dims) for n, s in inputs.items())),
-                   out_format, None if out_dims is None else tuple(out_dims))
+                   out_format, None if out_dims is None else tuple(out_dims), fuse)
             p = _PLAN_CACHE.get(key)
         except TypeError:            # an unhashable format: plan every time
             key, p = None, None
@@ -517,7 +822,7 @@ def evaluate(expr, inputs: Dict[str, TensorStorage], out_format: Optional[Tensor
         out_dims = tuple(checked.var_extents[v] for v in assignment.lhs.ivars)
     if tuple(out_dims) != tuple(checked.var_extents[v] for v in assignment.lhs.ivars):
         raise ValidationError("out_dims disagree with the expression's variable extents")
-    p = plan(checked, bindings, out_format, tuple(out_dims))
+    p = plan(checked, bindings, out_format, tuple(out_dims), fuse=fuse)
     if key is not None:
         if len(_PLAN_CACHE) >= _PLAN_CACHE_MAX:
             _PLAN_CACHE.clear()
@@ -527,7 +832,7 @@ def evaluate(expr, inputs: Dict[str, TensorStorage], out_format: Optional[Tensor
 
 
 def plan_expression(expr, inputs: Dict[str, TensorStorage],
-                    out_format: Optional[TensorFormat] = None) -> Plan:
+                    out_format: Optional[TensorFormat] = None, *, fuse: bool = True) -> Plan:
     """The kernel binding `evaluate` would use (cf. the reference's `plan`)."""
     assignment = parse(expr) if isinstance(expr, str) else expr
     bindings = {name: (s.format, s.dims) for name, s in inputs.items()}
@@ -535,4 +840,4 @@ def plan_expression(expr, inputs: Dict[str, TensorStorage],
     if out_format is None:
         out_format = preset("dense", order=len(assignment.lhs.ivars))
     out_dims = tuple(checked.var_extents[v] for v in assignment.lhs.ivars)
-    return plan(checked, bindings, out_format, out_dims)
+    return plan(checked, bindings, out_format, out_dims, fuse=fuse)
