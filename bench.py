@@ -104,6 +104,14 @@ def host_threads():
     return len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
 
 
+def headline_config(world, rows_per_gpu, nnz_per_gpu, slots):
+    """The workload, identical in both arms (the measurement protocol is
+    reported separately under "timing")."""
+    return {"workload": WORKLOAD, "grid": f"{G}x{G}x{G * world}", "rows_per_gpu": rows_per_gpu,
+            "nnz_per_gpu": nnz_per_gpu, "ell_slots": slots,
+            "step": "CSR SpMV + ELL SpMV of the same matrix"}
+
+
 # ---------------------------------------------------------------------------
 # algorithmic (compulsory) bytes per launch, SURVEY.md §8(d)
 
@@ -435,11 +443,8 @@ def run_ours(args, rank, world, local_rank):
             "vs_baseline": None,
             "dtype": "f64",
             "data": "synthetic (seeded numpy; BASELINE configs have no public dataset)",
-            "config": {"workload": WORKLOAD, "grid": f"{G}x{G}x{G * world}",
-                       "rows_per_gpu": nrows, "nnz_per_gpu": nnz, "ell_slots": S,
-                       "step": "CSR SpMV + ELL SpMV of the same matrix",
-                       "l2": timer.describe(),
-                       "operand_copies": {"csr": nc_csr, "ell": nc_ell},
+            "config": headline_config(world, nrows, nnz, S),
+            "timing": {"l2": timer.describe(), "operand_copies": {"csr": nc_csr, "ell": nc_ell},
                        "launch": dict(timer.method),
                        "parallelism": f"row-block shards x{world}, x replicated (NCCL broadcast)"},
             "pct_of_peak": round(100.0 * value / (peak * world), 2),
@@ -946,11 +951,8 @@ def run_reference(args, rank, world):
         "ms_per_step": round(dt * reps * 1e3, 4), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded numpy; BASELINE configs have no public dataset)",
-        "config": {"workload": WORKLOAD, "grid": f"{G}x{G}x{G * world}",
-                   "rows_per_gpu": nrows // world, "nnz_per_gpu": nnz // world, "ell_slots": S,
-                   "step": "CSR SpMV + ELL SpMV of the same matrix",
-                   "l2": "host caches (CPU run)", "operand_copies": None,
-                   "parallelism": f"host threads x{thr} (whole grid on rank 0)"},
+        "config": headline_config(world, nrows // world, nnz // world, S),
+        "timing": {"parallelism": f"host threads x{thr} (the whole grid on rank 0)"},
         "cpu_baseline": {"value": round(value, 3), "unit": "GB/s", "cores": thr, "kind": "port",
                          "sample": f"{args.steps} steps x {reps} CSR+ELL SpMVs of the full grid "
                                    f"({dt * reps * args.steps:.1f} s); C restatement of the "
