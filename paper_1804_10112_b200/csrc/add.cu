@@ -39,7 +39,13 @@ constexpr int kRowptrIpt = 8;   // elements per thread (two 16-byte loads when a
 
 __global__ void __launch_bounds__(256)
 coo_rowptr_kernel(int64_t nrows, int64_t nnz, const int32_t* __restrict__ rows,
-                  int32_t* __restrict__ rowptr) {
+                  int32_t* __restrict__ rowptr, int64_t* __restrict__ zero = nullptr,
+                  int64_t nzero = 0) {
+  pdl_trigger();                           // the count pass may begin launching
+  // the count pass's super-tile totals start at zero (saves a memset node)
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < nzero;
+       q += (int64_t)gridDim.x * blockDim.x)
+    zero[q] = 0;
   // rowptr[r] = first e with rows[e] >= r, r in [0, nrows]: element e writes the
   // entries r in (rows[e-1], rows[e]] (e = nnz closes the trailing rows)
   const int64_t e0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * kRowptrIpt;
@@ -158,74 +164,31 @@ SL_DEV int count_row_idx(int ia, int iah, int ib, int ibh, const int32_t* s_col)
   return n;
 }
 
-// Fill merge in the same single-stream form (values staged at the same
-// indices as their columns): each iteration consumes one element, folds it
-// into the current output run (A value; B group: b1 alone, or Python's sum()
-// over a repeated coordinate's values — PySum's state carried in (bs, bc)) and
-// rewrites the run's output slot; the slot's last write, at the run's last
-// element, is the final value 0 + (a + bgroup | a | bgroup) (engine.py:404,
-// 413, 524-531, 625-631).  No divergent branches.
-// The fill merge for a tile whose B slice repeats no coordinate (the usual
-// case; checked per tile): a run is one entry, or an A entry followed by the
-// B entry it matches, so the value is v, or a + b for the match — stored as
-// 0 + value like the general form, without its repeat-group state.
-SL_DEV void fill_row_idx_unique(int ia, int iah, int ib, int ibh, const int32_t* s_col,
-                                const double* s_val, int32_t* oc, double* ov) {
+// Fill merge over staged columns only: per output its column and its sources,
+// packed as bits 0-10 = A's stage index + 1 (0: no A entry), bits 11-21 = the
+// first stage index (relative to B's region) + 1 of B's run (0: none), bits
+// 22-31 = the run's length.  A's row holds unique columns (a non-unique CSR
+// is grouped before it gets here), and A comes first on ties, so an A entry is
+// always the first of its output.  The values are read from global memory by
+// emit_outputs, coalesced across the tile's consecutive outputs.
+SL_DEV int fill_row_src(int ia, int iah, int ib, int ibh, int kcs, const int32_t* s_col,
+                        int32_t* oc, uint32_t* os) {
   int n = -1;
   int32_t last = -1;
-  double prev = 0.0;
+  uint32_t src = 0;
   int32_t ca = ia < iah ? s_col[ia] : INT32_MAX;
   int32_t cb = ib < ibh ? s_col[ib] : INT32_MAX;
   for (int it = (iah - ia) + (ibh - ib); it > 0; --it) {
     const bool ta = ca <= cb;
     const int32_t c = ta ? ca : cb;
-    const double v = s_val[ta ? ia : ib];
     const bool fresh = c != last;
     n += fresh;
     last = c;
+    src = fresh ? 0u : src;
+    const uint32_t bsrc = ((src >> 11) & 0x7ffu) ? src : (src | ((uint32_t)(ib - kcs + 1) << 11));
+    src = ta ? (src | (uint32_t)(ia + 1)) : bsrc + (1u << 22);
     oc[n] = c;
-    ov[n] = dadd(0.0, fresh ? v : dadd(prev, v));   // not fresh: B matching the A before it
-    prev = v;
-    ia += ta;
-    ib += !ta;
-    const int idx = ta ? ia : ib;
-    const int32_t nx = idx < (ta ? iah : ibh) ? s_col[idx] : INT32_MAX;
-    ca = ta ? nx : ca;
-    cb = ta ? cb : nx;
-  }
-}
-
-SL_DEV int fill_row_idx(int ia, int iah, int ib, int ibh, const int32_t* s_col,
-                        const double* s_val, int32_t* oc, double* ov) {
-  int n = -1;
-  int32_t last = -1;
-  double ra = 0.0, bs = 0.0, bc = 0.0;
-  bool has_a = false;
-  int nb = 0;
-  int32_t ca = ia < iah ? s_col[ia] : INT32_MAX;
-  int32_t cb = ib < ibh ? s_col[ib] : INT32_MAX;
-  for (int it = (iah - ia) + (ibh - ib); it > 0; --it) {
-    const bool ta = ca <= cb;
-    const int32_t c = ta ? ca : cb;
-    const double v = s_val[ta ? ia : ib];
-    const bool fresh = c != last;
-    n += fresh;
-    last = c;
-    has_a = (fresh ? false : has_a) || ta;
-    nb = fresh ? 0 : nb;
-    ra = ta ? v : ra;
-    // B's group: nb == 0 -> b1; else one PySum step from f (0 + b1 when nb == 1)
-    const double f = nb == 1 ? dadd(0.0, bs) : bs;
-    const double t = dadd(f, v);
-    const double cnext = nb == 0 ? 0.0
-        : dadd(nb == 1 ? 0.0 : bc, fabs(f) >= fabs(v) ? dadd(dsub(f, t), v) : dadd(dsub(v, t), f));
-    bs = ta ? bs : (nb == 0 ? v : t);
-    bc = ta ? bc : cnext;
-    nb += !ta;
-    const double g = (nb >= 2 && bc != 0.0 && isfinite(bc)) ? dadd(bs, bc) : bs;
-    const double e = has_a ? (nb ? dadd(ra, g) : ra) : g;
-    oc[n] = c;
-    ov[n] = dadd(0.0, e);
+    os[n] = src;
     ia += ta;
     ib += !ta;
     const int idx = ta ? ia : ib;
@@ -234,6 +197,51 @@ SL_DEV int fill_row_idx(int ia, int iah, int ib, int ibh, const int32_t* s_col,
     cb = ta ? cb : nx;
   }
   return n + 1;
+}
+
+// Writes outputs [0, n) of a staged run: column from the stage, value
+// 0 + (a + bgroup | a | bgroup) from the global A / B values (a0 / b0: the
+// global index of stage index 0 of each), four outputs per thread in flight.
+constexpr int kEmitUnroll = 2;
+
+template <int kThreads>
+SL_DEV void emit_outputs(int n, const int32_t* s_ccrd, const uint32_t* s_src, int64_t a0,
+                         int64_t b0, const double* __restrict__ a_vals,
+                         const double* __restrict__ b_vals, int32_t* gc, double* gv) {
+  const double* ap = a_vals + a0 - 1;      // source fields hold stage index + 1
+  const double* bp = b_vals + b0 - 1;
+  for (int q0 = threadIdx.x; q0 < n; q0 += kEmitUnroll * kThreads) {
+    uint32_t src[kEmitUnroll];
+    double av[kEmitUnroll], bv[kEmitUnroll];
+#pragma unroll
+    for (int u = 0; u < kEmitUnroll; ++u) {
+      const int q = q0 + u * kThreads;
+      src[u] = q < n ? s_src[q] : 0u;
+    }
+#pragma unroll
+    for (int u = 0; u < kEmitUnroll; ++u) {
+      const uint32_t sa = src[u] & 0x7ffu, sb = (src[u] >> 11) & 0x7ffu;
+      av[u] = sa ? ldg(ap + sa) : 0.0;
+      bv[u] = sb ? ldg(bp + sb) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < kEmitUnroll; ++u) {
+      const int q = q0 + u * kThreads;
+      if (q < n) {
+        const uint32_t sa = src[u] & 0x7ffu, sb = (src[u] >> 11) & 0x7ffu, nbv = src[u] >> 22;
+        double g = bv[u];
+        if (nbv > 1) {                       // a repeated B coordinate: Python's sum()
+          PySum p;
+          p.start(g);
+          for (uint32_t k = 1; k < nbv; ++k) p.add(ldg(bp + sb + k));
+          g = p.value();
+        }
+        const double e = sa ? (sb ? dadd(av[u], g) : av[u]) : g;
+        gc[q] = s_ccrd[q];
+        gv[q] = dadd(0.0, e);
+      }
+    }
+  }
 }
 
 // first index in [lo, hi) of a sorted global int32 range whose value is >= c
@@ -320,10 +328,10 @@ SL_DEV int64_t tile_prefix(int64_t tile, const int64_t* tile_tot, const int64_t*
   return acc;
 }
 
-// count: 32 registers keep 16 blocks (64 warps) resident; fill: ~90 registers
-// and the output stage allow 5 (the merge is instruction-bound, not occupancy-bound)
+// count: 32 registers keep 16 blocks (64 warps) resident; fill: columns-only
+// staging (~17 KB of shared memory) and <= 40 registers keep 12
 template <int kMode>
-__global__ void __launch_bounds__(kAddRows, kMode == 0 ? 16 : 1)
+__global__ void __launch_bounds__(kAddRows, kMode == 0 ? 16 : 10)
 add_tile_kernel(int64_t nrows, const int32_t* __restrict__ a_pos, const int32_t* __restrict__ a_crd,
                 const double* __restrict__ a_vals, const int32_t* __restrict__ b_pos,
                 const int32_t* __restrict__ b_cols, const double* __restrict__ b_vals,
@@ -333,20 +341,25 @@ add_tile_kernel(int64_t nrows, const int32_t* __restrict__ a_pos, const int32_t*
                 const int32_t* __restrict__ guard = nullptr) {
   constexpr bool kValues = kMode != 0;
   constexpr int kAddCap = kValues ? kAddCapFill : kAddCapCount;
-  if (guard != nullptr && ldg(guard) == 0) return;   // nothing to merge (see the exact convert)
+  if (guard != nullptr) {                  // nothing to merge (see the exact convert)
+    pdl_wait();
+    if (ldg(guard) == 0) return;
+  }
   __shared__ int32_t s_apos[kAddRows + 1], s_bpos[kAddRows + 1];
   // unified stages: A's slice at [0, kCS), B's at [kCS, 2 kCS); a value is
   // staged at the same index as its column
   constexpr int kCS = kAddCap + 8;
   __shared__ __align__(16) int32_t s_col[2 * kCS];
-  __shared__ __align__(16) double s_val[kValues ? 2 * kCS : 2];
   __shared__ int32_t s_rbase[kAddRows];         // row output offsets within the tile
   __shared__ int s_warp[kAddRows / 32];
   __shared__ int64_t s_tile_out;
   __shared__ __align__(8) uint64_t bar;
-  // output stage (fill modes): the tile's outputs are contiguous in C
+  // output stage (fill modes): the tile's outputs are contiguous in C; per
+  // output its column and its sources (fill_row_src) — the values are read
+  // from global memory when the stage is written out, so only columns are
+  // staged and the block's shared memory stays at ~17 KB
   __shared__ int32_t s_ccrd[kValues ? 2 * kAddCap : 1];
-  __shared__ double s_cval[kValues ? 2 * kAddCap : 1];
+  __shared__ uint32_t s_src[kValues ? 2 * kAddCap : 1];
   const int tid = threadIdx.x;
   if (tid == 0) {
     mbar_init(&bar, 1);
@@ -355,6 +368,13 @@ add_tile_kernel(int64_t nrows, const int32_t* __restrict__ a_pos, const int32_t*
   const int64_t tile = blockIdx.x;
   const int64_t r0 = tile * kAddRows;
   const int nr = (int)min64(kAddRows, nrows - r0);
+  if (kMode == 0) {
+    // launched with PDL behind the row-pointer pass: its b_pos and zeroed
+    // super-tile totals must be visible; then let the fill begin launching
+    // (it reads b_pos before its own wait: complete once this wait returns)
+    pdl_wait();
+    pdl_trigger();
+  }
   for (int t = tid; t <= nr; t += kAddRows) {
     s_apos[t] = ldg(a_pos + r0 + t);
     s_bpos[t] = ldg(b_pos + r0 + t);
@@ -364,27 +384,18 @@ add_tile_kernel(int64_t nrows, const int32_t* __restrict__ a_pos, const int32_t*
   const int32_t ea1 = s_apos[nr], eb1 = s_bpos[nr];
   const int na = ea1 - ea0, nb = eb1 - eb0;
   const bool fits = staged_ok && na <= kAddCap && nb <= kAddCap;   // block-uniform
-  BulkRange32 ra{}, rb{}, rav{}, rbv{};
+  BulkRange32 ra{}, rb{};
   if (fits) {
     ra = plan_granules32(a_crd, ea0, ea1);
     rb = plan_granules32(b_cols, eb0, eb1);
-    if (kValues) {
-      rav = plan_granules32(a_vals, ea0, ea1);
-      rbv = plan_granules32(b_vals, eb0, eb1);
-    }
-    // element p of A lands at s_col[p - ra.lo0] and s_val[p - ra.lo0] (B: + kCS);
-    // with 16-byte-aligned operands (staged_ok) the value copies stay aligned
-    int32_t* sa = s_col;
-    int32_t* sb = s_col + kCS;
-    double* sav = s_val + (int32_t)(rav.lo0 - ra.lo0);
-    double* sbv = kValues ? s_val + kCS + (int32_t)(rbv.lo0 - rb.lo0) : s_val;
+    // element p of A lands at s_col[p - ra.lo0] (B: kCS + p - rb.lo0)
     if (tid == 0) {
-      mbar_arrive_expect_tx(&bar, ra.tx_bytes + rb.tx_bytes + rav.tx_bytes + rbv.tx_bytes);
-      issue_range32(a_crd, ra, sa, &bar);
-      issue_range32(b_cols, rb, sb, &bar);
-      if (kValues) {
-        issue_range32(a_vals, rav, sav, &bar);
-        issue_range32(b_vals, rbv, sbv, &bar);
+      mbar_arrive_expect_tx(&bar, ra.tx_bytes + rb.tx_bytes);
+      issue_range32(a_crd, ra, s_col, &bar);
+      issue_range32(b_cols, rb, s_col + kCS, &bar);
+      if (kValues) {            // the values the emitter reads after the merge: to L2 now
+        prefetch_l2(a_vals + ea0, na);
+        prefetch_l2(b_vals + eb0, nb);
       }
     }
     __syncthreads();
@@ -417,22 +428,11 @@ add_tile_kernel(int64_t nrows, const int32_t* __restrict__ a_pos, const int32_t*
   auto stage_group = [&](int g0, int g1, int32_t& oa, int32_t& ob) {
     const int32_t alo = s_apos[g0], ahi = s_apos[g1], blo = s_bpos[g0], bhi = s_bpos[g1];
     const BulkRange32 ga = plan_granules32(a_crd, alo, ahi), gb = plan_granules32(b_cols, blo, bhi);
-    BulkRange32 gav{}, gbv{};
-    if (kValues) {
-      gav = plan_granules32(a_vals, alo, ahi);
-      gbv = plan_granules32(b_vals, blo, bhi);
-    }
-    double* sav = s_val + (int32_t)(gav.lo0 - ga.lo0);
-    double* sbv = kValues ? s_val + kCS + (int32_t)(gbv.lo0 - gb.lo0) : s_val;
     if (tid == 0) {
       fence_proxy_async_smem();          // the previous group's reads precede these writes
-      mbar_arrive_expect_tx(&bar, ga.tx_bytes + gb.tx_bytes + gav.tx_bytes + gbv.tx_bytes);
+      mbar_arrive_expect_tx(&bar, ga.tx_bytes + gb.tx_bytes);
       issue_range32(a_crd, ga, s_col, &bar);
       issue_range32(b_cols, gb, s_col + kCS, &bar);
-      if (kValues) {
-        issue_range32(a_vals, gav, sav, &bar);
-        issue_range32(b_vals, gbv, sbv, &bar);
-      }
     }
     __syncthreads();
     mbar_wait(&bar, gphase);
@@ -512,6 +512,9 @@ add_tile_kernel(int64_t nrows, const int32_t* __restrict__ a_pos, const int32_t*
   }
 
   int64_t tile_out, n_out;
+  // fill launched with PDL behind the count pass: the stage copies above are
+  // in flight; the counts, totals and c_pos it wrote are read from here on
+  pdl_wait();
   if (kMode == 1) {
     tile_out = ldg(c_pos + r0);
     n_out = ldg(c_pos + r0 + nr) - tile_out;
@@ -546,16 +549,13 @@ add_tile_kernel(int64_t nrows, const int32_t* __restrict__ a_pos, const int32_t*
         stage_group(g0, g1, oa, ob);
         const int row = g0 + tid;
         if (row < g1)
-          fill_row_idx(s_apos[row] - oa, s_apos[row + 1] - oa, kCS + s_bpos[row] - ob,
-                       kCS + s_bpos[row + 1] - ob, s_col, s_val, s_ccrd + (s_rbase[row] - ob0),
-                       s_cval + (s_rbase[row] - ob0));
+          fill_row_src(s_apos[row] - oa, s_apos[row + 1] - oa, kCS + s_bpos[row] - ob,
+                       kCS + s_bpos[row + 1] - ob, kCS, s_col, s_ccrd + (s_rbase[row] - ob0),
+                       s_src + (s_rbase[row] - ob0));
         __syncthreads();
-        int32_t* gc = c_crd + tile_out + ob0;              // the group's outputs, coalesced
-        double* gv = c_vals + tile_out + ob0;
-        for (int q = tid; q < ob1 - ob0; q += kAddRows) {
-          gc[q] = s_ccrd[q];
-          gv[q] = s_cval[q];
-        }
+        // the group's outputs, coalesced
+        emit_outputs<kAddRows>(ob1 - ob0, s_ccrd, s_src, oa, ob, a_vals, b_vals,
+                               c_crd + tile_out + ob0, c_vals + tile_out + ob0);
       }
       __syncthreads();                     // stages free for the next group
       g0 = g1;
@@ -618,37 +618,17 @@ add_tile_kernel(int64_t nrows, const int32_t* __restrict__ a_pos, const int32_t*
     }
     return;
   }
-  if (fits) mbar_wait(&bar, 0);
-  // does the staged B slice repeat a coordinate?  (adjacent equal columns;
-  // across a row boundary this only makes the check conservative)
-  bool b_rep = false;
   if (fits) {
-    const int boff = kCS + eb0 - (int32_t)rb.lo0;
-    for (int q = 1 + tid; q < nb; q += kAddRows) b_rep |= s_col[boff + q] == s_col[boff + q - 1];
-  }
-  const bool b_unique = fits && !__syncthreads_or(b_rep);
-  const bool staged_out = n_out <= 2 * kAddCap;
-  int32_t* oc = staged_out ? s_ccrd : c_crd + tile_out;
-  double* ov = staged_out ? s_cval : c_vals + tile_out;
-  if (mine) {
-    const int32_t lo = s_rbase[tid];
-    if (fits)
-      if (b_unique)
-        fill_row_idx_unique(ia, iah, ib, ibh, s_col, s_val, oc + lo, ov + lo);
-      else
-        fill_row_idx(ia, iah, ib, ibh, s_col, s_val, oc + lo, ov + lo);
-    else
-      merge_row<true>(s_apos[tid], s_apos[tid + 1], s_bpos[tid], s_bpos[tid + 1], gacc,
-                      FillEmit{oc + lo, ov + lo});
-  }
-  if (staged_out) {
+    mbar_wait(&bar, 0);
+    // n_out <= na + nb <= 2 kAddCap: the tile's outputs fit the output stage
+    if (mine)
+      fill_row_src(ia, iah, ib, ibh, kCS, s_col, s_ccrd + s_rbase[tid], s_src + s_rbase[tid]);
     __syncthreads();
-    int32_t* gc = c_crd + tile_out;
-    double* gv = c_vals + tile_out;
-    for (int q = tid; q < (int)n_out; q += kAddRows) {
-      gc[q] = s_ccrd[q];
-      gv[q] = s_cval[q];
-    }
+    emit_outputs<kAddRows>((int)n_out, s_ccrd, s_src, ra.lo0, rb.lo0, a_vals, b_vals,
+                           c_crd + tile_out, c_vals + tile_out);
+  } else if (mine) {                       // unaligned operands: merged from global memory
+    merge_row<true>(s_apos[tid], s_apos[tid + 1], s_bpos[tid], s_bpos[tid + 1], gacc,
+                    FillEmit{c_crd + tile_out + s_rbase[tid], c_vals + tile_out + s_rbase[tid]});
   }
 }
 
@@ -814,16 +794,25 @@ static int add_check(int64_t nrows, int64_t b_nnz, const int32_t* a_pos, const i
   return SL_OK;
 }
 
-// count pass: rowptr (COO B), tile counts (tile-local c_pos, tile and super-tile totals)
+// count pass: rowptr (COO B; it also zeroes the super-tile totals), tile
+// counts (tile-local c_pos, tile and super-tile totals), the count launched
+// with PDL behind the row pointer
 static const int32_t* add_count_pass(int64_t nrows, const int32_t* a_pos, const int32_t* a_crd,
                                      int64_t b_nnz, const int32_t* b_pos, const int32_t* b_rows,
                                      const int32_t* b_cols, int32_t* c_pos, const AddWs& w,
                                      cudaStream_t s) {
-  cudaMemsetAsync(w.supers, 0, (size_t)add_nsuper(nrows) * 8, s);
-  const int32_t* bp = add_rowptr(nrows, b_nnz, b_pos, b_rows, w, true, s);
-  add_tile_kernel<0><<<(int)add_ntiles(nrows), kAddRows, 0, s>>>(
-      nrows, a_pos, a_crd, nullptr, bp, b_cols, nullptr, c_pos, nullptr, nullptr, w.tiles,
-      w.supers, true);
+  const int32_t* bp = b_pos;
+  if (b_pos) {
+    cudaMemsetAsync(w.supers, 0, (size_t)add_nsuper(nrows) * 8, s);
+  } else {
+    coo_rowptr_kernel<<<ceil_div(ceil_div(b_nnz + 1, kRowptrIpt), 256), 256, 0, s>>>(
+        nrows, b_nnz, b_rows, w.rowptr, w.supers, add_nsuper(nrows));
+    bp = w.rowptr;
+  }
+  sl_host::launch_pdl(add_tile_kernel<0>, dim3((unsigned)add_ntiles(nrows)), dim3(kAddRows), s,
+                      nrows, a_pos, a_crd, (const double*)nullptr, bp, b_cols,
+                      (const double*)nullptr, c_pos, (int32_t*)nullptr, (double*)nullptr, w.tiles,
+                      w.supers, true, (const int32_t*)nullptr);
   return bp;
 }
 
@@ -873,9 +862,10 @@ extern "C" int sl_add_csr_f64(int64_t nrows, const int32_t* a_pos, const int32_t
     return cudaMemsetAsync(c_pos, 0, sizeof(int32_t), s) == cudaSuccess ? SL_OK : SL_ERR_CUDA;
   const AddWs w = add_ws(ws, nrows);
   const int32_t* bp = add_count_pass(nrows, a_pos, a_crd, b_nnz, b_pos, b_rows, b_cols, c_pos, w, s);
-  add_tile_kernel<2><<<(int)add_ntiles(nrows), kAddRows, 0, s>>>(
-      nrows, a_pos, a_crd, a_vals, bp, b_cols, b_vals, c_pos, c_crd, c_vals, w.tiles, w.supers,
-      add_staged_ok(a_crd, a_vals, b_cols, b_vals));
+  sl_host::launch_pdl(add_tile_kernel<2>, dim3((unsigned)add_ntiles(nrows)), dim3(kAddRows), s,
+                      nrows, a_pos, a_crd, a_vals, bp, b_cols, b_vals, c_pos, c_crd, c_vals,
+                      w.tiles, w.supers, add_staged_ok(a_crd, a_vals, b_cols, b_vals),
+                      (const int32_t*)nullptr);
   return sl_host::launch_status();
 }
 

@@ -34,6 +34,11 @@ struct PySum {
   SL_DEV double value() const { return (c != 0.0 && isfinite(c)) ? dadd(f, c) : f; }
 };
 
+// Programmatic dependent launch: wait for the preceding grid (its writes
+// visible), and let the next grid in the stream begin launching.
+SL_DEV void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+SL_DEV void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // Read-only loads through the non-coherent path.
 template <typename T>
 SL_DEV T ldg(const T* p) { return __ldg(p); }
@@ -123,4 +128,23 @@ int sm_count();                              // cached per current device
 inline int ceil_div(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
 int launch_status();                         // SL_OK or SL_ERR_CUDA after a launch
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// Launch with programmatic dependent launch (PDL): the kernel may start while
+// the previous kernel in the stream drains; it must execute
+// sl::pdl_wait() before reading anything that kernel writes.
+template <typename... KArgs, typename... Args>
+inline void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, cudaStream_t s,
+                       Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
 }  // namespace sl_host

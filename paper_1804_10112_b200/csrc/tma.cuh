@@ -49,6 +49,18 @@ SL_DEV void mbar_arrive(uint64_t* bar) {
 }
 
 // Named barrier over `nthreads` threads (a consumer warp-group), id >= 1.
+// Bulk prefetch of [p, p + n) elements into L2 (cp.async.bulk.prefetch.L2,
+// one instruction; the range is widened to whole 16-byte granules, which
+// stay inside the allocation's 16-byte-aligned extent)
+template <typename T>
+SL_DEV void prefetch_l2(const T* p, int64_t n) {
+  if (n <= 0) return;
+  const uintptr_t lo = reinterpret_cast<uintptr_t>(p) & ~uintptr_t(15);
+  const uintptr_t hi = (reinterpret_cast<uintptr_t>(p + n) + 15) & ~uintptr_t(15);
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(lo), "r"((uint32_t)(hi - lo))
+               : "memory");
+}
+
 SL_DEV void group_sync(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
