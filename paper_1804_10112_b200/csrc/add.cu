@@ -145,10 +145,15 @@ SL_DEV int merge_row(int32_t alo, int32_t ahi, int32_t blo, int32_t bhi, const A
 // instructions at 90% issue; this form, with one shared load per element and
 // no 64-bit pointer selects, is what the count pass executes.)
 SL_DEV int count_row_idx(int ia, int iah, int ib, int ibh, const int32_t* s_col) {
+  // explicit 32-bit shared addresses: with generic indexing the compiler
+  // rematerialised the shared-window base (S2R CgaCtaId + 3 ops) per load
+  const uint32_t base = smem_u32(s_col);
   int n = 0;
   int32_t last = -1;
-  int32_t ca = ia < iah ? s_col[ia] : INT32_MAX;
-  int32_t cb = ib < ibh ? s_col[ib] : INT32_MAX;
+  int32_t ca = lds32(base + 4u * ia);      // the stage holds one slack element past B's end
+  int32_t cb = lds32(base + 4u * ib);
+  ca = ia < iah ? ca : INT32_MAX;
+  cb = ib < ibh ? cb : INT32_MAX;
   for (int it = (iah - ia) + (ibh - ib); it > 0; --it) {
     const bool ta = ca <= cb;
     const int32_t c = ta ? ca : cb;
@@ -157,7 +162,8 @@ SL_DEV int count_row_idx(int ia, int iah, int ib, int ibh, const int32_t* s_col)
     ia += ta;
     ib += !ta;
     const int idx = ta ? ia : ib;
-    const int32_t nx = idx < (ta ? iah : ibh) ? s_col[idx] : INT32_MAX;
+    const int32_t v = lds32(base + 4u * idx);
+    const int32_t nx = idx < (ta ? iah : ibh) ? v : INT32_MAX;
     ca = ta ? nx : ca;
     cb = ta ? cb : nx;
   }
@@ -173,26 +179,33 @@ SL_DEV int count_row_idx(int ia, int iah, int ib, int ibh, const int32_t* s_col)
 // emit_outputs, coalesced across the tile's consecutive outputs.
 SL_DEV int fill_row_src(int ia, int iah, int ib, int ibh, int kcs, const int32_t* s_col,
                         int32_t* oc, uint32_t* os) {
+  const uint32_t base = smem_u32(s_col);
+  uint32_t pc = smem_u32(oc) - 4u, ps = smem_u32(os) - 4u;   // output n at pc + 4 (n + 1)
   int n = -1;
   int32_t last = -1;
   uint32_t src = 0;
-  int32_t ca = ia < iah ? s_col[ia] : INT32_MAX;
-  int32_t cb = ib < ibh ? s_col[ib] : INT32_MAX;
+  int32_t ca = lds32(base + 4u * ia);
+  int32_t cb = lds32(base + 4u * ib);
+  ca = ia < iah ? ca : INT32_MAX;
+  cb = ib < ibh ? cb : INT32_MAX;
   for (int it = (iah - ia) + (ibh - ib); it > 0; --it) {
     const bool ta = ca <= cb;
     const int32_t c = ta ? ca : cb;
     const bool fresh = c != last;
     n += fresh;
+    pc += fresh ? 4u : 0u;
+    ps += fresh ? 4u : 0u;
     last = c;
     src = fresh ? 0u : src;
     const uint32_t bsrc = ((src >> 11) & 0x7ffu) ? src : (src | ((uint32_t)(ib - kcs + 1) << 11));
     src = ta ? (src | (uint32_t)(ia + 1)) : bsrc + (1u << 22);
-    oc[n] = c;
-    os[n] = src;
+    sts32(pc, (uint32_t)c);
+    sts32(ps, src);
     ia += ta;
     ib += !ta;
     const int idx = ta ? ia : ib;
-    const int32_t nx = idx < (ta ? iah : ibh) ? s_col[idx] : INT32_MAX;
+    const int32_t v = lds32(base + 4u * idx);
+    const int32_t nx = idx < (ta ? iah : ibh) ? v : INT32_MAX;
     ca = ta ? nx : ca;
     cb = ta ? cb : nx;
   }
@@ -349,7 +362,7 @@ add_tile_kernel(int64_t nrows, const int32_t* __restrict__ a_pos, const int32_t*
   // unified stages: A's slice at [0, kCS), B's at [kCS, 2 kCS); a value is
   // staged at the same index as its column
   constexpr int kCS = kAddCap + 8;
-  __shared__ __align__(16) int32_t s_col[2 * kCS];
+  __shared__ __align__(16) int32_t s_col[2 * kCS + 4];   // + slack read past B's end
   __shared__ int32_t s_rbase[kAddRows];         // row output offsets within the tile
   __shared__ int s_warp[kAddRows / 32];
   __shared__ int64_t s_tile_out;
