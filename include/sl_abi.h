@@ -161,7 +161,12 @@ int sl_hashed_slot_map(int64_t n, int64_t w, const int32_t* crd, void* ws, size_
  * are written as +0.0 in the same launch (no memset). */
 int sl_spmv_coo_f64(int64_t nrows, int64_t ncols, int64_t nnz,
                     const int32_t* rows, const int32_t* cols, const double* vals,
-                    const double* x, double* y, void* stream);
+                    const double* x, double* y, void* ws, size_t ws_bytes, void* stream);
+/* Workspace of sl_spmv_coo_f64: the row level's position index (nrows + 1
+ * ints), built per call by one streaming pass over the row coordinates; with
+ * it (and rows averaging <= 28 nonzeros, 16-byte-aligned arrays) the sums run
+ * in the register hand-off kernel; ws == NULL keeps the staged-tile kernel. */
+size_t sl_spmv_coo_workspace_bytes(int64_t nrows);
 
 /* CSR (formats.py:126-127). Replaces run_node(i) -> run_node(j) with
  * locate of x (engine.py:591-634).

@@ -456,11 +456,6 @@ add_tile_kernel(int64_t nrows, const int32_t* __restrict__ a_pos, const int32_t*
   const bool grouped = !fits && staged_ok;   // block-uniform
 
   const bool mine = tid < nr;
-  // this row's slices as stage indices
-  const int ia = mine ? s_apos[tid] - (int32_t)ra.lo0 : 0;
-  const int iah = mine ? s_apos[tid + 1] - (int32_t)ra.lo0 : 0;
-  const int ib = mine ? kCS + s_bpos[tid] - (int32_t)rb.lo0 : 0;
-  const int ibh = mine ? kCS + s_bpos[tid + 1] - (int32_t)rb.lo0 : 0;
   const GlobalAcc gacc{a_crd, a_vals, b_cols, b_vals};
   // Rows of a staged tile are merged in order of their merge length (a
   // counting sort over lengths clamped to 31; ties in any order), so each
@@ -859,7 +854,7 @@ static const int32_t* add_count_pass(int64_t nrows, const int32_t* a_pos, const 
     bp = w.rowptr;
   }
   sl_host::launch_pdl(add_tile_kernel<0>, dim3((unsigned)add_ntiles(nrows)), dim3(kAddRows), s,
-                      nrows, a_pos, a_crd, (const double*)nullptr, bp, b_cols,
+                      (size_t)0, nrows, a_pos, a_crd, (const double*)nullptr, bp, b_cols,
                       (const double*)nullptr, c_pos, (int32_t*)nullptr, (double*)nullptr, w.tiles,
                       w.supers, true, (const int32_t*)nullptr);
   return bp;
@@ -912,7 +907,7 @@ extern "C" int sl_add_csr_f64(int64_t nrows, const int32_t* a_pos, const int32_t
   const AddWs w = add_ws(ws, nrows);
   const int32_t* bp = add_count_pass(nrows, a_pos, a_crd, b_nnz, b_pos, b_rows, b_cols, c_pos, w, s);
   sl_host::launch_pdl(add_tile_kernel<2>, dim3((unsigned)add_ntiles(nrows)), dim3(kAddRows), s,
-                      nrows, a_pos, a_crd, a_vals, bp, b_cols, b_vals, c_pos, c_crd, c_vals,
+                      (size_t)0, nrows, a_pos, a_crd, a_vals, bp, b_cols, b_vals, c_pos, c_crd, c_vals,
                       w.tiles, w.supers, add_staged_ok(a_crd, a_vals, b_cols, b_vals),
                       (const int32_t*)nullptr);
   return sl_host::launch_status();

@@ -588,6 +588,7 @@ spmv_csr_handoff_kernel(int64_t nrows, const int32_t* __restrict__ pos,
   const int64_t ntiles = (nrows + 31) / 32;
   int64_t tile = blockIdx.x;
   if (tile >= ntiles) return;
+  pdl_wait();            // COO path: launched with PDL behind the row-pointer pass
   if (lane == 0) {
     mbar_init(bar, 1);
     fence_mbar_init();
@@ -698,10 +699,15 @@ spmv_csr_handoff_kernel(int64_t nrows, const int32_t* __restrict__ pos,
 template <int kCap, int kMaxRow, int kBatch, int kMinBlocks, int kX>
 static void launch_csr_handoff(int64_t nrows, const int32_t* pos, const int32_t* crd,
                                const double* vals, XOperand<kX> xop, double* y, int blocks_per_sm,
-                               cudaStream_t s) {
+                               cudaStream_t s, bool pdl = false) {
   constexpr size_t smem = 16 + (size_t)kCap * 12;
   const int64_t ntiles = (nrows + 31) / 32;
   const int grid = (int)min64(ntiles, (int64_t)sl_host::sm_count() * blocks_per_sm);
+  if (pdl) {
+    sl_host::launch_pdl(spmv_csr_handoff_kernel<kCap, kMaxRow, kBatch, kMinBlocks, kX>, dim3(grid),
+                        dim3(32), s, smem, nrows, pos, crd, vals, xop, y);
+    return;
+  }
   spmv_csr_handoff_kernel<kCap, kMaxRow, kBatch, kMinBlocks, kX><<<grid, 32, smem, s>>>(
       nrows, pos, crd, vals, xop, y);
 }
@@ -960,9 +966,13 @@ static int spmv_path() {
 }
 
 
+extern "C" size_t sl_spmv_coo_workspace_bytes(int64_t nrows) {
+  return ((size_t)(nrows + 1) * sizeof(int32_t) + 255) & ~size_t(255);
+}
+
 extern "C" int sl_spmv_coo_f64(int64_t nrows, int64_t ncols, int64_t nnz, const int32_t* rows,
                                const int32_t* cols, const double* vals, const double* x,
-                               double* y, void* stream) {
+                               double* y, void* ws, size_t ws_bytes, void* stream) {
   if (nrows < 0 || ncols < 0 || nnz < 0) return SL_ERR_INVALID;
   if (nrows > INT32_MAX || ncols > INT32_MAX || nnz > INT32_MAX) return SL_ERR_RANGE;
   if (nrows == 0) return SL_OK;
@@ -974,16 +984,29 @@ extern "C" int sl_spmv_coo_f64(int64_t nrows, int64_t ncols, int64_t nnz, const 
   }
   const bool vec_ok = aligned16(rows) && aligned16(cols) && aligned16(vals);
   if (vec_ok && spmv_path() == 2) return sl_host::launch_coo_pipe(nrows, nnz, rows, cols, vals, x, y, s);
+  // With a workspace and rows averaging <= 28 nonzeros: the row level's
+  // position index (one streaming pass over the row coordinates into the
+  // workspace; cols and vals are not touched), then the register hand-off
+  // kernel K2r over (row pointer, cols, vals), launched with PDL so it starts
+  // while the pass drains.  D1: 20.4 us (staged tiles below) -> see DESIGN.md.
+  // The staged-tile kernel K1 computes on the coordinates alone (no
+  // workspace): the path for longer rows, misaligned arrays, or ws == NULL.
+  const char* ck = getenv("SL_COO_KERNEL");       // A/B knob: "tile" forces K1
+  if (ws && ws_bytes >= sl_spmv_coo_workspace_bytes(nrows) && vec_ok &&
+      nnz <= (int64_t)kCsrHandoffMaxRow * nrows && !(ck && ck[0] == 't')) {
+    int32_t* rowptr = static_cast<int32_t*>(ws);
+    sl_host::launch_coo_rowptr(nrows, nnz, rows, rowptr, s);
+    launch_csr_handoff<kCsrHandoffCap, kCsrHandoffMaxRow, kCsrHandoffBatch, kCsrHandoffBlocks>(
+        nrows, rowptr, cols, vals, XOperand<0>{x}, y, kCsrHandoffBlocks, s, true);
+    return sl_host::launch_status();
+  }
   // 1024-nonzero tiles, 8 blocks/SM: on D1 (2M nonzeros) the grid is 1.65x the
   // resident slots, so later tiles' loads overlap earlier tiles' sum phases
-  // (measured: 2048-nonzero tiles in one wave 37.0 us, this 26.2 us; dropping
-  // the start compaction for per-thread walks from each staged item's start
-  // bit: 29.4 vs 24.8 us, the walks imbalance the lanes; 512-tile
-  // and 128-thread variants 26.7-42 us; a persistent version prefetching the
-  // next tile into registers during the current tile's shared-memory phases
-  // 26.9-34.8 us at 4-8 blocks/SM: profiles/ab/r1_coo_persistent_prefetch.txt;
-  // a persistent version with a two-stage TMA ring of rows/cols/vals and
-  // in-place products 34.9-36.8 us at 3-5 blocks/SM: r1_coo_tma_ring.txt)
+  // (round 1: 2048-nonzero tiles in one wave 37.0 us vs 26.2 us; per-thread
+  // walks without the start compaction 29.4 vs 24.8 us; persistent and TMA-ring
+  // variants 26.9-36.8 us; round 2: a warp-segmented register version (heads
+  // by ballot, per-lane-source shuffle sums, no shared memory) 32-37 us — its
+  // sum loop runs as many warp steps as the round's longest row for ~3 heads)
   spmv_coo_kernel<256, 1, 8><<<ceil_div(nnz, 1024), 256, 0, s>>>(nrows, nnz, rows, cols, vals,
                                                                  x, y, vec_ok);
   return sl_host::launch_status();

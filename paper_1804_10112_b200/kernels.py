@@ -49,12 +49,19 @@ P = _lib.ptr
 
 # ---- SpMV -------------------------------------------------------------------
 
-def spmv_coo(nrows, ncols, rows, cols, vals, x, y=None):
+def spmv_coo(nrows, ncols, rows, cols, vals, x, y=None, ws=None, direct=False):
+    """COO SpMV.  The workspace holds the row level's position index, built
+    per call; direct=True runs the staged-tile kernel on the coordinates
+    alone (no workspace)."""
     rows, cols = _t(rows, I32, "rows"), _t(cols, I32, "cols")
     vals, x = _t(vals, F64, "vals"), _t(x, F64, "x")
     y = _out(y, nrows, F64, x, "y")
+    if direct:
+        ws = None
+    elif ws is None:
+        ws = _ws(L().sl_spmv_coo_workspace_bytes(nrows), x)
     _lib.check(L().sl_spmv_coo_f64(nrows, ncols, rows.numel(), P(rows), P(cols), P(vals), P(x),
-                                   P(y), S()), "spmv_coo")
+                                   P(y), P(ws), 0 if ws is None else ws.numel(), S()), "spmv_coo")
     return y
 
 

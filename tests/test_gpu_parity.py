@@ -82,8 +82,10 @@ def test_spmv_coo_csr_vs_oracle(orc, n, nnz, lam, seed):
     d = wl.coo_spmv(n=n, ncols=max(n, 4000), nnz=nnz, lam=lam, seed=seed)
     ref, _ = orc.spmv_coo(n, d["rows"], d["cols"], d["vals"], d["x"])
     x = cuda(d["x"])
-    y = K.spmv_coo(n, d["ncols"], cuda(d["rows"]), cuda(d["cols"]), cuda(d["vals"]), x)
-    assert np.array_equal(bits(y), bits(ref))
+    for direct in (False, True):       # row-pointer + hand-off path, staged-tile kernel
+        y = K.spmv_coo(n, d["ncols"], cuda(d["rows"]), cuda(d["cols"]), cuda(d["vals"]), x,
+                       direct=direct)
+        assert np.array_equal(bits(y), bits(ref)), direct
     pos = wl.coo_to_csr_pos(d["rows"], n)
     for variant in (0, 1, 2, 3, 4, 5, 6):
         y = K.spmv_csr(n, d["ncols"], cuda(pos), cuda(d["cols"]), cuda(d["vals"]), x,

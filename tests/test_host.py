@@ -36,7 +36,7 @@ def test_library_host_only_calls():
     assert lib.sl_status_string(4) == b"hashed segment is full"
     assert lib.sl_status_string(999) == b"unknown status"
     # argument validation happens before any CUDA call
-    assert lib.sl_spmv_coo_f64(-1, 0, 0, None, None, None, None, None, None) == 1
+    assert lib.sl_spmv_coo_f64(-1, 0, 0, None, None, None, None, None, None, 0, None) == 1
     assert lib.sl_spmv_csr_f64(2**40, 1, 0, None, None, None, None, None, 0, None, 0, None) == 7
     assert lib.sl_hashed_locate(1, None, None, 0, None, None, None, 8, None) == 1
     assert lib.sl_mttkrp_coo3_f64(1, 1, 1, 200, 1, None, None, None, None, None, None, None, None,
