@@ -7,15 +7,21 @@ over NCCL is used only to replicate x / the factors once (broadcast) and,
 optionally, to gather the row blocks of y back (all-gather of padded
 blocks).  One process per GPU.
 
-The host-side partition and shard functions are pure numpy, so the
-multi-rank logic is covered by world_size-2 gloo tests on CPU
-(tests/test_dist_gloo.py); the kernels each rank runs are the single-GPU ones.
+`evaluate_sharded` is the public multi-GPU entry: every rank passes the same
+global operands (resident on its own device); the row blocks are cut on the
+device (searchsorted on the row pointer / row coordinates), each rank's
+shard is a view or a device-side slice of the operand, the rank evaluates its
+block with the single-GPU `evaluate`, and the blocks are optionally
+all-gathered.  The numpy partition/shard helpers below serve the bench and
+the host-side tests; everything is covered by world_size-2 gloo tests on CPU
+(tests/test_dist_gloo.py) — there the per-rank evaluation is injected (the C
+oracle), on a GPU box it is the sm_100a kernels.
 """
 
 from __future__ import annotations
 
 from dataclasses import dataclass
-from typing import List, Sequence
+from typing import Callable, Dict, List, Optional, Sequence, Tuple
 
 import numpy as np
 
@@ -184,3 +190,206 @@ def sum_over_ranks(value: float, device=None) -> float:
 
 def shards_for(bounds: np.ndarray) -> List[RowShard]:
     return [RowShard(p, int(bounds[p]), int(bounds[p + 1])) for p in range(len(bounds) - 1)]
+
+
+# ---------------------------------------------------------------------------
+# public multi-GPU evaluation: device-side row blocks through `evaluate`
+
+def _world(group):
+    import torch.distributed as dist
+
+    if not dist.is_initialized():
+        return 0, 1
+    return dist.get_rank(group), dist.get_world_size(group)
+
+
+def _cuts(prefix, nparts: int):
+    """Indices b[p] = first index with prefix[b] >= total * p / nparts (device
+    searchsorted), b[0] = 0, b[nparts] = len(prefix) - 1."""
+    import torch
+
+    total = int(prefix[-1]) if prefix.numel() else 0
+    n = prefix.numel() - 1
+    tgt = torch.tensor([(total * p) // nparts for p in range(1, nparts)], dtype=prefix.dtype,
+                       device=prefix.device)
+    mid = torch.searchsorted(prefix, tgt).clamp_(max=n).tolist() if nparts > 1 else []
+    b = [0] + [int(v) for v in mid] + [n]
+    for p in range(1, len(b)):
+        b[p] = max(b[p], b[p - 1])
+    return b
+
+
+def _coo_row_prefix_cuts(rows, nrows: int, nparts: int):
+    """Row blocks of a row-sorted coordinate list, balanced by nonzeros:
+    element cut points snapped back to their row's first element."""
+    import torch
+
+    nnz = rows.numel()
+    if nparts == 1:
+        return [0, nrows]
+    if nnz == 0:
+        return [(nrows * p) // nparts for p in range(nparts + 1)]
+    idx = torch.tensor([(nnz * p) // nparts for p in range(1, nparts)], dtype=torch.int64,
+                       device=rows.device).clamp_(max=nnz - 1)
+    r = rows.to(torch.int64)[idx].tolist()
+    b = [0] + [int(v) for v in r] + [nrows]
+    for p in range(1, len(b)):
+        b[p] = min(max(b[p], b[p - 1]), nrows)
+    return b
+
+
+def row_blocks(st, fmt_class: str, nparts: int, mode_dim: int):
+    """Boundaries r[0] = 0 <= ... <= r[nparts] = n of contiguous blocks of the
+    operand's first mode, balanced by stored nonzeros (ELL / DIA / dense:
+    equal rows)."""
+    import torch
+
+    n = mode_dim
+    if fmt_class == "csr":
+        return _cuts(st.levels[1].pos.to(torch.int64), nparts)
+    if fmt_class in ("coo", "coo3"):
+        return _coo_row_prefix_cuts(st.levels[0].crd, n, nparts)
+    if fmt_class == "csf":
+        lv0, lv1, lv2 = st.levels
+        leaf = lv2.pos.to(torch.int64)[lv1.pos.to(torch.int64)]     # nnz before each slice
+        sb = _cuts(leaf, nparts)                                    # slice cut points
+        crd0 = lv0.crd.to(torch.int64)
+        return [0] + [int(crd0[s]) if s < crd0.numel() else n for s in sb[1:-1]] + [n]
+    return [(n * p) // nparts for p in range(nparts + 1)]
+
+
+def shard_storage(st, fmt_class: str, r0: int, r1: int):
+    """Rows [r0, r1) of the operand's first mode as a storage of r1 - r0 rows
+    (coordinates shifted by -r0), on the operand's device: views of the
+    contiguous ranges for CSR / COO / COO-3 / CSF, a strided copy for ELL and
+    DIA (their positions are slot- / diagonal-major)."""
+    import torch
+
+    from .formats import TensorStorage
+    from .levels import LevelStorage
+
+    dims = (r1 - r0,) + tuple(st.dims[1:])
+    dev = st.vals.device
+    L = st.levels
+    if fmt_class == "csr":
+        pos = L[1].pos
+        lo, hi = int(pos[r0]), int(pos[r1])
+        l0 = LevelStorage(L[0].spec, n=r1 - r0, device=dev)
+        l1 = LevelStorage(L[1].spec, pos=(pos[r0:r1 + 1] - lo), crd=L[1].crd[lo:hi], device=dev)
+        return TensorStorage(st.format, dims, [l0, l1], st.vals[lo:hi])
+    if fmt_class in ("coo", "coo3"):
+        rows = L[0].crd
+        lo = int(torch.searchsorted(rows, torch.tensor([r0], dtype=rows.dtype, device=dev)))
+        hi = int(torch.searchsorted(rows, torch.tensor([r1], dtype=rows.dtype, device=dev)))
+        l0 = LevelStorage(L[0].spec, pos=[0, hi - lo], crd=rows[lo:hi] - r0, device=dev)
+        rest = [LevelStorage(lv.spec, crd=lv.crd[lo:hi], device=dev) for lv in L[1:]]
+        return TensorStorage(st.format, dims, [l0] + rest, st.vals[lo:hi])
+    if fmt_class == "csf":
+        crd0 = L[0].crd
+        s0 = int(torch.searchsorted(crd0, torch.tensor([r0], dtype=crd0.dtype, device=dev)))
+        s1 = int(torch.searchsorted(crd0, torch.tensor([r1], dtype=crd0.dtype, device=dev)))
+        f0, f1 = int(L[1].pos[s0]), int(L[1].pos[s1])
+        e0, e1 = int(L[2].pos[f0]), int(L[2].pos[f1])
+        l0 = LevelStorage(L[0].spec, pos=[0, s1 - s0], crd=crd0[s0:s1] - r0, device=dev)
+        l1 = LevelStorage(L[1].spec, pos=L[1].pos[s0:s1 + 1] - f0, crd=L[1].crd[f0:f1], device=dev)
+        l2 = LevelStorage(L[2].spec, pos=L[2].pos[f0:f1 + 1] - e0, crd=L[2].crd[e0:e1], device=dev)
+        return TensorStorage(st.format, dims, [l0, l1, l2], st.vals[e0:e1])
+    if fmt_class == "ell":
+        S, n = L[0].n, st.dims[0]
+        crd = L[2].crd.view(S, n)[:, r0:r1].reshape(-1).contiguous() if S else L[2].crd[:0]
+        vals = st.vals[:S * n].view(S, n)[:, r0:r1].reshape(-1).contiguous() if S else st.vals[:0]
+        return TensorStorage(st.format, dims, [LevelStorage(L[0].spec, n=S, device=dev),
+                                               LevelStorage(L[1].spec, n=r1 - r0, device=dev),
+                                               LevelStorage(L[2].spec, crd=crd, device=dev)], vals)
+    if fmt_class == "dia":
+        # row i of the block is global row r0 + i: a diagonal at offset o
+        # pairs it with column r0 + i + o, so the block is a DIA of
+        # (r1 - r0) x ncols with offsets o + r0 over the same stored values
+        D, n = L[0].n, st.dims[0]
+        offs = L[1].offset.to(torch.int64)
+        vals = st.vals[:D * n].view(D, n)[:, r0:r1].reshape(-1).contiguous()
+        noffs = (offs + r0).to(torch.int32)
+        l1 = LevelStorage(L[1].spec, n=r1 - r0, m=st.dims[1], offset=noffs, device=dev)
+        l2 = LevelStorage(L[2].spec, offset=l1.offset, range_n=r1 - r0, device=dev)
+        l2.offset = l1.offset
+        out = TensorStorage(st.format, dims, [LevelStorage(L[0].spec, n=D, device=dev), l1, l2],
+                            vals)
+        out._host_offsets = noffs.cpu().numpy()
+        return out
+    raise ValueError(f"no row sharding for {fmt_class}")
+
+
+_SHARDED = {"spmv": ("A",), "spmm": ("A",), "add": ("A", "B"), "mttkrp": ("X",),
+            "ttv": ("X",), "ttm": ("X",)}
+
+
+def evaluate_sharded(expr, inputs: Dict[str, "object"], out_format=None, *, group=None,
+                     gather: bool = True, local_eval: Optional[Callable] = None):
+    """Multi-GPU `evaluate`, one process per GPU.
+
+    Every rank passes the same global operands, resident on its device.  The
+    output's first mode is cut into contiguous nnz-balanced blocks, one per
+    rank; the sharded operand (the matrix / tensor whose first mode is the
+    output's) is sliced on the device, the replicated ones (x, B, C, v, U —
+    replicate them with `replicate` first if only one rank holds them) are
+    used whole, and the rank evaluates its block with the single-GPU
+    `evaluate` (no exchange during compute).  With gather=True the blocks are
+    all-gathered (dense: padded row blocks; CSR / COO: nnz totals first, then
+    the arrays), so every rank returns the full result; with gather=False it
+    returns (local block, (r0, r1)).  `local_eval` replaces the per-rank
+    evaluation (tests inject the CPU oracle on gloo ranks)."""
+    import torch
+
+    from . import engine as E
+    from .formats import TensorStorage, preset
+    from .levels import LevelStorage
+
+    rank, world = _world(group)
+    p = E.plan_expression(expr, inputs, out_format)
+    ev = local_eval or E.evaluate
+    if p.pattern not in _SHARDED or world == 1:
+        res = ev(expr, inputs, out_format)
+        return res if gather else (res, (0, res.dims[0] if res.dims else 0))
+    roles = _SHARDED[p.pattern]
+    lead = inputs[p.operands[roles[0]]]
+    n = lead.dims[0]
+    bounds = row_blocks(lead, E.format_class(lead.format), world, n)
+    r0, r1 = bounds[rank], bounds[rank + 1]
+    local = dict(inputs)
+    for role in roles:
+        name = p.operands[role]
+        local[name] = shard_storage(inputs[name], E.format_class(inputs[name].format), r0, r1)
+    res = ev(expr, local, out_format)
+    if not gather:
+        return res, (r0, r1)
+    ocls = E.format_class(res.format)
+    f = res.format
+    dev = res.vals.device
+    if ocls.startswith("dense"):
+        inner = int(np.prod(res.dims[1:])) if len(res.dims) > 1 else 1
+        full = gather_row_blocks(res.vals[:(r1 - r0) * inner], [b * inner for b in bounds], group)
+        dims = (n,) + tuple(res.dims[1:])
+        return TensorStorage(f, dims, [LevelStorage(spec, n=d, device=dev)
+                                       for spec, d in zip(f.levels, dims)], full)
+    if ocls in ("csr", "coo"):
+        if ocls == "csr":
+            pos_l, crd_l = res.levels[1].pos, res.levels[1].crd
+        else:                                   # COO block: rows back to a pointer
+            rows_l = res.levels[0].crd.to(torch.int64)
+            cnt = torch.bincount(rows_l, minlength=r1 - r0)
+            pos_l = torch.cat([torch.zeros(1, dtype=torch.int64, device=dev),
+                               torch.cumsum(cnt, 0)]).to(torch.int32)
+            crd_l = res.levels[1].crd
+        nnz = int(pos_l[-1])
+        pos, crd, vals = concat_csr_blocks(pos_l, crd_l[:nnz], res.vals[:nnz], group)
+        if ocls == "csr":
+            return TensorStorage(f, (n,) + tuple(res.dims[1:]),
+                                 [LevelStorage(f.levels[0], n=n, device=dev),
+                                  LevelStorage(f.levels[1], pos=pos, crd=crd, device=dev)], vals)
+        rows = torch.repeat_interleave(torch.arange(n, dtype=torch.int32, device=dev),
+                                       (pos[1:] - pos[:-1]).to(torch.int64))
+        nz = int(crd.numel())
+        return TensorStorage(f, (n,) + tuple(res.dims[1:]),
+                             [LevelStorage(f.levels[0], pos=[0, nz], crd=rows, device=dev),
+                              LevelStorage(f.levels[1], crd=crd, device=dev)], vals)
+    raise ValueError(f"gather of a {ocls} output is not supported; use gather=False")

@@ -127,3 +127,133 @@ def test_stencil_slabs_are_row_blocks():
     assert all(p["row0"] == 8 * 8 * z for p, z in zip(parts, range(0, 16, 4)))
     pos = np.concatenate([[0], np.cumsum([np.diff(p["pos"]).sum() for p in parts])])
     assert pos[-1] == full["pos"][-1]
+
+
+# ---------------------------------------------------------------------------
+# the public multi-GPU entry, evaluate_sharded, on two gloo ranks: device-side
+# row blocks and shards, per-rank evaluation injected (the C oracle standing
+# in for the sm_100a kernels), blocks all-gathered
+
+def _oracle_eval(expr, inputs, out_format=None):
+    """Per-rank evaluation by the C oracle for the patterns exercised below
+    (test infrastructure; on a GPU box evaluate_sharded runs `evaluate`)."""
+    import oracle
+
+    from paper_1804_10112_b200 import engine as E
+    from paper_1804_10112_b200 import formats as F
+
+    p = E.plan_expression(expr, inputs, out_format)
+    op = {role: inputs[name] for role, name in p.operands.items()}
+    npy = lambda t: t.numpy()  # noqa: E731
+    if p.pattern == "spmv":
+        A, x = op["A"], npy(op["x"].vals)
+        n, m = A.dims
+        if p.kernel == "spmv_csr":
+            y, _ = oracle.spmv_csr(n, npy(A.levels[1].pos), npy(A.levels[1].crd), npy(A.vals), x)
+        elif p.kernel == "spmv_coo":
+            y, _ = oracle.spmv_coo(n, npy(A.levels[0].crd), npy(A.levels[1].crd), npy(A.vals), x)
+        elif p.kernel == "spmv_ell":
+            y, _ = oracle.spmv_ell(n, A.levels[0].n, npy(A.levels[2].crd), npy(A.vals), x)
+        else:
+            y, _ = oracle.spmv_dia(n, m, npy(A.levels[1].offset), npy(A.vals), x)
+        return F.dense_storage(torch.as_tensor(y), (n,), device="cpu")
+    if p.pattern == "add":
+        A, B = op["A"], op["B"]
+        n = A.dims[0]
+        cp, cc, cv = oracle.add_csr(n, npy(A.levels[1].pos), npy(A.levels[1].crd), npy(A.vals),
+                                    npy(B.levels[1].crd), npy(B.vals), b_rows=npy(B.levels[0].crd))
+        return F.csr_storage(cp, cc, cv, A.dims, device="cpu")
+    if p.pattern == "mttkrp":
+        X, Bm, Cm = op["X"], op["B"], op["C"]
+        I, J, K = X.dims
+        R = Bm.dims[1]
+        Bv, Cv = npy(Bm.vals).reshape(J, R), npy(Cm.vals).reshape(K, R)
+        if p.kernel == "mttkrp_csf":
+            A, _ = oracle.mttkrp_csf(I, npy(X.levels[0].crd), npy(X.levels[1].pos),
+                                     npy(X.levels[1].crd), npy(X.levels[2].pos),
+                                     npy(X.levels[2].crd), npy(X.vals), Bv, Cv)
+        else:
+            A, _ = oracle.mttkrp_coo3(I, npy(X.levels[0].crd), npy(X.levels[1].crd),
+                                      npy(X.levels[2].crd), npy(X.vals), Bv, Cv)
+        return F.dense_storage(torch.as_tensor(A.reshape(-1)), (I, R), device="cpu")
+    raise AssertionError(p.pattern)
+
+
+def _sharded_worker(rank, world, port, out_dir):
+    from paper_1804_10112_b200 import formats as F
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        out = {}
+        d = wl.coo_spmv(n=3000, nnz=40000, seed=5)
+        n, m = d["nrows"], d["ncols"]
+        pos = wl.coo_to_csr_pos(d["rows"], n)
+        x = F.dense_storage(torch.as_tensor(d["x"]), (m,), device="cpu")
+        e = wl.csr_to_ell(pos, d["cols"], d["vals"], n)
+        band = np.abs(d["cols"].astype(np.int64) - d["rows"]) <= 300
+        dd = wl.dia_from_coo(d["rows"][band], d["cols"][band], d["vals"][band], n, m)
+        mats = {"csr": F.csr_storage(pos, d["cols"], d["vals"], (n, m), device="cpu"),
+                "coo": F.coo_storage(d["rows"], d["cols"], d["vals"], (n, m), device="cpu"),
+                "ell": F.ell_storage(e["nslots"], e["crd"], e["vals"], (n, m), device="cpu"),
+                "dia": F.dia_storage(dd["offsets"], dd["vals"], (n, m), device="cpu")}
+        for name, A in mats.items():
+            y = D.evaluate_sharded("y(i) = A(i,j) * x(j)", {"A": A, "x": x},
+                                   local_eval=_oracle_eval)
+            out[f"y_{name}"] = y.vals.numpy()
+        ab = wl.add_ab(n=4000, nnz_a=16000, nnz_b=16000, seed=8)
+        A = F.csr_storage(ab["a_pos"], ab["a_crd"], ab["a_vals"], (4000, 4000), device="cpu")
+        B = F.coo_storage(ab["b_rows"], ab["b_cols"], ab["b_vals"], (4000, 4000), device="cpu")
+        C = D.evaluate_sharded("C(i,j) = A(i,j) + B(i,j)", {"A": A, "B": B}, F.preset("csr"),
+                               local_eval=_oracle_eval)
+        out["c_pos"], out["c_crd"] = C.levels[1].pos.numpy(), C.levels[1].crd.numpy()
+        out["c_vals"] = C.vals.numpy()
+        mt = wl.mttkrp(I=300, J=200, K=100, nnz=30000, R=8, seed=6)
+        csf = wl.coo3_to_csf(mt["i"], mt["j"], mt["k"], None)
+        Bf = F.dense_storage(torch.as_tensor(mt["B"].reshape(-1)), (200, 8), device="cpu")
+        Cf = F.dense_storage(torch.as_tensor(mt["C"].reshape(-1)), (100, 8), device="cpu")
+        Xs = {"coo3": F.coo3_storage(mt["i"], mt["j"], mt["k"], mt["vals"], (300, 200, 100),
+                                     device="cpu"),
+              "csf": F.csf_storage([0, len(csf["crd0"])], csf["crd0"], csf["pos1"], csf["crd1"],
+                                   csf["pos2"], csf["crd2"], mt["vals"], (300, 200, 100),
+                                   device="cpu")}
+        for name, X in Xs.items():
+            A_ = D.evaluate_sharded("A(i,r) = X(i,j,k) * B(j,r) * C(k,r)",
+                                    {"X": X, "B": Bf, "C": Cf}, local_eval=_oracle_eval)
+            out[f"A_{name}"] = A_.vals.numpy()
+        loc, (r0, r1) = D.evaluate_sharded("y(i) = A(i,j) * x(j)", {"A": mats["csr"], "x": x},
+                                           gather=False, local_eval=_oracle_eval)
+        out[f"block{rank}"] = np.array([r0, r1])
+        allb = [torch.zeros(2, dtype=torch.int64) for _ in range(world)]
+        dist.all_gather(allb, torch.tensor([r0, r1]))
+        if rank == 0:
+            out["blocks"] = torch.stack(allb).numpy()
+            np.savez(out_dir / "sharded.npz", **out)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_gloo_evaluate_sharded(tmp_path, orc):
+    world = 2
+    mp.spawn(_sharded_worker, args=(world, _free_port(), tmp_path), nprocs=world, join=True)
+    r = np.load(tmp_path / "sharded.npz")
+    d = wl.coo_spmv(n=3000, nnz=40000, seed=5)
+    n, m = d["nrows"], d["ncols"]
+    ref, _ = orc.spmv_coo(n, d["rows"], d["cols"], d["vals"], d["x"])
+    for name in ("csr", "coo", "ell"):
+        assert np.array_equal(r[f"y_{name}"].view(np.int64), ref.view(np.int64)), name
+    band = np.abs(d["cols"].astype(np.int64) - d["rows"]) <= 300
+    dd = wl.dia_from_coo(d["rows"][band], d["cols"][band], d["vals"][band], n, m)
+    ref_d, _ = orc.spmv_dia(n, m, dd["offsets"], dd["vals"], d["x"])
+    assert np.array_equal(r["y_dia"].view(np.int64), ref_d.view(np.int64))
+    ab = wl.add_ab(n=4000, nnz_a=16000, nnz_b=16000, seed=8)
+    rp, rc, rv = orc.add_csr(4000, ab["a_pos"], ab["a_crd"], ab["a_vals"], ab["b_cols"],
+                             ab["b_vals"], b_rows=ab["b_rows"])
+    assert np.array_equal(r["c_pos"], rp) and np.array_equal(r["c_crd"], rc)
+    assert np.array_equal(r["c_vals"].view(np.int64), rv.view(np.int64))
+    mt = wl.mttkrp(I=300, J=200, K=100, nnz=30000, R=8, seed=6)
+    Aref, _ = orc.mttkrp_coo3(300, mt["i"], mt["j"], mt["k"], mt["vals"], mt["B"], mt["C"])
+    for name in ("coo3", "csf"):        # whole slices per rank: the reference order per row
+        assert np.array_equal(r[f"A_{name}"].view(np.int64), Aref.reshape(-1).view(np.int64)), name
+    b = r["blocks"]
+    assert b[0, 0] == 0 and b[0, 1] == b[1, 0] and b[1, 1] == n and 0 < b[0, 1] < n
