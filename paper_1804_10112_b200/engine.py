@@ -80,6 +80,10 @@ def format_class(fmt: TensorFormat) -> str:
             return "csf"
         if k == (LK.HASHED,):
             return "hash1"
+        if k == (LK.HASHED, LK.DENSE):
+            return "hash_dense"     # hashed rows over dense columns
+        if k == (LK.DENSE, LK.HASHED):
+            return "dense_hash"     # a hashed segment of columns per row
         if k == (LK.COMPRESSED,) and fmt.levels[0].props.ordered and fmt.levels[0].props.unique:
             return "spvec"
     roles = tuple(r.part for r in fmt.roles)
@@ -171,13 +175,16 @@ def _plan(checked: CheckedExpr, bindings, out_format: TensorFormat,
                 if (X.ivars[0] == j and lhs.ivars == (i, X.ivars[1])
                         and len({i, j, X.ivars[1]}) == 3):
                     ca, cx = cls[A.tensor], cls[X.tensor]
-                    if ca == "csr" and cx == "dense2":
-                        if ocls != "dense2":
-                            raise UnsupportedOutputError("SpMM output must be dense-2")
-                        return Plan("spmm", "spmm_csr", {"A": A.tensor, "X": X.tensor},
+                    if ca in ("csr", "coo") and cx == "dense2":
+                        if ocls not in ("dense2", "hash_dense"):
+                            raise UnsupportedOutputError(
+                                "SpMM output must be dense-2 or {hashed, dense}")
+                        kern = "spmm_csr" if ca == "csr" else (
+                            "spmm_coo" if fuse else "spmm_coo_grouped")
+                        return Plan("spmm", kern, {"A": A.tensor, "X": X.tensor},
                                     out_format, out_dims, ivars=(i, j, X.ivars[1]))
             raise UnsupportedMergeError("no B200 kernel for this matrix product "
-                                        "(supported: CSR x dense-2)")
+                                        "(supported: CSR / COO x dense-2)")
 
     # ---- 3-tensor x vector / matrix / tensor (X CSF or COO-3)
     if isinstance(rhs, Mul) and all(isinstance(t, Access) for t in (rhs.left, rhs.right)):
@@ -190,19 +197,19 @@ def _plan(checked: CheckedExpr, bindings, out_format: TensorFormat,
             cX, cO = cls[X.tensor], cls[other.tensor]
             # TTV: Y(i,j) = X(i,j,k) * v(k)
             if other.ivars == (k,) and lhs.ivars == (i, j) and len({i, j, k}) == 3:
-                if cX == "csf" and cO == "dense1":
+                if (cX == "csf" or (cX == "coo3" and fuse)) and cO == "dense1":
                     if ocls not in ("dense2", "csr"):
                         raise UnsupportedOutputError("TTV output must be dense-2 or CSR")
-                    return Plan("ttv", f"ttv_csf_{ocls}", {"X": X.tensor, "v": other.tensor},
+                    return Plan("ttv", f"ttv_{cX}_{ocls}", {"X": X.tensor, "v": other.tensor},
                                 out_format, out_dims, ivars=(i, j, k))
                 raise UnsupportedMergeError(f"no B200 kernel for TTV with X {cX}, v {cO}")
             # TTM: Y(i,j,r) = X(i,j,k) * U(k,r)
             if (len(other.ivars) == 2 and other.ivars[0] == k and len(lhs.ivars) == 3
                     and lhs.ivars == (i, j, other.ivars[1]) and len({i, j, k, other.ivars[1]}) == 4):
-                if cX == "csf" and cO == "dense2":
+                if (cX == "csf" or (cX == "coo3" and fuse)) and cO == "dense2":
                     if ocls != "dense3":
                         raise UnsupportedOutputError("TTM output must be dense-3")
-                    return Plan("ttm", "ttm_csf", {"X": X.tensor, "U": other.tensor},
+                    return Plan("ttm", f"ttm_{cX}", {"X": X.tensor, "U": other.tensor},
                                 out_format, out_dims, ivars=(i, j, k, other.ivars[1]))
                 raise UnsupportedMergeError(f"no B200 kernel for TTM with X {cX}, U {cO}")
             # INNERPROD: a() = X(i,j,k) * Z(i,j,k)
@@ -215,21 +222,40 @@ def _plan(checked: CheckedExpr, bindings, out_format: TensorFormat,
                 raise UnsupportedMergeError(
                     f"no B200 kernel for the inner product of {cX} and {cO} (COO-3 x COO-3)")
 
+    # ---- A(i,j,k) = X(i,j,k) + Z(i,j,k) (3rd-order PLUS): the union merge of
+    # the (i,j)-fibre x k matrices — the 2-D A + B kernels over fibre keys
+    if isinstance(rhs, Add) and all(isinstance(t, Access) for t in (rhs.left, rhs.right)):
+        L_, R_ = rhs.left, rhs.right
+        if len(lhs.ivars) == 3 and L_.ivars == lhs.ivars and R_.ivars == lhs.ivars and \
+                len(set(lhs.ivars)) == 3:
+            cl, cr = cls[L_.tensor], cls[R_.tensor]
+            if cl in ("coo3", "csf") and cr in ("coo3", "csf"):
+                if ocls not in ("coo3", "csf", "dense3"):
+                    raise UnsupportedOutputError(
+                        f"PLUS output must be COO-3, CSF or dense-3; got {out_format.describe()}")
+                I_, J_, _ = bindings[L_.tensor][1]
+                if I_ * J_ > 2 ** 31 - 2:
+                    raise UnsupportedMergeError("PLUS: I x J fibre keys exceed int32")
+                return Plan("plus3", f"plus3_{ocls}", {"X": L_.tensor, "Z": R_.tensor},
+                            out_format, out_dims, ivars=lhs.ivars)
+            raise UnsupportedMergeError(f"no B200 kernel for PLUS with {cl} + {cr}")
+
     # ---- C(i,j) = A(i,j) + B(i,j)
     if isinstance(rhs, Add) and all(isinstance(t, Access) for t in (rhs.left, rhs.right)):
         L_, R_ = rhs.left, rhs.right
         if len(lhs.ivars) == 2 and L_.ivars == lhs.ivars and R_.ivars == lhs.ivars:
-            if ocls not in ("csr", "coo"):
+            if ocls not in ("csr", "coo", "dense_hash"):
                 raise UnsupportedOutputError(
-                    f"A + B is assembled by gather-append into CSR or COO; got "
-                    f"{out_format.describe()}")
+                    f"A + B is assembled by gather-append into CSR or COO (or scattered into "
+                    f"a hashed row segment); got {out_format.describe()}")
             cl, cr = cls[L_.tensor], cls[R_.tensor]
             if cl in ("csr", "coo") and cr in ("csr", "coo"):
                 # a + b == b + a bit-for-bit: keep a CSR operand (if any) as A and
                 # a COO one as B, whose duplicate coordinates the kernels group
                 A_, B_ = (L_, R_) if (cl == "csr" or cr == "coo") else (R_, L_)
                 ca = cls[A_.tensor]
-                return Plan("add", f"add_{ca}_{cls[B_.tensor]}_{ocls}",
+                ko = "hash" if ocls == "dense_hash" else ocls
+                return Plan("add", f"add_{ca}_{cls[B_.tensor]}_{ko}",
                             {"A": A_.tensor, "B": B_.tensor}, out_format, out_dims,
                             ivars=lhs.ivars)
             raise UnsupportedMergeError(f"no B200 kernel for A + B with {cl} + {cr}")
@@ -248,8 +274,9 @@ def _plan(checked: CheckedExpr, bindings, out_format: TensorFormat,
                 i, j, k = X.ivars
                 if (len({i, j, k}) == 3 and len(lhs.ivars) == 2 and lhs.ivars[0] == i
                         and Bm.ivars == (j, lhs.ivars[1]) and Cm.ivars == (k, lhs.ivars[1])):
-                    if ocls != "dense2":
-                        raise UnsupportedOutputError("MTTKRP output must be dense-2")
+                    if ocls not in ("dense2", "hash_dense"):
+                        raise UnsupportedOutputError(
+                            "MTTKRP output must be dense-2 or {hashed, dense}")
                     cX = cls[X.tensor]
                     if cX in ("coo3", "csf") and cls[Bm.tensor] == "dense2" and \
                             cls[Cm.tensor] == "dense2":
@@ -350,6 +377,164 @@ def _csr_level(st: TensorStorage):
 def _csr_arrays(st: TensorStorage):
     lv, vals = _csr_level(st)
     return lv.pos, lv.crd, vals
+
+
+def _hashed_rows_output(f: TensorFormat, dims, rows, Y, dev) -> TensorStorage:
+    """{hashed, dense} output of a row-scattered result Y (rows x cols, dense):
+    the written rows inserted in first-write order (the ordered bulk insert
+    = the reference's sequential insert_coord calls, levels.py:312-333), each
+    slot holding its row (engine.py:292-317)."""
+    n, ncols = dims
+    w = f.hash_width or _next_pow2(max(4, 2 * n))
+    crd, err = K.hashed_insert(rows, w)
+    if int(err.item()) != 0:
+        raise HashSegmentFullError(f"hashed segment of width {w} is full")
+    vals = torch.zeros(w * ncols, dtype=torch.float64, device=dev)
+    if rows.numel():
+        slots, _ = K.hashed_locate(rows, w, crd)
+        vals.view(w, ncols)[slots.long()] = Y.reshape(n, ncols)[rows.long()]
+    return TensorStorage(f, tuple(dims), [LevelStorage(f.levels[0], w=w, crd=crd, device=dev),
+                                          LevelStorage(f.levels[1], n=ncols, device=dev)], vals)
+
+
+def _hashed_segments_output(f: TensorFormat, dims, c_pos, c_crd, c_vals, dev) -> TensorStorage:
+    """{dense, hashed} output of a row-wise union (A + B): row i's columns
+    inserted into segment i in ascending order (the order the gather of the
+    union writes them), each slot holding its value."""
+    n, ncols = dims
+    w = f.hash_width or _next_pow2(max(4, 2 * ncols))
+    nnz = int(c_crd.numel())
+    rows = K.csr_rows(n, c_pos, nnz)
+    crd, err = K.hashed_insert(c_crd, w, nseg=max(n, 1), parent=rows)
+    if int(err.item()) != 0:
+        raise HashSegmentFullError(f"hashed segment of width {w} is full")
+    vals = torch.zeros(max(n, 1) * w, dtype=torch.float64, device=dev)
+    if nnz:
+        slots, _ = K.hashed_locate(c_crd, w, crd, parent=rows)
+        vals[slots.long()] = c_vals
+    return TensorStorage(f, tuple(dims), [LevelStorage(f.levels[0], n=n, device=dev),
+                                          LevelStorage(f.levels[1], w=w, crd=crd, device=dev)],
+                         vals)
+
+
+def _coo3_fibres(X: TensorStorage):
+    """The (i, j)-fibre structure of an ordered COO-3 as CSF-shaped levels
+    (slices, fibres, leaves), derived on the device from the coordinates
+    (the leaves are X's own k coordinates and values, duplicates kept)."""
+    i, j, k = X.levels[0].crd, X.levels[1].crd, X.levels[2].crd
+    dev = k.device
+    nnz = int(k.numel())
+    if nnz == 0:
+        z = torch.zeros(1, dtype=torch.int32, device=dev)
+        e = torch.empty(0, dtype=torch.int32, device=dev)
+        return [LevelStorage(X.levels[0].spec, crd=e, device=dev),
+                LevelStorage(X.levels[1].spec, pos=z, crd=e, device=dev),
+                LevelStorage(X.levels[2].spec, pos=z, crd=k, device=dev)]
+    J = X.dims[1]
+    key = i.to(torch.int64) * J + j.to(torch.int64)
+    fst = torch.ones(nnz, dtype=torch.bool, device=dev)
+    fst[1:] = key[1:] != key[:-1]
+    fpos = torch.nonzero(fst).squeeze(1)
+    fi = i[fpos]
+    sst = torch.ones(fpos.numel(), dtype=torch.bool, device=dev)
+    sst[1:] = fi[1:] != fi[:-1]
+    spos = torch.nonzero(sst).squeeze(1)
+    end = lambda t, v: torch.cat([t, torch.tensor([v], device=dev)]).to(torch.int32)  # noqa: E731
+    return [LevelStorage(X.levels[0].spec, crd=fi[spos], device=dev),
+            LevelStorage(X.levels[1].spec, pos=end(spos, fpos.numel()), crd=j[fpos], device=dev),
+            LevelStorage(X.levels[2].spec, pos=end(fpos, nnz), crd=k, device=dev)]
+
+
+def _coo3_grouped(X: TensorStorage):
+    """CSF-shaped levels and values of a COO-3 whose repeated (i, j, k) are
+    grouped (Grouped, engine.py:107-149: one visit, Python's sum() of the
+    run): the exact copy of the (fibre key x k) matrix, its non-empty rows
+    being the fibres."""
+    I, J, Kd = X.dims
+    key, kc, v = _fibre_coo(X)
+    pos, crd, vals = K.coo_to_csr(I * J, key, kc, v)
+    dev = vals.device
+    cnt = pos[1:] - pos[:-1]
+    fib = torch.nonzero(cnt > 0).squeeze(1)
+    fi = (fib // J).to(torch.int32)
+    sst = torch.ones(fib.numel(), dtype=torch.bool, device=dev)
+    if fib.numel():
+        sst[1:] = fi[1:] != fi[:-1]
+    spos = torch.nonzero(sst).squeeze(1)
+    end = lambda t, n: torch.cat([t.to(torch.int64), torch.tensor([n], device=dev)]).to(  # noqa: E731
+        torch.int32)
+    return [LevelStorage(X.levels[0].spec, crd=fi[spos], device=dev),
+            LevelStorage(X.levels[1].spec, pos=end(spos, fib.numel()),
+                         crd=(fib % J).to(torch.int32), device=dev),
+            LevelStorage(X.levels[2].spec, pos=torch.cat([pos[fib], pos[-1:]]), crd=crd,
+                         device=dev)], vals
+
+
+def _fibre_coo(X: TensorStorage):
+    """(fibre key i*J + j, k, vals) of a COO-3 or CSF operand, storage order."""
+    J = X.dims[1]
+    if format_class(X.format) == "coo3":
+        key = X.levels[0].crd.to(torch.int64) * J + X.levels[1].crd.to(torch.int64)
+        return key.to(torch.int32), X.levels[2].crd, X.vals[:X.levels[2].crd.numel()]
+    L = X.levels
+    n1 = int(L[1].crd.numel())
+    nnz = int(L[2].crd.numel())
+    dev = X.vals.device
+    fs = torch.repeat_interleave(torch.arange(L[0].crd.numel(), device=dev),
+                                 (L[1].pos[1:] - L[1].pos[:-1]).to(torch.int64))
+    fkey = L[0].crd.to(torch.int64)[fs] * J + L[1].crd.to(torch.int64)
+    leaf_f = torch.repeat_interleave(torch.arange(n1, device=dev),
+                                     (L[2].pos[1:] - L[2].pos[:-1]).to(torch.int64))
+    return fkey[leaf_f].to(torch.int32), L[2].crd, X.vals[:nnz]
+
+
+def _plus3(p: Plan, X: TensorStorage, Z: TensorStorage, dev) -> TensorStorage:
+    """A(i,j,k) = X(i,j,k) + Z(i,j,k): the rows of the 2-D union are the (i, j)
+    fibres (keys i*J + j, in storage order), its columns k — the same
+    gather-append union and duplicate grouping as A + B (X's exact grouped
+    copy, Z's repeats grouped by the kernels; engine.py:107-149, 330-434)."""
+    I, J, Kd = X.dims
+    nkey = I * J
+    xr, xc, xv = _fibre_coo(X)
+    zr, zc, zv = _fibre_coo(Z)
+    a_pos, a_crd, a_vals = K.coo_to_csr(nkey, xr, xc, xv)
+    c_pos, c_crd, c_vals = K.add_csr(nkey, a_pos, a_crd, a_vals, zc, zv, b_rows=zr)
+    f = p.out_format
+    ocls = format_class(f)
+    nnz = int(c_crd.numel())
+    if ocls == "dense3":
+        out = torch.zeros(I * J * Kd, dtype=torch.float64, device=dev)
+        if nnz:
+            rows = K.csr_rows(nkey, c_pos, nnz).to(torch.int64)
+            out[rows * Kd + c_crd.to(torch.int64)] = c_vals
+        return TensorStorage(f, (I, J, Kd), [LevelStorage(s_, n=d, device=dev)
+                                             for s_, d in zip(f.levels, (I, J, Kd))], out)
+    rows = K.csr_rows(nkey, c_pos, nnz).to(torch.int64) if nnz else \
+        torch.empty(0, dtype=torch.int64, device=dev)
+    ci, cj = (rows // J).to(torch.int32), (rows % J).to(torch.int32)
+    if ocls == "coo3":
+        return TensorStorage(f, (I, J, Kd), [LevelStorage(f.levels[0], pos=[0, nnz], crd=ci,
+                                                          device=dev),
+                                             LevelStorage(f.levels[1], crd=cj, device=dev),
+                                             LevelStorage(f.levels[2], crd=c_crd, device=dev)],
+                             c_vals)
+    # CSF: the non-empty fibres, their slices
+    cnt = c_pos[1:] - c_pos[:-1]
+    fib = torch.nonzero(cnt > 0).squeeze(1)
+    fi = (fib // J).to(torch.int32)
+    sst = torch.ones(fib.numel(), dtype=torch.bool, device=dev)
+    if fib.numel():
+        sst[1:] = fi[1:] != fi[:-1]
+    spos = torch.nonzero(sst).squeeze(1)
+    end = lambda t, v: torch.cat([t.to(torch.int64), torch.tensor([v], device=dev)]).to(  # noqa: E731
+        torch.int32)
+    return TensorStorage(f, (I, J, Kd), [
+        LevelStorage(f.levels[0], pos=[0, int(spos.numel())], crd=fi[spos], device=dev),
+        LevelStorage(f.levels[1], pos=end(spos, fib.numel()), crd=(fib % J).to(torch.int32),
+                     device=dev),
+        LevelStorage(f.levels[2], pos=torch.cat([c_pos[fib], c_pos[-1:]]), crd=c_crd,
+                     device=dev)],
+        c_vals)
 
 
 _SKEW_TILE = 4 * 896   # 32-row tiles heavier than four hand-off stages: merge-path
@@ -466,6 +651,8 @@ def _run_on(p: Plan, inputs: Dict[str, TensorStorage], stats: Optional[EvalStats
             out = TensorStorage(f, A.dims, [LevelStorage(f.levels[0], n=nrows, device=dev),
                                             LevelStorage(f.levels[1], pos=c_pos, crd=c_crd,
                                                          device=dev)], c_vals)
+        elif ko == "hash":           # dense_hash: each row's columns in its own segment
+            out = _hashed_segments_output(f, A.dims, c_pos, c_crd, c_vals, dev)
         else:
             rows = K.csr_rows(nrows, c_pos, c_crd.numel())
             nnz = int(c_crd.numel())
@@ -478,26 +665,45 @@ def _run_on(p: Plan, inputs: Dict[str, TensorStorage], stats: Optional[EvalStats
         A, X = ops["A"], ops["X"]
         nrows, ncols = A.dims
         Kc = X.dims[1]
-        lv, vals = _csr_level(A)
+        if p.kernel == "spmm_coo":           # fused COO chain: the row level's position index
+            lv = LevelStorage(A.levels[0].spec, pos=K.coo_rowptr(nrows, A.levels[0].crd),
+                              crd=A.levels[1].crd, device=dev)
+            vals = A.vals
+        elif p.kernel == "spmm_coo_grouped":  # unfused: rows and (row, column) runs grouped
+            pos, crd, vals = K.coo_to_csr(nrows, A.levels[0].crd, A.levels[1].crd, A.vals)
+            lv = LevelStorage(A.levels[1].spec, pos=pos, crd=crd, device=dev)
+        else:
+            lv, vals = _csr_level(A)
         long_min = _SPMM_LONG_ROW if _row_stats(lv)[1] > _SPMM_LONG_ROW else None
         Y = K.spmm_csr(nrows, ncols, lv.pos, lv.crd, vals, X.vals.view(ncols, Kc),
                        long_min=long_min)
         f = p.out_format
-        out = TensorStorage(f, (nrows, Kc), [LevelStorage(f.levels[0], n=nrows, device=dev),
-                                             LevelStorage(f.levels[1], n=Kc, device=dev)],
-                            Y.reshape(-1))
+        if format_class(f) == "hash_dense":   # rows written = rows holding a nonzero
+            cnt = lv.pos[1:] - lv.pos[:-1]
+            rows = torch.nonzero(cnt > 0).squeeze(1).to(torch.int32)
+            out = _hashed_rows_output(f, (nrows, Kc), rows, Y, dev)
+        else:
+            out = TensorStorage(f, (nrows, Kc), [LevelStorage(f.levels[0], n=nrows, device=dev),
+                                                 LevelStorage(f.levels[1], n=Kc, device=dev)],
+                                Y.reshape(-1))
     elif p.pattern in ("ttv", "ttm"):
         X = ops["X"]
         I, J, Kd = X.dims
-        lv = X.levels
-        args = (I, J, Kd, lv[0].crd, lv[1].pos, lv[1].crd, lv[2].pos, lv[2].crd, X.vals)
+        xv = X.vals
+        if p.kernel == "ttv_coo3_csr":       # gather output: the chain's repeats grouped
+            lv, xv = _coo3_grouped(X)
+        elif "_coo3" in p.kernel:            # scatter output: per-nonzero, storage order
+            lv = _coo3_fibres(X)
+        else:
+            lv = X.levels
+        args = (I, J, Kd, lv[0].crd, lv[1].pos, lv[1].crd, lv[2].pos, lv[2].crd, xv)
         f = p.out_format
-        if p.kernel == "ttv_csf_csr":
+        if p.kernel.endswith("_csr"):
             pos, crd, vals = K.ttv_csf(*args, ops["v"].vals, out="csr")
             out = TensorStorage(f, (I, J), [LevelStorage(f.levels[0], n=I, device=dev),
                                             LevelStorage(f.levels[1], pos=pos, crd=crd,
                                                          device=dev)], vals)
-        elif p.kernel == "ttv_csf_dense2":
+        elif p.kernel.endswith("_dense2"):
             Y = K.ttv_csf(*args, ops["v"].vals)
             out = TensorStorage(f, (I, J), [LevelStorage(f.levels[0], n=I, device=dev),
                                             LevelStorage(f.levels[1], n=J, device=dev)],
@@ -511,6 +717,8 @@ def _run_on(p: Plan, inputs: Dict[str, TensorStorage], stats: Optional[EvalStats
                                                LevelStorage(f.levels[1], n=J, device=dev),
                                                LevelStorage(f.levels[2], n=R, device=dev)],
                                 Y.reshape(-1))
+    elif p.pattern == "plus3":
+        out = _plus3(p, ops["X"], ops["Z"], dev)
     elif p.pattern == "inner":
         X, Z = ops["X"], ops["Z"]
         I, J, Kd = X.dims
@@ -530,9 +738,14 @@ def _run_on(p: Plan, inputs: Dict[str, TensorStorage], stats: Optional[EvalStats
             A = K.mttkrp_csf(I, J, Kd, X.levels[0].crd, X.levels[1].pos, X.levels[1].crd,
                              X.levels[2].pos, X.levels[2].crd, X.vals, Bt, Ct)
         f = p.out_format
-        out = TensorStorage(f, (I, R), [LevelStorage(f.levels[0], n=I, device=dev),
-                                        LevelStorage(f.levels[1], n=R, device=dev)],
-                            A.reshape(-1))
+        if format_class(f) == "hash_dense":   # rows written = the stored slices, in order
+            rows = torch.unique_consecutive(X.levels[0].crd) if X.levels[0].crd.numel() else \
+                X.levels[0].crd
+            out = _hashed_rows_output(f, (I, R), rows, A, dev)
+        else:
+            out = TensorStorage(f, (I, R), [LevelStorage(f.levels[0], n=I, device=dev),
+                                            LevelStorage(f.levels[1], n=R, device=dev)],
+                                A.reshape(-1))
     if stats is not None:
         for (var, label), n in _loop_counts(p, ops, locals().get("res_csr")).items():
             if n:
@@ -638,11 +851,24 @@ def _loop_counts(p: Plan, ops, res_csr) -> Dict[Tuple[str, str], int]:
                 out[(v[1], jl)] = int(lv.crd.numel())
     elif p.pattern == "spmm":
         A, X = ops["A"], ops["X"]
-        lv, _ = _csr_level(A)
-        nnz = int(lv.crd.numel())
-        out[(v[0], _label(p, (n["A"], 0)))] = A.dims[0]
-        out[(v[1], _label(p, (n["A"], 1), (n["X"], 0)))] = nnz
-        out[(v[2], _label(p, (n["X"], 1)))] = nnz * X.dims[1]
+        Kc = X.dims[1]
+        if p.kernel == "spmm_coo":            # fused chain: one visit per nonzero
+            nnz = int(A.levels[1].crd.numel())
+            out[(v[0], _label(p, (n["A"], 0)))] = nnz
+            out[(v[2], _label(p, (n["X"], 1)))] = nnz * Kc
+        elif p.kernel == "spmm_coo_grouped":
+            r, c = A.levels[0].crd, A.levels[1].crd
+            nr = int(torch.unique_consecutive(r).numel()) if r.numel() else 0
+            nij = int(_grouped_keys(r, c, A.dims[1]).numel())
+            out[(v[0], _label(p, (n["A"], 0)))] = nr
+            out[(v[1], _label(p, (n["A"], 1), (n["X"], 0)))] = nij
+            out[(v[2], _label(p, (n["X"], 1)))] = nij * Kc
+        else:
+            lv, _ = _csr_level(A)
+            nnz = int(lv.crd.numel())
+            out[(v[0], _label(p, (n["A"], 0)))] = A.dims[0]
+            out[(v[1], _label(p, (n["A"], 1), (n["X"], 0)))] = nnz
+            out[(v[2], _label(p, (n["X"], 1)))] = nnz * Kc
     elif p.pattern == "add":
         out.update(_add_counts(p, ops, res_csr))
     elif p.pattern == "mttkrp":
@@ -659,6 +885,20 @@ def _loop_counts(p: Plan, ops, res_csr) -> Dict[Tuple[str, str], int]:
             out[(v[1], _label(p, (Xn, 1), (Bn, 0)))] = nij
             out[(v[2], _label(p, (Xn, 2), (Cn, 0)))] = nijk
             out[(v[3], _label(p, (Bn, 1), (Cn, 1)))] = nijk * R
+    elif p.pattern in ("ttv", "ttm") and "_coo3" in p.kernel:
+        X = ops["X"]
+        On = n["v"] if p.pattern == "ttv" else n["U"]
+        nnz = int(X.levels[2].crd.numel())
+        if p.kernel == "ttv_coo3_csr":        # gather output: (i, j) then k grouped
+            _, nij, nijk = _coo3_level_sizes(X)
+            out[(v[0], _label(p, (n["X"], 0)))] = nij
+            out[(v[2], _label(p, (n["X"], 2), (On, 0)))] = nijk
+        else:                                 # scatter: the fused chain, per nonzero
+            out[(v[0], _label(p, (n["X"], 0)))] = nnz
+            if p.pattern == "ttm":
+                out[(v[3], _label(p, (On, 1)))] = nnz * ops["U"].dims[1]
+    elif p.pattern == "plus3":
+        out.update(_plus3_counts(p, ops))
     elif p.pattern in ("ttv", "ttm"):
         X = ops["X"]
         On = n["v"] if p.pattern == "ttv" else n["U"]
@@ -735,6 +975,47 @@ def _add_counts(p: Plan, ops, res_csr):
     out[(v[1], _label(p, (An, 1), (Bn, 1)))] = int(both_j)
     out[(v[1], _label(p, (An, 1)))] = int(a_j)
     out[(v[1], _label(p, (Bn, 1)))] = int(b_j)
+    return out
+
+
+def _level_keys(st: TensorStorage):
+    """Distinct coordinate keys of a COO-3 / CSF operand per level: i,
+    i*J + j, (i*J + j)*K + k (sorted)."""
+    I, J, Kd = st.dims
+    if format_class(st.format) == "coo3":
+        i, j, k = (_i64(st.levels[t].crd) for t in range(3))
+        if i.numel() == 0:
+            return i, i, i
+        ij = i * J + j
+        return (torch.unique_consecutive(i), torch.unique_consecutive(ij),
+                torch.unique_consecutive(ij * Kd + k))
+    L = st.levels
+    dev = st.vals.device
+    s_of_f = torch.repeat_interleave(torch.arange(L[0].crd.numel(), device=dev),
+                                     _i64(L[1].pos[1:] - L[1].pos[:-1]))
+    fkey = _i64(L[0].crd)[s_of_f] * J + _i64(L[1].crd)
+    f_of_l = torch.repeat_interleave(torch.arange(L[1].crd.numel(), device=dev),
+                                     _i64(L[2].pos[1:] - L[2].pos[:-1]))
+    lkey = fkey[f_of_l] * Kd + _i64(L[2].crd)
+    uq = lambda t: torch.unique_consecutive(t) if t.numel() else t  # noqa: E731
+    return uq(_i64(L[0].crd)), uq(fkey), uq(lkey)
+
+
+def _plus3_counts(p: Plan, ops):
+    """Union lattices of X + Z at every level (each visited parent's streams
+    merged, then the longer one's remainder): (var, {X?,Z?}) visit counts."""
+    v = p.ivars
+    X, Z = ops["X"], ops["Z"]
+    Xn, Zn = p.operands["X"], p.operands["Z"]
+    I, J, Kd = X.dims
+    kx, kz = _level_keys(X), _level_keys(Z)
+    out = {}
+    for lvl, (a, b, w) in enumerate(((kx[0], kz[0], 1 << 40), (kx[1], kz[1], J),
+                                     (kx[2], kz[2], Kd))):
+        both, a_only, b_only, _ = _merge_counts(a, b, w)
+        out[(v[lvl], _label(p, (Xn, lvl), (Zn, lvl)))] = int(both)
+        out[(v[lvl], _label(p, (Xn, lvl)))] = int(a_only)
+        out[(v[lvl], _label(p, (Zn, lvl)))] = int(b_only)
     return out
 
 

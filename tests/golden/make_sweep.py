@@ -65,7 +65,14 @@ def variants(name):
 
 
 def primary(name):
-    return ("base", name, {}, sl.preset(name))
+    return ("base", name, {}, custom(name) if name.startswith("custom:") else sl.preset(name))
+
+
+def custom(name):
+    """custom:<kinds> formats beyond the presets, e.g. custom:hd = {hashed,
+    dense} (a hashed first level over rows, dense columns)."""
+    kinds = {"h": rl.hashed, "d": rl.dense, "c": rl.compressed}
+    return sl.formats.simple_format([kinds[ch]() for ch in name.split(":", 1)[1]], name=name)
 
 
 # ---------------------------------------------------------------------------
@@ -243,6 +250,32 @@ def sweep():
             for vo in all_variants(2):
                 run_case(pack, cases, "mttkrp", expr, {"X": primary(xb), "B": d2, "C": d2}, vo,
                          fuse, dims, rng)
+
+    # ---- 3rd-order PLUS A(i,j,k) = X(i,j,k) + Z(i,j,k)
+    expr = "A(i,j,k) = X(i,j,k) + Z(i,j,k)"
+    dims = {"X": (4, 5, 6), "Z": (4, 5, 6)}
+    c3 = primary("coo-3")
+    for fuse in fuses:
+        for vx in all_variants(3):
+            run_case(pack, cases, "plus3", expr, {"X": vx, "Z": c3}, c3, fuse, dims, rng)
+            run_case(pack, cases, "plus3", expr, {"X": c3, "Z": vx}, c3, fuse, dims, rng)
+        for vo in all_variants(3):
+            run_case(pack, cases, "plus3", expr, {"X": c3, "Z": c3}, vo, fuse, dims, rng)
+
+    # ---- hashed outputs beyond SpMV: MTTKRP and SpMM into {hashed, dense},
+    # A + B into {dense, hashed} (engine.py:292-317, levels.py:312-333)
+    hd, dh = primary("custom:hd"), primary("custom:dh")
+    for fuse in fuses:
+        for xb in ("coo-3", "csf"):
+            run_case(pack, cases, "mttkrp", "A(i,r) = X(i,j,k) * B(j,r) * C(k,r)",
+                     {"X": primary(xb), "B": d2, "C": d2}, hd, fuse,
+                     {"X": (4, 5, 6), "B": (5, 3), "C": (6, 3)}, rng)
+        for ab in ("csr", "coo-soa"):
+            run_case(pack, cases, "spmm", "Y(i,k) = A(i,j) * X(j,k)",
+                     {"A": primary(ab), "X": d2}, hd, fuse, {"A": (6, 7), "X": (7, 3)}, rng)
+            run_case(pack, cases, "add", "C(i,j) = A(i,j) + B(i,j)",
+                     {"A": primary("csr"), "B": primary(ab)}, dh, fuse,
+                     {"A": (6, 7), "B": (6, 7)}, rng)
 
     # ---- TTV Y(i,j) = X(i,j,k) * v(k), TTM Y(i,j,r) = X(i,j,k) * U(k,r)
     for fuse in fuses:

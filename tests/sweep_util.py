@@ -45,7 +45,13 @@ def fmt(desc):
     """Our TensorFormat for a sweep format description (preset + level flags)."""
     if desc is None:
         return None
-    f = slb.preset(desc["preset"])
+    if desc["preset"].startswith("custom:"):
+        kinds = {"h": L.hashed, "d": L.dense, "c": L.compressed}
+        from paper_1804_10112_b200.formats import simple_format
+        f = simple_format([kinds[ch]() for ch in desc["preset"].split(":", 1)[1]],
+                          name=desc["preset"])
+    else:
+        f = slb.preset(desc["preset"])
     levels = list(f.levels)
     for k, flags in desc["levels"].items():
         spec = levels[int(k)]
