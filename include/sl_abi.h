@@ -159,6 +159,12 @@ int sl_hashed_slot_map(int64_t n, int64_t w, const int32_t* crd, void* ws, size_
  * nonzeros are staged, products formed in parallel, and each row is summed in
  * storage order by the thread that owns the row's first nonzero.  Empty rows
  * are written as +0.0 in the same launch (no memset). */
+/* Optional kernels this build carries: bit 0 = the A/B alternatives (CSR
+ * variants 1, 3, 4 and the persistent TMA pipelines of SL_SPMV_PATH=pipe),
+ * compiled only with SL_BUILD_ALT=1; without them those variants return
+ * SL_ERR_INVALID. */
+int sl_build_features(void);
+
 int sl_spmv_coo_f64(int64_t nrows, int64_t ncols, int64_t nnz,
                     const int32_t* rows, const int32_t* cols, const double* vals,
                     const double* x, double* y, void* ws, size_t ws_bytes, void* stream);

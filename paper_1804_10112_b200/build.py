@@ -18,17 +18,27 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 INCLUDE = ROOT / "include"
-LIBDIR = PKG / "_lib"
+LIBDIR = PKG / "_lib" / ("alt" if os.environ.get("SL_BUILD_ALT", "") not in ("", "0") else "")
 LIB = LIBDIR / "libsl_b200.so"
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr",
          "-Xcompiler", "-fPIC,-O2", "-cudart", "static", "-I", str(INCLUDE), "-I", str(CSRC)]
+if os.environ.get("SL_BUILD_ALT", "") not in ("", "0"):
+    FLAGS += ["-DSL_WITH_ALT"]
+
+
+# SL_BUILD_ALT=1: also the A/B alternatives kept for measurement (CSR variants
+# 1 / 3 / 4 and the persistent TMA pipelines of pipe.cu), into _lib/alt/ —
+# load it with SL_LIB_PATH.  The default library carries only the kernels the
+# dispatch chooses.
+ALT = os.environ.get("SL_BUILD_ALT", "") not in ("", "0")
+ALT_ONLY = {"pipe.cu"}
 
 
 def sources():
-    return sorted(CSRC.glob("*.cu"))
+    return sorted(p for p in CSRC.glob("*.cu") if ALT or p.name not in ALT_ONLY)
 
 
 def _stale() -> bool:
@@ -42,7 +52,7 @@ def _stale() -> bool:
 def build(force: bool = False, verbose: bool = False) -> Path:
     if not force and not _stale():
         return LIB
-    LIBDIR.mkdir(exist_ok=True)
+    LIBDIR.mkdir(parents=True, exist_ok=True)
     objs, procs = [], []
     for src in sources():                     # one nvcc per translation unit, in parallel
         obj = LIBDIR / (src.stem + ".o")

@@ -458,6 +458,7 @@ spmv_csr_rowblock_kernel(int64_t nrows, const int32_t* __restrict__ pos,
 // (warps run the longest row) and K2a stays faster (20.5 vs 29 us), so the
 // automatic choice takes K2f only for rows averaging >= 16 nonzeros.
 
+#ifdef SL_WITH_ALT   // row-stage CSR (variant 4): A/B variant, opt-in build (SL_BUILD_ALT=1)
 constexpr int kCsrStageRows = 32;
 constexpr int kCsrStageCap = 896;     // 28 per row: the 27-point stencil's rows fit in one round
 constexpr int kCsrStageBatch = 9;
@@ -553,6 +554,8 @@ static void launch_csr_stage(int64_t nrows, const int32_t* pos, const int32_t* c
 // The register batch's terms: dense x gathers x[c]; a slot-mapped hashed x
 // (kX 2) or a sparse-vector x (kX 3) first gathers the coordinate's slot, then
 // x[slot]; a missing coordinate contributes no term (+0.0, see XOperand<1>).
+#endif  // SL_WITH_ALT
+
 template <int kX, int kB>
 SL_DEV void handoff_terms(const XOperand<kX>& xop, const int32_t* c, const double* v, int u0,
                           int len, double* t) {
@@ -730,6 +733,7 @@ constexpr int kCsrHandoffBlocks = 12;
 // products of its row in order.  Warps synchronise with __syncwarp only, so
 // they progress independently (the block-level barriers of K2a stall on the
 // slowest warp).
+#ifdef SL_WITH_ALT   // warp row-block (3) and vector-per-row (1) CSR: A/B variant, opt-in build (SL_BUILD_ALT=1)
 constexpr int kCsrWarpIpt = 8;
 constexpr int kCsrWarpChunk = 32 * kCsrWarpIpt;   // 256 products per round
 
@@ -802,6 +806,8 @@ spmv_csr_vector_kernel(int64_t nrows, const int32_t* __restrict__ pos,
 // done by a partition kernel.  A row is owned by the tile holding its end
 // item; its owner re-reads the row's head from earlier tiles if the row
 // started before the tile, so every row is still summed in order by one thread.
+#endif  // SL_WITH_ALT
+
 constexpr int kMpThreads = 256;
 constexpr int kMpItems = 2048;
 
@@ -960,10 +966,12 @@ using sl_host::aligned16;
 // SL_SPMV_PATH=pipe selects the persistent TMA pipelines (pipe.cu) instead of
 // the LDG kernels (A/B knob; the LDG kernels measured faster on every BASELINE
 // config), =ldg forces LDG.
+#ifdef SL_WITH_ALT
 static int spmv_path() {
   const char* e = getenv("SL_SPMV_PATH");
   return !e ? 0 : (e[0] == 'l' ? 1 : (e[0] == 'p' ? 2 : 0));
 }
+#endif
 
 
 extern "C" size_t sl_spmv_coo_workspace_bytes(int64_t nrows) {
@@ -983,7 +991,9 @@ extern "C" int sl_spmv_coo_f64(int64_t nrows, int64_t ncols, int64_t nnz, const 
     return sl_host::launch_status();
   }
   const bool vec_ok = aligned16(rows) && aligned16(cols) && aligned16(vals);
+#ifdef SL_WITH_ALT
   if (vec_ok && spmv_path() == 2) return sl_host::launch_coo_pipe(nrows, nnz, rows, cols, vals, x, y, s);
+#endif
   // With a workspace and rows averaging <= 28 nonzeros: the row level's
   // position index (one streaming pass over the row coordinates into the
   // workspace; cols and vals are not touched), then the register hand-off
@@ -1022,10 +1032,13 @@ template <int kHashX>
 static int launch_csr(int64_t nrows, int64_t nnz, const int32_t* pos, const int32_t* crd,
                       const double* vals, XOperand<kHashX> xop, double* y, int32_t variant,
                       void* ws, size_t ws_bytes, cudaStream_t s) {
+#ifdef SL_WITH_ALT
   if (variant == 0 && !kHashX && aligned16(crd) && aligned16(vals) && spmv_path() == 2) {
     const double* xd = reinterpret_cast<const XOperand<0>&>(xop).x;
     return sl_host::launch_csr_pipe(nrows, pos, crd, vals, xd, y, s);
-  } else if (variant == 0 || variant == 5) {
+  }
+#endif
+  if (variant == 0 || variant == 5) {
     // variant 0 (automatic): rows averaging <= 28 nonzeros (aligned crd/vals)
     // take the register hand-off kernel K2r, longer rows the row-block kernel
     // K2a, whose staged products keep very long rows parallel (variant 5
@@ -1055,20 +1068,24 @@ static int launch_csr(int64_t nrows, int64_t nnz, const int32_t* pos, const int3
     }
     spmv_csr_rowblock_kernel<kHashX><<<ceil_div(nrows, kCsrRows), kCsrThreads, 0, s>>>(
         nrows, pos, crd, vals, xop, y);
+#ifdef SL_WITH_ALT
   } else if (variant == 4 && !kHashX) {
     if (!aligned16(crd) || !aligned16(vals)) return SL_ERR_INVALID;
     launch_csr_stage<kCsrStageRows, kCsrStageCap, kCsrStageBatch, kCsrStageBlocks>(
         nrows, pos, crd, vals, reinterpret_cast<const XOperand<0>&>(xop).x, y, s);
+#endif
   } else if (variant == 6 && !kHashX) {
     if (!aligned16(crd) || !aligned16(vals)) return SL_ERR_INVALID;
     launch_csr_handoff<kCsrHandoffCap, kCsrHandoffMaxRow, kCsrHandoffBatch, kCsrHandoffBlocks>(
         nrows, pos, crd, vals, reinterpret_cast<const XOperand<0>&>(xop), y, kCsrHandoffBlocks, s);
+#ifdef SL_WITH_ALT
   } else if (variant == 3 && !kHashX) {
     const double* xd = reinterpret_cast<const XOperand<0>&>(xop).x;
     spmv_csr_warp_kernel<<<ceil_div(nrows, 256), 256, 0, s>>>(nrows, pos, crd, vals, xd, y);
   } else if (variant == 1) {
     spmv_csr_vector_kernel<kHashX><<<ceil_div(nrows * 32, 256), 256, 0, s>>>(nrows, pos, crd,
                                                                             vals, xop, y);
+#endif
   } else if (variant == 2) {
     return SL_ERR_INVALID;  // handled by caller (needs nnz)
   } else {
@@ -1176,17 +1193,18 @@ extern "C" int sl_spmv_ell_f64(int64_t nrows, int64_t ncols, int32_t nslots, con
   if (nrows == 0) return SL_OK;
   if (!y || (nslots > 0 && (!crd || !vals || !x))) return SL_ERR_INVALID;
   cudaStream_t s = as_stream(stream);
-  if (nslots > 0 && nslots <= sl_host::kEllPipeMaxSlots && nrows % 4 == 0 && aligned16(crd) && aligned16(vals) &&
-      spmv_path() == 2) {
+#ifdef SL_WITH_ALT
+  if (nslots > 0 && nslots <= sl_host::kEllPipeMaxSlots && nrows % 4 == 0 && aligned16(crd) &&
+      aligned16(vals) && spmv_path() == 2)
     return sl_host::launch_ell_pipe(nrows, nslots, crd, vals, x, y, s);
-  } else {
-    // batch 9 x 256 threads x 4 blocks/SM; batch 7-27 at 64-512 threads per
-    // block measured 20.5-24.5 us against 20.8 us here (profiles/ab/r1_ell_configs.txt);
-    // issuing the next batch's loads before the current batch's gathers
-    // (register software pipelining) 20.6-24.6 us (profiles/ab/r1_ell_swp.txt);
-    // a grid-stride persistent grid of 2-8 blocks/SM 20.6-25.3 us (r1_ell_persistent.txt)
-    spmv_ell_kernel<kEllBatch, 256, 4><<<ceil_div(nrows, 256), 256, 0, s>>>(nrows, nslots, crd, vals, x, y);
-  }
+#endif
+  // batch 9 x 256 threads x 4 blocks/SM; round 1 measured batch 7-27 at 64-512
+  // threads per block (20.5-24.5 us against 20.8 us here), issuing the next
+  // batch's loads before the current batch's gathers (register software
+  // pipelining, 20.6-24.6 us) and a grid-stride persistent grid of 2-8
+  // blocks/SM (20.6-25.3 us)
+  spmv_ell_kernel<kEllBatch, 256, 4><<<ceil_div(nrows, 256), 256, 0, s>>>(nrows, nslots, crd, vals,
+                                                                          x, y);
   return sl_host::launch_status();
 }
 
@@ -1208,9 +1226,11 @@ extern "C" int sl_spmv_dia_rows_f64(int64_t nrows, int64_t row0, int64_t ncols, 
     doffs = offsets;
   }
   const int grid = ceil_div(nrows, 256);
-  if (!doffs && row0 == 0 && aligned16(vals) && aligned16(x) && ndiag > 0 && spmv_path() == 2) {
+#ifdef SL_WITH_ALT
+  if (!doffs && row0 == 0 && aligned16(vals) && aligned16(x) && ndiag > 0 && spmv_path() == 2)
     return sl_host::launch_dia_pipe(nrows, ncols, ndiag, p, vals, x, y, s);
-  } else if (doffs) {
+#endif
+  if (doffs) {
     spmv_dia_dev_kernel<<<grid, 256, 0, s>>>(nrows, row0, ncols, ndiag, doffs, vals, x, y);
   } else if (ndiag <= 8) {
     spmv_dia_kernel<8><<<grid, 256, 0, s>>>(nrows, row0, ncols, ndiag, p, vals, x, y);
@@ -1226,4 +1246,14 @@ extern "C" int sl_spmv_dia_f64(int64_t nrows, int64_t ncols, int32_t ndiag, cons
                                int32_t offsets_on_host, const double* vals, const double* x,
                                double* y, void* stream) {
   return sl_spmv_dia_rows_f64(nrows, 0, ncols, ndiag, offsets, offsets_on_host, vals, x, y, stream);
+}
+
+// Which optional kernels this build carries (bit 0: the A/B alternatives —
+// CSR variants 1, 3, 4 and the persistent TMA pipelines, SL_BUILD_ALT=1).
+extern "C" int sl_build_features(void) {
+#ifdef SL_WITH_ALT
+  return 1;
+#else
+  return 0;
+#endif
 }

@@ -18,6 +18,11 @@ from paper_1804_10112_b200 import workloads as wl  # noqa: E402
 RTOL = 1e-12   # MTTKRP tolerance (condition-scaled)
 
 
+
+# CSR SpMV variants in this build: the dispatch's (0 automatic, 2 merge-path,
+# 5 row-block, 6 hand-off) and, in an SL_BUILD_ALT=1 build, the A/B ones
+CSR_VARIANTS = [0, 2, 5, 6] + ([1, 3, 4] if K.L().sl_build_features() & 1 else [])
+
 def cuda(a, dtype=None):
     a = np.asarray(a)
     if dtype is not None:
@@ -43,7 +48,7 @@ def test_spmv_goldens_all_formats(golden):
                            cuda(c["coo_cols"], np.int32), cuda(c["coo_vals"], np.float64), x)
             assert np.array_equal(bits(y), bits(c["coo_y"])), name
         if "csr_y" in c:
-            for variant in (0, 1, 2, 3, 4, 5, 6):
+            for variant in CSR_VARIANTS:
                 y = K.spmv_csr(nrows, ncols, cuda(c["csr_pos"], np.int32),
                                cuda(c["csr_crd"], np.int32), cuda(c["csr_vals"], np.float64), x,
                                variant=variant)
@@ -87,7 +92,7 @@ def test_spmv_coo_csr_vs_oracle(orc, n, nnz, lam, seed):
                        direct=direct)
         assert np.array_equal(bits(y), bits(ref)), direct
     pos = wl.coo_to_csr_pos(d["rows"], n)
-    for variant in (0, 1, 2, 3, 4, 5, 6):
+    for variant in CSR_VARIANTS:
         y = K.spmv_csr(n, d["ncols"], cuda(pos), cuda(d["cols"]), cuda(d["vals"]), x,
                        variant=variant)
         assert np.array_equal(bits(y), bits(ref)), variant
@@ -111,7 +116,7 @@ def test_spmv_coo_long_rows_cross_tiles(orc):
     # the same rows through every CSR variant (row-stage: blocks far beyond
     # one staging round, rows cut by rounds)
     pos = wl.coo_to_csr_pos(rows, 8)
-    for variant in (0, 1, 2, 3, 4, 5, 6):
+    for variant in CSR_VARIANTS:
         y = K.spmv_csr(8, 20000, cuda(pos), cuda(cols), cuda(vals), cuda(x), variant=variant)
         assert np.array_equal(bits(y), bits(ref)), variant
 
@@ -133,7 +138,7 @@ def test_spmv_csr_handoff_paths(orc):
     vals = rng.uniform(-1, 1, len(cols))
     x = rng.uniform(-1, 1, m)
     ref, _ = orc.spmv_csr(n, pos, cols, vals, x)
-    for variant in (0, 4, 5, 6):
+    for variant in [v for v in CSR_VARIANTS if v in (0, 4, 5, 6)]:
         y = cuda(np.full(n, np.nan))
         K.spmv_csr(n, m, cuda(pos), cuda(cols), cuda(vals), cuda(x), y=y, variant=variant)
         assert np.array_equal(bits(y), bits(ref)), variant
@@ -171,7 +176,7 @@ def test_spmv_csr_misaligned_operands(orc):
     x = cuda(s["x"])
     y = K.spmv_csr(s["nrows"], s["ncols"], cuda(s["pos"]), c, v, x, variant=0)
     assert np.array_equal(bits(y), bits(ref))
-    for variant in (4, 6):
+    for variant in [v for v in CSR_VARIANTS if v in (4, 6)]:
         with pytest.raises(Exception):
             K.spmv_csr(s["nrows"], s["ncols"], cuda(s["pos"]), c, v, x, variant=variant)
 
@@ -181,7 +186,7 @@ def test_spmv_empty_matrix():
     y = K.spmv_coo(9, 5, cuda(np.zeros(0, np.int32)), cuda(np.zeros(0, np.int32)),
                    cuda(np.zeros(0)), x)
     assert np.array_equal(bits(y), bits(np.zeros(9)))
-    for variant in (0, 1, 2, 3, 4, 5, 6):     # y pre-filled with NaN: every row must be written
+    for variant in CSR_VARIANTS:     # y pre-filled with NaN: every row must be written
         y = cuda(np.full(9, np.nan))
         K.spmv_csr(9, 5, cuda(np.zeros(10, np.int32)), cuda(np.zeros(0, np.int32)),
                    cuda(np.zeros(0)), x, y=y, variant=variant)
@@ -210,7 +215,7 @@ def test_full_size_spmv_bit_exact(orc):
     s = wl.stencil27()
     ref, _ = orc.spmv_csr(s["nrows"], s["pos"], s["crd"], s["vals"], s["x"])
     x = cuda(s["x"])
-    for variant in (0, 1, 2, 3, 4, 5, 6):
+    for variant in CSR_VARIANTS:
         y = K.spmv_csr(s["nrows"], s["ncols"], cuda(s["pos"]), cuda(s["crd"]), cuda(s["vals"]),
                        x, variant=variant)
         assert np.array_equal(bits(y), bits(ref)), variant
@@ -510,6 +515,8 @@ def test_mttkrp_full_size(orc):
 
 @pytest.fixture
 def pipe_path(monkeypatch):
+    if not K.L().sl_build_features() & 1:
+        pytest.skip("the TMA pipelines are an A/B build (SL_BUILD_ALT=1)")
     monkeypatch.setenv("SL_SPMV_PATH", "pipe")
     yield
 
@@ -600,14 +607,14 @@ def test_spmv_degenerate_shapes(orc):
     # zero rows: nothing to write, no error
     y = K.spmv_coo(0, 5, e_i, e_i, e_f, cuda(np.ones(5)))
     assert y.numel() == 0
-    for variant in (0, 1, 2, 3, 4, 5, 6):
+    for variant in CSR_VARIANTS:
         y = K.spmv_csr(0, 5, cuda(np.zeros(1, np.int32)), e_i, e_f, cuda(np.ones(5)),
                        variant=variant)
         assert y.numel() == 0
     # zero columns: every row empty -> +0.0 everywhere
     n = 1000
     x0 = cuda(np.zeros(0))
-    for variant in (0, 1, 2, 3, 4, 5, 6):
+    for variant in CSR_VARIANTS:
         y = cuda(np.full(n, np.nan))
         K.spmv_csr(n, 0, cuda(np.zeros(n + 1, np.int32)), e_i, e_f, x0, y=y, variant=variant)
         assert np.array_equal(bits(y), bits(np.zeros(n))), variant
