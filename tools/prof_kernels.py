@@ -67,9 +67,10 @@ def main():
         rr = T(np.repeat(np.arange(n, dtype=np.int32), np.diff(s["pos"])))
         jobs["coo_st"] = (16 * len(s["crd"]) + 16 * n,
                           lambda: K.spmv_coo(n, n, rr, c, v, x, y))
-        jobs["csr_vec"] = (bc, lambda: K.spmv_csr(n, n, p, c, v, x, y, variant=1))
         jobs["csr_merge"] = (bc, lambda: K.spmv_csr(n, n, p, c, v, x, y, variant=2))
-        jobs["csr_warp"] = (bc, lambda: K.spmv_csr(n, n, p, c, v, x, y, variant=3))
+        if K.L().sl_build_features() & 1:     # A/B build (SL_BUILD_ALT=1) only
+            jobs["csr_vec"] = (bc, lambda: K.spmv_csr(n, n, p, c, v, x, y, variant=1))
+            jobs["csr_warp"] = (bc, lambda: K.spmv_csr(n, n, p, c, v, x, y, variant=3))
         for Kc in (4, 16, 32):
             Xd = torch.rand((n, Kc), dtype=torch.float64, device=dev)
             Yd = torch.empty((n, Kc), dtype=torch.float64, device=dev)
