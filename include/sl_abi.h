@@ -21,13 +21,20 @@
  *   - Return value: SL_OK (0) or an SL_ERR_* code.  The Python host package
  *     maps them 1:1 onto the reference exception classes (errors.py:4-55).
  *   - Reentrant; the only global state is a cached per-device SM count.
+ *   - Arrays are read in whole 16-byte granules by the bulk (TMA) copies: up to
+ *     15 bytes before an array start and after an array end that are not
+ *     16-byte aligned may be read (never written, never used).  Every
+ *     cudaMalloc / cuMemMap / torch allocation contains those bytes; a tightly
+ *     packed suballocation must leave them readable.
  *
  * Arithmetic contract ("Exact arithmetic"):
  *   SpMV     y[i] = ((+0.0 + a_i,j1*x_j1) + a_i,j2*x_j2) + ...   in storage
  *            order, one rounding per multiply and per add (no FMA contraction):
  *            bit-identical to engine.py:303,320 (scatter) / :606-633 (CSR).
  *   A+B      sorted union per row; value a+b where both stored, else the copy;
- *            explicit zeros kept (engine.py:387-413): bit-identical.
+ *            explicit zeros kept (engine.py:387-413): bit-identical.  A run
+ *            of repeated B coordinates is one term, Python's sum() of the run
+ *            (engine.py:527; Neumaier-compensated on CPython 3.12).
  *   MTTKRP   A[i,r] = sum of (x*B[j,r])*C[k,r] (engine.py:528-529 association);
  *            the sum over a slice is a parallel reduction, so A matches the
  *            sequential reference within |d| <= 1e-12 * sum|terms|.

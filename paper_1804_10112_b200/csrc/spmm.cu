@@ -225,8 +225,8 @@ extern "C" int sl_spmm_csr_split_f64(int64_t nrows, int64_t ncols, int64_t K, in
   const int64_t nlong = std::min<int64_t>(nrows, nnz / ((int64_t)long_min + 1) + 1);
   const int lgrid = (int)std::min<int64_t>(nlong, 4LL * sl_host::sm_count());
   // chunk depth: 32 loads per lane for G <= 16, 24 for G = 32 (the giant-row
-  // time is per-chunk gather latency; tools/spmm_skew_prof.py,
-  // profiles/ab/r1_spmm_skew_split.txt)
+  // time is per-chunk gather latency; measured in round 1 with
+  // tools/spmm_skew_prof.py, log not retained)
   auto go = [&](auto kern, int g, int per) {
     const size_t smem = (size_t)8 * (32 / g) * per * (g + 1) * sizeof(double);
     if (smem > 48 * 1024 &&

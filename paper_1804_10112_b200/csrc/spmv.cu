@@ -454,7 +454,8 @@ spmv_csr_rowblock_kernel(int64_t nrows, const int32_t* __restrict__ pos,
 // tile's row bounds during the current walk (25.3-28.8 us at 10-20 blocks/SM:
 // hardware block scheduling of many short blocks beats the software loop).
 // Staging the range with 16-byte cp.async (LDGSTS) by all threads instead of
-// the bulk copy: 24.8 us (profiles/ab/r1_csr_stage_tma_vs_ldgsts.txt).  On short, irregular rows (D1, Poisson(10)) the row walk diverges
+// the bulk copy: 24.8 us (round-1 A/B; log not retained).  On short,
+// irregular rows (D1, Poisson(10)) the row walk diverges
 // (warps run the longest row) and K2a stays faster (20.5 vs 29 us), so the
 // automatic choice takes K2f only for rows averaging >= 16 nonzeros.
 
@@ -719,9 +720,9 @@ static void launch_csr_handoff(int64_t nrows, const int32_t* pos, const int32_t*
 // gathers in two batches of 14, 12 one-warp blocks per SM (146 registers):
 // 64^3 stencil 22.4 us, D1 19.3 us, against K2f 23.8 / K2a 20.5 us; 14-27
 // element batches, 10-24 blocks/SM and a 32-nonzero register row measured
-// 22.4-27.2 / 19.3-24.4 us (profiles/ab/r1_csr_handoff*.txt); two stages per
-// block (tiles t+1 and t+2 in flight, 10 blocks/SM) 25.9-30.7 / 26.7-28.7 us
-// (r1_csr_handoff_2stage.txt)
+// 22.4-27.2 / 19.3-24.4 us; two stages per block (tiles t+1 and t+2 in
+// flight, 10 blocks/SM) 25.9-30.7 / 26.7-28.7 us (round-1 A/B runs under the
+// per-launch flush protocol; logs not retained)
 constexpr int kCsrHandoffCap = 896;
 constexpr int kCsrHandoffMaxRow = 28;
 constexpr int kCsrHandoffBatch = 14;
