@@ -174,6 +174,12 @@ class LevelStorage:
         self.spec = spec
         self._sl_max_row = None   # (pos, heaviest 32-row tile): engine's CSR variant choice, cached
         self.n, self.m, self.w = int(n), int(m), int(w)
+        # the reference defaults pos / crd to [] (levels.py:185-186): position
+        # iterated levels always carry (possibly empty) arrays here too
+        if spec.kind in (LevelKind.COMPRESSED, LevelKind.SINGLETON, LevelKind.HASHED):
+            crd = [] if crd is None else crd
+            if spec.kind is LevelKind.COMPRESSED:
+                pos = [] if pos is None else pos
         self.pos = _as_i32(pos, device)
         self.crd = _as_i32(crd, device)
         self.offset = _as_i32(offset, device)

@@ -147,9 +147,13 @@ class Pack:
 
 
 def fmt_desc(v):
-    tag, name, flags, _ = v
-    return {"preset": name, "tag": tag,
-            "levels": {k: {f: bool(b) for f, b in fl.items()} for k, fl in flags.items()}}
+    tag, name, flags, f = v
+    d = {"preset": name, "tag": tag,
+         "levels": {k: {f: bool(b) for f, b in fl.items()} for k, fl in flags.items()}}
+    if f.hash_width:
+        d["width"] = int(f.hash_width)
+        d["tag"] = f"{tag},w={f.hash_width}"
+    return d
 
 
 def run_case(pack, cases, pattern, expr, ops, out, fuse, dims_of, rng):
@@ -276,6 +280,41 @@ def sweep():
             run_case(pack, cases, "add", "C(i,j) = A(i,j) + B(i,j)",
                      {"A": primary("csr"), "B": primary(ab)}, dh, fuse,
                      {"A": (6, 7), "B": (6, 7)}, rng)
+
+    # ---- edge cases: empty operands and pinned hashed widths (too small ->
+    # HashSegmentFullError in the reference, exactly full, roomy)
+    def empty_case(pattern, expr, ops, out, dims_of):
+        inputs = {n: sl.assemble(v[3], tuple(dims_of[n]), sl.CoordList(tuple(dims_of[n]), []))
+                  for n, v in ops.items()}
+        case = {"pattern": pattern, "expr": expr, "fuse": True,
+                "inputs": {n: pack.storage(st, fmt_desc(ops[n])) for n, st in inputs.items()},
+                "absdense": {n: pack.arr(abs_dense(st), np.float64) for n, st in inputs.items()},
+                "out_format": None if out is None else fmt_desc(out)}
+        stats = EvalStats()
+        try:
+            res = sl.evaluate(expr, inputs, None if out is None else out[3], stats=stats)
+            case["result"] = pack.storage(res, case["out_format"])
+            case["by_loop"] = [[k[0], k[1], int(v)] for k, v in stats.by_loop.items()]
+        except sl.SparseLevelsError as e:
+            case["error"] = type(e).__name__
+        cases.append(case)
+
+    d3 = {"X": (4, 5, 6), "Z": (4, 5, 6)}
+    for o in ("coo-3", "csf", "dense-3"):
+        empty_case("plus3", "A(i,j,k) = X(i,j,k) + Z(i,j,k)", {"X": c3, "Z": c3}, primary(o), d3)
+    empty_case("ttv", "Y(i,j) = X(i,j,k) * v(k)", {"X": c3, "v": primary("dense")}, None,
+               {"X": (4, 5, 6), "v": (6,)})
+    empty_case("spmm", "Y(i,k) = A(i,j) * X(j,k)", {"A": primary("coo-soa"), "X": d2}, hd,
+               {"A": (6, 7), "X": (7, 3)})
+    for width in (2, 4, 8, 64):
+        hdw = ("base", "custom:hd", {}, dataclasses.replace(custom("custom:hd"), hash_width=width))
+        dhw = ("base", "custom:dh", {}, dataclasses.replace(custom("custom:dh"), hash_width=width))
+        run_case(pack, cases, "mttkrp", "A(i,r) = X(i,j,k) * B(j,r) * C(k,r)",
+                 {"X": primary("coo-3"), "B": d2, "C": d2}, hdw, True,
+                 {"X": (4, 5, 6), "B": (5, 3), "C": (6, 3)}, rng)
+        run_case(pack, cases, "add", "C(i,j) = A(i,j) + B(i,j)",
+                 {"A": primary("csr"), "B": primary("coo-soa")}, dhw, True,
+                 {"A": (6, 7), "B": (6, 7)}, rng)
 
     # ---- TTV Y(i,j) = X(i,j,k) * v(k), TTM Y(i,j,r) = X(i,j,k) * U(k,r)
     for fuse in fuses:

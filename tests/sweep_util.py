@@ -52,6 +52,8 @@ def fmt(desc):
                           name=desc["preset"])
     else:
         f = slb.preset(desc["preset"])
+    if desc.get("width"):
+        f = dataclasses.replace(f, hash_width=desc["width"])
     levels = list(f.levels)
     for k, flags in desc["levels"].items():
         spec = levels[int(k)]

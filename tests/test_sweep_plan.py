@@ -22,9 +22,14 @@ def _plan(case, inputs):
                                fuse=case["fuse"])
 
 
+# raised by the reference while executing (a full hashed segment): the
+# planner cannot know; the GPU sweep checks that `evaluate` raises them too
+RUNTIME_ERRORS = {"HashSegmentFullError"}
+
+
 def test_rejected_by_reference_rejected_here():
     for i, case in CASES:
-        if "error" not in case:
+        if "error" not in case or case["error"] in RUNTIME_ERRORS:
             continue
         with pytest.raises(slb.SparseLevelsError):
             _plan(case, su.inputs(case, "cpu"))
