@@ -729,6 +729,25 @@ def run_formats(torch, K, F, wl, evaluate, dev, timer, peak, l2, clk, steps):
                                    "frac": round(b_spx / t / 1e6 / peak, 4), "bytes": b_spx,
                                    "x_nnz": int(len(keep))}
     del mops, xops, sws
+    # the paper's SpDM on COO (row pointer per call + SpMM), D1's matrix, K = 16
+    dd = wl.coo_spmv()
+    nd, md, nnzd = dd["nrows"], dd["ncols"], len(dd["rows"])
+    Xc = rng.uniform(-1, 1, (md, Kc))
+    b_sd = 16 * nnzd + 8 * md * Kc + 8 * nd * Kc
+    sdops = dev_copies(torch, (dd["rows"], dd["cols"], dd["vals"], Xc, np.empty((nd, Kc))),
+                       copies_for(b_sd, l2), dev)
+
+    def spdm(o):
+        pos = K.coo_rowptr(nd, o[0])
+        K.spmm_csr(nd, md, pos, o[1], o[2], o[3], o[4])
+
+    with clk.timed("formats"):
+        tt = timer.run({"spdm": [lambda o=o: spdm(o) for o in sdops]}, steps, 3)
+    t = tt["spdm"]
+    res["spdm_coo_D1_K16"] = {"ms": round(t, 5), "GB/s": round(b_sd / t / 1e6, 1),
+                              "frac": round(b_sd / t / 1e6 / peak, 4), "bytes": b_sd,
+                              "GFLOP/s": round(2 * nnzd * Kc / t / 1e6, 1)}
+    del sdops
 
     # ---- D3: DIA SpMV
     g = wl.dia7()
@@ -902,6 +921,28 @@ def run_formats(torch, K, F, wl, evaluate, dev, timer, peak, l2, clk, steps):
     res["innerprod_coo3_D5"] = {"ms": round(t, 4), "GB/s": round(b_in / t / 1e6, 1),
                                 "frac": round(b_in / t / 1e6 / peak, 4), "bytes": b_in,
                                 "nnz/s": round(nnz / t * 1e3, 1)}
+
+    # 3rd-order PLUS through `evaluate`: X = D5 (COO-3) plus Z =
+    # every other nonzero of it with new values, into COO-3
+    X_st = F.coo3_storage(ti, tj, tk, tv, (I, J, Kd), device=dev)
+    Z_st = F.coo3_storage(ti[::2].contiguous(), tj[::2].contiguous(), tk[::2].contiguous(),
+                          (tv[::2] * 0.5).contiguous(), (I, J, Kd), device=dev)
+    out = {}
+
+    def plus3():
+        out["c"] = evaluate("A(i,j,k) = X(i,j,k) + Z(i,j,k)", {"X": X_st, "Z": Z_st},
+                            F.preset("coo-3"))
+
+    with clk.timed("formats"):
+        tt = timer.run({"plus3": [plus3, plus3]}, 3, 1)
+    nz_c = int(out["c"].levels[2].crd.numel())
+    b_p = 20 * nnz + 20 * (nnz // 2) + 20 * nz_c
+    res["plus3_coo3_D5"] = {"ms": round(tt["plus3"], 4), "GB/s": round(b_p / tt["plus3"] / 1e6, 1),
+                            "frac": round(b_p / tt["plus3"] / 1e6 / peak, 4), "bytes": b_p,
+                            "nnz_c": nz_c, "launch": timer.method.get("plus3"),
+                            "path": "evaluate(): union of the operands' fibres, the A + B kernels "
+                                    "over (fibre x k); host syncs for the output sizes"}
+    del X_st, Z_st, out
     return res
 
 

@@ -329,6 +329,91 @@ SL_DEV int block_incl_scan(int v, int* s_warp, int* total) {
   return before + incl;
 }
 
+// One row beyond the stage, merged by the whole block (merge path): thread t
+// takes diagonals [t E, (t + 1) E) of the row's merged sequence (A first on
+// ties), found by one binary search along the diagonal, and walks them from
+// global memory (L1 catches each thread's sequential reads).  An output
+// starts at an item whose column differs from the item before it; its owner
+// (the thread holding that item) reads ahead through B's run of the column,
+// even past its segment, and the items of a run inside another thread's
+// segment are skipped there.  Count mode returns the row's output count
+// (every thread); fill mode writes the outputs at oc / ov, 0 + (a + g | a | g)
+// with g Python's sum() of B's run.  O((|A| + |B|) / 128 + log) per thread,
+// whatever the row's shape (repeated B coordinates included).
+template <bool kFill>
+SL_DEV int merge_long_row(int32_t a0, int32_t a1, int32_t b0, int32_t b1,
+                          const int32_t* __restrict__ a_crd, const double* __restrict__ a_vals,
+                          const int32_t* __restrict__ b_cols, const double* __restrict__ b_vals,
+                          int32_t* oc, double* ov, int* s_warp) {
+  const int tid = threadIdx.x;
+  const int na = a1 - a0, nb = b1 - b0, T = na + nb;
+  const int E = (T + blockDim.x - 1) / blockDim.x;
+  const int d0 = min(T, tid * E), d1 = min(T, d0 + E);
+  int lo = max(0, d0 - nb), hi = min(d0, na);
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (ldg(a_crd + a0 + mid) <= ldg(b_cols + b0 + d0 - mid - 1)) lo = mid + 1; else hi = mid;
+  }
+  const int ia0 = lo, ib0 = d0 - lo;
+  int32_t before = -1;                      // column of the item before diagonal d0
+  if (d0 > 0) {
+    const int32_t la = ia0 > 0 ? ldg(a_crd + a0 + ia0 - 1) : -1;
+    const int32_t lb = ib0 > 0 ? ldg(b_cols + b0 + ib0 - 1) : -1;
+    before = max(la, lb);
+  }
+  int cnt = 0;
+  {
+    int pa = ia0, pb = ib0;
+    int32_t last = before;
+    for (int d = d0; d < d1; ++d) {
+      const int32_t ca = pa < na ? ldg(a_crd + a0 + pa) : INT32_MAX;
+      const int32_t cb = pb < nb ? ldg(b_cols + b0 + pb) : INT32_MAX;
+      const bool ta = ca <= cb;
+      const int32_t c = ta ? ca : cb;
+      cnt += c != last;
+      last = c;
+      pa += ta;
+      pb += !ta;
+    }
+  }
+  int total;
+  const int incl = block_incl_scan(cnt, s_warp, &total);
+  if (!kFill) {
+    __syncthreads();                        // s_warp reused by the caller
+    return total;
+  }
+  int q = incl - cnt;
+  int pa = ia0, pb = ib0;
+  int32_t last = before;
+  for (int d = d0; d < d1; ++d) {
+    const int32_t ca = pa < na ? ldg(a_crd + a0 + pa) : INT32_MAX;
+    const int32_t cb = pb < nb ? ldg(b_cols + b0 + pb) : INT32_MAX;
+    const bool ta = ca <= cb;
+    const int32_t c = ta ? ca : cb;
+    if (c != last) {                        // this thread owns the output of column c
+      const double a = ta ? ldg(a_vals + a0 + pa) : 0.0;
+      int u = ta ? pb : pb;                 // B's run of c starts at pb either way
+      double g = 0.0;
+      int nbr = 0;
+      PySum ps;
+      for (; u < nb && ldg(b_cols + b0 + u) == c; ++u, ++nbr) {
+        const double bv = ldg(b_vals + b0 + u);
+        if (nbr == 0) g = bv; else { if (nbr == 1) ps.start(g); ps.add(bv); }
+      }
+      if (nbr > 1) g = ps.value();
+      const double e = ta ? (nbr ? dadd(a, g) : a) : g;
+      oc[q] = c;
+      ov[q] = dadd(0.0, e);
+      ++q;
+    }
+    last = c;
+    pa += ta;
+    pb += !ta;
+  }
+  __syncthreads();
+  return total;
+}
+
 // exclusive prefix of all tile totals before `tile` (one warp; lane 0 result)
 SL_DEV int64_t tile_prefix(int64_t tile, const int64_t* tile_tot, const int64_t* super_tot) {
   const int lane = threadIdx.x & 31;
@@ -505,27 +590,14 @@ add_tile_kernel(int64_t nrows, const int32_t* __restrict__ a_pos, const int32_t*
         __syncthreads();                   // counts written, stage free
         g0 = g1;
       }
-      // rows alone beyond the stage: the block counts each one element-parallel
-      // (a B entry adds a coordinate unless it repeats its predecessor or is
-      // found in A's row by binary search)
+      // rows alone beyond the stage: merged by the whole block (merge path)
       const bool any_big = __syncthreads_or(mine && oversized(tid));
       for (int r = 0; any_big && r < nr; ++r) {
         if (!oversized(r)) continue;
-        const int32_t a0 = s_apos[r], a1 = s_apos[r + 1], b0 = s_bpos[r], b1 = s_bpos[r + 1];
-        if (tid == 0) s_g1 = 0;
-        __syncthreads();
-        int fresh = 0;
-        for (int32_t j = b0 + tid; j < b1; j += kAddRows) {
-          const int32_t c = ldg(b_cols + j);
-          const bool dup = j > b0 && ldg(b_cols + j - 1) == c;
-          if (!dup) {
-            const int32_t p = lower_bound_g(a_crd, a0, a1, c);
-            fresh += !(p < a1 && ldg(a_crd + p) == c);
-          }
-        }
-        if (fresh) atomicAdd(&s_g1, fresh);
-        __syncthreads();
-        if (tid == 0) s_rbase[r] = (a1 - a0) + s_g1;
+        const int n = merge_long_row<false>(s_apos[r], s_apos[r + 1], s_bpos[r], s_bpos[r + 1],
+                                            a_crd, nullptr, b_cols, nullptr, nullptr, nullptr,
+                                            s_warp);
+        if (tid == 0) s_rbase[r] = n;
         __syncthreads();
       }
       cnt = mine ? s_rbase[tid] : 0;
@@ -601,61 +673,13 @@ add_tile_kernel(int64_t nrows, const int32_t* __restrict__ a_pos, const int32_t*
       __syncthreads();                     // stages free for the next group
       g0 = g1;
     }
-    // rows alone beyond the stage: element-parallel by the block when B's row
-    // has no repeated coordinate (a match is emitted once, by A's entry, as
-    // 0 + (a + b)), else merged by one thread from global memory
+    // rows alone beyond the stage: merged by the whole block (merge path)
     const bool any_big = __syncthreads_or(mine && oversized(tid));
     for (int r = 0; any_big && r < nr; ++r) {
       if (!oversized(r)) continue;
-      const int32_t a0 = s_apos[r], a1 = s_apos[r + 1], b0 = s_bpos[r], b1 = s_bpos[r + 1];
-      int32_t* oc = c_crd + tile_out + s_rbase[r];
-      double* ov = c_vals + tile_out + s_rbase[r];
-      bool dup = false;
-      for (int32_t j = b0 + 1 + tid; j < b1; j += kAddRows)
-        dup |= ldg(b_cols + j) == ldg(b_cols + j - 1);
-      if (__syncthreads_or(dup)) {
-        if (tid == 0)
-          merge_row<true>(a0, a1, b0, b1, gacc, FillEmit{oc, ov});
-        continue;
-      }
-      // slot of an entry = (its rank in its row) + (the other row's entries
-      // below it) - (matched pairs below it); the matched pairs below an entry
-      // are the matched entries before it in its own row: a running block scan
-      int carry = 0;
-      for (int32_t i0 = a0; i0 < a1; i0 += kAddRows) {
-        const int32_t i = i0 + tid;
-        const bool in = i < a1;
-        const int32_t c = in ? ldg(a_crd + i) : 0;
-        const int32_t lb = in ? lower_bound_g(b_cols, b0, b1, c) : b0;
-        const bool m = in && lb < b1 && ldg(b_cols + lb) == c;
-        int tot;
-        const int before = carry + block_incl_scan(m ? 1 : 0, s_warp, &tot) - (m ? 1 : 0);
-        if (in) {
-          const int32_t q = (i - a0) + (lb - b0) - before;
-          const double a = ldg(a_vals + i);
-          oc[q] = c;
-          ov[q] = dadd(0.0, m ? dadd(a, ldg(b_vals + lb)) : a);
-        }
-        carry += tot;
-        __syncthreads();                   // s_warp reused by the next round's scan
-      }
-      carry = 0;
-      for (int32_t j0 = b0; j0 < b1; j0 += kAddRows) {
-        const int32_t j = j0 + tid;
-        const bool in = j < b1;
-        const int32_t c = in ? ldg(b_cols + j) : 0;
-        const int32_t la = in ? lower_bound_g(a_crd, a0, a1, c) : a0;
-        const bool m = in && la < a1 && ldg(a_crd + la) == c;
-        int tot;
-        const int before = carry + block_incl_scan(m ? 1 : 0, s_warp, &tot) - (m ? 1 : 0);
-        if (in && !m) {                    // a matched entry was emitted with A's
-          const int32_t q = (la - a0) + (j - b0) - before;
-          oc[q] = c;
-          ov[q] = dadd(0.0, ldg(b_vals + j));
-        }
-        carry += tot;
-        __syncthreads();
-      }
+      merge_long_row<true>(s_apos[r], s_apos[r + 1], s_bpos[r], s_bpos[r + 1], a_crd, a_vals,
+                           b_cols, b_vals, c_crd + tile_out + s_rbase[r],
+                           c_vals + tile_out + s_rbase[r], s_warp);
     }
     return;
   }

@@ -233,9 +233,6 @@ def _plan(checked: CheckedExpr, bindings, out_format: TensorFormat,
                 if ocls not in ("coo3", "csf", "dense3"):
                     raise UnsupportedOutputError(
                         f"PLUS output must be COO-3, CSF or dense-3; got {out_format.describe()}")
-                I_, J_, _ = bindings[L_.tensor][1]
-                if I_ * J_ > 2 ** 31 - 2:
-                    raise UnsupportedMergeError("PLUS: I x J fibre keys exceed int32")
                 return Plan("plus3", f"plus3_{ocls}", {"X": L_.tensor, "Z": R_.tensor},
                             out_format, out_dims, ivars=lhs.ivars)
             raise UnsupportedMergeError(f"no B200 kernel for PLUS with {cl} + {cr}")
@@ -448,34 +445,34 @@ def _coo3_fibres(X: TensorStorage):
 def _coo3_grouped(X: TensorStorage):
     """CSF-shaped levels and values of a COO-3 whose repeated (i, j, k) are
     grouped (Grouped, engine.py:107-149: one visit, Python's sum() of the
-    run): the exact copy of the (fibre key x k) matrix, its non-empty rows
-    being the fibres."""
+    run): the exact copy of the (fibre x k) matrix whose rows are X's
+    distinct fibres (keys i*J + j, located by searchsorted)."""
     I, J, Kd = X.dims
     key, kc, v = _fibre_coo(X)
-    pos, crd, vals = K.coo_to_csr(I * J, key, kc, v)
+    fk = torch.unique_consecutive(key) if key.numel() else key
+    rows = torch.searchsorted(fk, key).to(torch.int32)
+    pos, crd, vals = K.coo_to_csr(int(fk.numel()), rows, kc, v)
     dev = vals.device
-    cnt = pos[1:] - pos[:-1]
-    fib = torch.nonzero(cnt > 0).squeeze(1)
-    fi = (fib // J).to(torch.int32)
-    sst = torch.ones(fib.numel(), dtype=torch.bool, device=dev)
-    if fib.numel():
+    fi = (fk // J).to(torch.int32)
+    sst = torch.ones(fk.numel(), dtype=torch.bool, device=dev)
+    if fk.numel():
         sst[1:] = fi[1:] != fi[:-1]
     spos = torch.nonzero(sst).squeeze(1)
     end = lambda t, n: torch.cat([t.to(torch.int64), torch.tensor([n], device=dev)]).to(  # noqa: E731
         torch.int32)
     return [LevelStorage(X.levels[0].spec, crd=fi[spos], device=dev),
-            LevelStorage(X.levels[1].spec, pos=end(spos, fib.numel()),
-                         crd=(fib % J).to(torch.int32), device=dev),
-            LevelStorage(X.levels[2].spec, pos=torch.cat([pos[fib], pos[-1:]]), crd=crd,
-                         device=dev)], vals
+            LevelStorage(X.levels[1].spec, pos=end(spos, fk.numel()),
+                         crd=(fk % J).to(torch.int32), device=dev),
+            LevelStorage(X.levels[2].spec, pos=pos, crd=crd, device=dev)], vals
 
 
 def _fibre_coo(X: TensorStorage):
-    """(fibre key i*J + j, k, vals) of a COO-3 or CSF operand, storage order."""
+    """(fibre key i*J + j as int64, k, vals) of a COO-3 or CSF operand, in
+    storage order."""
     J = X.dims[1]
     if format_class(X.format) == "coo3":
         key = X.levels[0].crd.to(torch.int64) * J + X.levels[1].crd.to(torch.int64)
-        return key.to(torch.int32), X.levels[2].crd, X.vals[:X.levels[2].crd.numel()]
+        return key, X.levels[2].crd, X.vals[:X.levels[2].crd.numel()]
     L = X.levels
     n1 = int(L[1].crd.numel())
     nnz = int(L[2].crd.numel())
@@ -485,56 +482,55 @@ def _fibre_coo(X: TensorStorage):
     fkey = L[0].crd.to(torch.int64)[fs] * J + L[1].crd.to(torch.int64)
     leaf_f = torch.repeat_interleave(torch.arange(n1, device=dev),
                                      (L[2].pos[1:] - L[2].pos[:-1]).to(torch.int64))
-    return fkey[leaf_f].to(torch.int32), L[2].crd, X.vals[:nnz]
+    return fkey[leaf_f], L[2].crd, X.vals[:nnz]
 
 
 def _plus3(p: Plan, X: TensorStorage, Z: TensorStorage, dev) -> TensorStorage:
-    """A(i,j,k) = X(i,j,k) + Z(i,j,k): the rows of the 2-D union are the (i, j)
-    fibres (keys i*J + j, in storage order), its columns k — the same
-    gather-append union and duplicate grouping as A + B (X's exact grouped
-    copy, Z's repeats grouped by the kernels; engine.py:107-149, 330-434)."""
+    """A(i,j,k) = X(i,j,k) + Z(i,j,k): the rows of the 2-D union are the
+    union of the operands' (i, j) fibres (sorted keys i*J + j; each nonzero's
+    row located by searchsorted), its columns k — the same gather-append
+    union and duplicate grouping as A + B (X's exact grouped copy, Z's
+    repeats grouped by the kernels; engine.py:107-149, 330-434)."""
     I, J, Kd = X.dims
-    nkey = I * J
-    xr, xc, xv = _fibre_coo(X)
-    zr, zc, zv = _fibre_coo(Z)
-    a_pos, a_crd, a_vals = K.coo_to_csr(nkey, xr, xc, xv)
-    c_pos, c_crd, c_vals = K.add_csr(nkey, a_pos, a_crd, a_vals, zc, zv, b_rows=zr)
+    xk, xc, xv = _fibre_coo(X)
+    zk, zc, zv = _fibre_coo(Z)
+    uq = lambda t: torch.unique_consecutive(t) if t.numel() else t  # noqa: E731
+    U = torch.unique(torch.cat([uq(xk), uq(zk)]))                   # sorted fibre keys
+    nU = int(U.numel())
+    xr = torch.searchsorted(U, xk).to(torch.int32)
+    zr = torch.searchsorted(U, zk).to(torch.int32)
+    a_pos, a_crd, a_vals = K.coo_to_csr(nU, xr, xc, xv)
+    c_pos, c_crd, c_vals = K.add_csr(nU, a_pos, a_crd, a_vals, zc, zv, b_rows=zr)
     f = p.out_format
     ocls = format_class(f)
     nnz = int(c_crd.numel())
+    fi, fj = (U // J).to(torch.int32), (U % J).to(torch.int32)
     if ocls == "dense3":
         out = torch.zeros(I * J * Kd, dtype=torch.float64, device=dev)
         if nnz:
-            rows = K.csr_rows(nkey, c_pos, nnz).to(torch.int64)
-            out[rows * Kd + c_crd.to(torch.int64)] = c_vals
+            rows = K.csr_rows(nU, c_pos, nnz).to(torch.int64)
+            out[U[rows] * Kd + c_crd.to(torch.int64)] = c_vals
         return TensorStorage(f, (I, J, Kd), [LevelStorage(s_, n=d, device=dev)
                                              for s_, d in zip(f.levels, (I, J, Kd))], out)
-    rows = K.csr_rows(nkey, c_pos, nnz).to(torch.int64) if nnz else \
-        torch.empty(0, dtype=torch.int64, device=dev)
-    ci, cj = (rows // J).to(torch.int32), (rows % J).to(torch.int32)
     if ocls == "coo3":
-        return TensorStorage(f, (I, J, Kd), [LevelStorage(f.levels[0], pos=[0, nnz], crd=ci,
+        rows = K.csr_rows(nU, c_pos, nnz).to(torch.int64) if nnz else \
+            torch.empty(0, dtype=torch.int64, device=dev)
+        return TensorStorage(f, (I, J, Kd), [LevelStorage(f.levels[0], pos=[0, nnz], crd=fi[rows],
                                                           device=dev),
-                                             LevelStorage(f.levels[1], crd=cj, device=dev),
+                                             LevelStorage(f.levels[1], crd=fj[rows], device=dev),
                                              LevelStorage(f.levels[2], crd=c_crd, device=dev)],
                              c_vals)
-    # CSF: the non-empty fibres, their slices
-    cnt = c_pos[1:] - c_pos[:-1]
-    fib = torch.nonzero(cnt > 0).squeeze(1)
-    fi = (fib // J).to(torch.int32)
-    sst = torch.ones(fib.numel(), dtype=torch.bool, device=dev)
-    if fib.numel():
+    # CSF: every union fibre holds an entry; slices are the runs of equal i
+    sst = torch.ones(nU, dtype=torch.bool, device=dev)
+    if nU:
         sst[1:] = fi[1:] != fi[:-1]
     spos = torch.nonzero(sst).squeeze(1)
     end = lambda t, v: torch.cat([t.to(torch.int64), torch.tensor([v], device=dev)]).to(  # noqa: E731
         torch.int32)
     return TensorStorage(f, (I, J, Kd), [
         LevelStorage(f.levels[0], pos=[0, int(spos.numel())], crd=fi[spos], device=dev),
-        LevelStorage(f.levels[1], pos=end(spos, fib.numel()), crd=(fib % J).to(torch.int32),
-                     device=dev),
-        LevelStorage(f.levels[2], pos=torch.cat([c_pos[fib], c_pos[-1:]]), crd=c_crd,
-                     device=dev)],
-        c_vals)
+        LevelStorage(f.levels[1], pos=end(spos, nU), crd=fj, device=dev),
+        LevelStorage(f.levels[2], pos=c_pos, crd=c_crd, device=dev)], c_vals)
 
 
 _SKEW_TILE = 4 * 896   # 32-row tiles heavier than four hand-off stages: merge-path

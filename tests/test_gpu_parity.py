@@ -704,3 +704,42 @@ def test_add_dense_and_power_law_rows(orc, lam, zipf, seed):
         assert np.array_equal(pos.cpu().numpy(), rp), two_pass
         assert np.array_equal(crd.cpu().numpy(), rc), two_pass
         assert np.array_equal(bits(vals), bits(rv)), two_pass
+
+
+@pytest.mark.parametrize("seed", [3, 4])
+def test_add_long_rows_with_matches_and_repeats(orc, seed):
+    """Rows far beyond the stage whose B part matches A's columns and repeats
+    coordinates (runs of up to 4): the block-cooperative merge path, B runs
+    summed as Python's sum() (Neumaier), owners reading ahead across thread
+    segments."""
+    rng = np.random.default_rng(seed)
+    n, m = 3000, 50_000
+    la = rng.poisson(4, n)
+    lb = rng.poisson(4, n)
+    long_rows = rng.choice(n, 12, replace=False)
+    la[long_rows] = rng.integers(800, 6000, 12)
+    lb[long_rows] = rng.integers(800, 6000, 12)
+    a_cols, b_cols, b_rows = [], [], []
+    for r in range(n):
+        ac = np.sort(rng.choice(m, int(la[r]), replace=False))
+        share = ac[rng.random(len(ac)) < 0.3] if len(ac) else ac[:0]
+        own = rng.choice(m, int(lb[r]), replace=True)
+        bc = np.concatenate([share, own])
+        reps = rng.integers(1, 5, len(bc)) * (rng.random(len(bc)) < 0.2) + 1
+        bc = np.sort(np.repeat(bc, reps))
+        a_cols.append(ac)
+        b_cols.append(bc)
+        b_rows.append(np.full(len(bc), r))
+    a_pos = np.concatenate([[0], np.cumsum([len(c) for c in a_cols])]).astype(np.int32)
+    a_crd = np.concatenate(a_cols).astype(np.int32)
+    b_cols = np.concatenate(b_cols).astype(np.int32)
+    b_rows = np.concatenate(b_rows).astype(np.int32)
+    a_vals = rng.uniform(-1, 1, len(a_crd))
+    b_vals = rng.uniform(-1, 1, len(b_cols))
+    rp, rc, rv = orc.add_csr(n, a_pos, a_crd, a_vals, b_cols, b_vals, b_rows=b_rows)
+    for two_pass in (False, True):
+        pos, crd, vals = K.add_csr(n, cuda(a_pos), cuda(a_crd), cuda(a_vals), cuda(b_cols),
+                                   cuda(b_vals), b_rows=cuda(b_rows), two_pass=two_pass)
+        assert np.array_equal(pos.cpu().numpy(), rp), two_pass
+        assert np.array_equal(crd.cpu().numpy(), rc), two_pass
+        assert np.array_equal(bits(vals), bits(rv)), two_pass
