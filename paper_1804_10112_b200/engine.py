@@ -105,6 +105,7 @@ class Plan:
     out_format: TensorFormat
     out_dims: Tuple[int, ...]
     fuse: bool = True            # the reference's fuse_branchless switch (engine.py:766-772)
+    out_class: str = ""          # format_class(out_format), fixed at planning
     ivars: Tuple[str, ...] = ()  # the loop variables, in schedule order (EvalStats keys)
     order: Tuple[str, ...] = ()  # tensor names in expression order (lattice-point labels)
 
@@ -123,6 +124,7 @@ def plan(checked: CheckedExpr, bindings, out_format: TensorFormat,
     (engine.py:200-209) — the B200 path then runs the exact-CSR copy."""
     p = _plan(checked, bindings, out_format, out_dims, fuse)
     p.fuse = fuse
+    p.out_class = format_class(out_format)
     p.order = tuple(dict.fromkeys(t.tensor for t in _accesses(checked.assignment.rhs)))
     return p
 
@@ -305,6 +307,19 @@ def _dia_host_offsets(st: TensorStorage):
         offs = st.levels[1].offset.cpu().numpy().astype(np.int32)
         st._host_offsets = offs
     return offs
+
+
+def _dense_level(spec, n: int) -> LevelStorage:
+    """A dense output level (no arrays): built without the array conversions
+    of LevelStorage.__init__ — the e2e step pays this per call."""
+    lv = LevelStorage.__new__(LevelStorage)
+    lv.spec, lv.n, lv.m, lv.w = spec, int(n), 0, 0
+    lv.pos = lv.crd = lv.offset = None
+    lv.crd_stride, lv.crd_base, lv.range_n = 1, 0, 0
+    lv._appended = lv._edges = None
+    lv._last_edge_parent = -1
+    lv._sl_max_row = None
+    return lv
 
 
 def _hashed_row_order(p: Plan, A: TensorStorage, nrows: int, dev):
@@ -583,7 +598,7 @@ def _run(p: Plan, inputs: Dict[str, TensorStorage], stats: Optional[EvalStats]):
             break
     if dev is None:
         dev = torch.device("cuda", torch.cuda.current_device())
-    if dev.index is not None and dev.index != torch.cuda.current_device():
+    if dev.index is not None and dev.index != torch._C._cuda_getDevice():
         # kernels launch on the current device's current stream: make it the
         # operands' device for the call (outputs are allocated there too)
         with torch.cuda.device(dev):
@@ -623,11 +638,11 @@ def _run_on(p: Plan, inputs: Dict[str, TensorStorage], stats: Optional[EvalStats
             # queries >= table slots: resolve each coordinate once (slot map)
             n_map = int(x.dims[0]) if nq >= hx.w else None
             y = K.spmv_csr_hashx(nrows, pos, crd, vals, hx.w, hx.crd, x.vals, n=n_map)
-        if format_class(p.out_format) == "hash1":
+        if p.out_class == "hash1":
             out = _hashed_spmv_output(p, A, y, nrows, dev)
         else:
-            out = TensorStorage(p.out_format, (nrows,),
-                                [LevelStorage(p.out_format.levels[0], n=nrows, device=dev)], y)
+            out = TensorStorage(p.out_format, (nrows,), [_dense_level(p.out_format.levels[0], nrows)],
+                                y)
     elif p.pattern == "add":
         A, B = ops["A"], ops["B"]
         nrows = A.dims[0]

@@ -70,12 +70,16 @@ def spmv_csr(nrows, ncols, pos, crd, vals, x, y=None, variant=0, ws=None):
     vals, x = _t(vals, F64, "vals"), _t(x, F64, "x")
     y = _out(y, nrows, F64, x, "y")
     nnz = crd.numel()
-    need = L().sl_spmv_csr_workspace_bytes(nrows, nnz, variant)
-    if ws is None or ws.numel() < need:
-        ws = _ws(need, x)
-    _lib.check(L().sl_spmv_csr_f64(nrows, ncols, nnz, P(pos), P(crd), P(vals), P(x), P(y),
-                                   variant, P(ws), 0 if ws is None else ws.numel(), S()),
-               "spmv_csr")
+    lib = L()
+    if variant == 2:                     # only the merge-path split uses a workspace
+        need = lib.sl_spmv_csr_workspace_bytes(nrows, nnz, variant)
+        if ws is None or ws.numel() < need:
+            ws = _ws(need, x)
+    st = lib.sl_spmv_csr_f64(nrows, ncols, nnz, pos.data_ptr(), crd.data_ptr(), vals.data_ptr(),
+                             x.data_ptr(), y.data_ptr(), variant, P(ws),
+                             0 if ws is None else ws.numel(), S())
+    if st:
+        _lib.check(st, "spmv_csr")
     return y
 
 
