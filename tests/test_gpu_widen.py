@@ -209,3 +209,32 @@ def test_tensor3_full_vs_oracle(orc):
                       tuple(cuda(z[k], np.int32 if k != "vals" else np.float64)
                             for k in ("i", "j", "k", "vals")))
     assert float(a2.cpu().numpy()[0]) == got          # deterministic
+
+
+@pytest.mark.slow
+def test_plus3_full_size_properties():
+    """3rd-order PLUS at D5 scale (40M nonzeros, power-law fibres), by
+    size-independent properties: X + X stores X's coordinates with 0 + (x + x)
+    = 2x exactly; X + (empty) is the identity copy 0 + x; X + Z with Z every
+    other nonzero of X gives X's structure with 0 + (x + z) on Z's entries."""
+    mt = wl.mttkrp()
+    I, J, Kd = mt["I"], mt["J"], mt["K"]
+    T = lambda a: torch.as_tensor(a, device="cuda")  # noqa: E731
+    ti, tj, tk, tv = T(mt["i"]), T(mt["j"]), T(mt["k"]), T(mt["vals"])
+    X = F.coo3_storage(ti, tj, tk, tv, (I, J, Kd))
+    expr = "A(i,j,k) = X(i,j,k) + Z(i,j,k)"
+    C = sl.evaluate(expr, {"X": X, "Z": X}, F.preset("coo-3"))
+    for lv, t in zip(C.levels, (ti, tj, tk)):
+        assert torch.equal(lv.crd, t)
+    assert torch.equal(C.vals, tv + tv)
+    e = torch.empty(0, dtype=torch.int32, device="cuda")
+    E0 = F.coo3_storage(e, e, e, torch.empty(0, dtype=torch.float64, device="cuda"), (I, J, Kd))
+    C = sl.evaluate(expr, {"X": X, "Z": E0}, F.preset("coo-3"))
+    assert torch.equal(C.levels[2].crd, tk) and torch.equal(C.vals, tv)
+    Z = F.coo3_storage(ti[::2].contiguous(), tj[::2].contiguous(), tk[::2].contiguous(),
+                       (tv[::2] * 0.5).contiguous(), (I, J, Kd))
+    C = sl.evaluate(expr, {"X": X, "Z": Z}, F.preset("coo-3"))
+    assert torch.equal(C.levels[0].crd, ti) and torch.equal(C.levels[2].crd, tk)
+    want = tv.clone()
+    want[::2] = tv[::2] + tv[::2] * 0.5
+    assert torch.equal(C.vals, want)
