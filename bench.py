@@ -537,16 +537,25 @@ def mttkrp_sharded(torch, dist, D, K, wl, dev, rank, world, timer, clk):
     e = [int(v) for v in sizes.tolist()]
     s0, s1 = int(slices[rank]), int(slices[rank + 1])
     n_loc = e[rank + 1] - e[rank]
+    # NCCL sends device buffers directly; gloo (the multi-rank smoke test on a
+    # 1-GPU box) only moves host tensors
+    via_host = dist.get_backend() != "nccl"
     if rank == 0:
         loc = [t[e[0]:e[1]] for t in full]
         for r in range(1, world):
             for t in full:
-                dist.send(t[e[r]:e[r + 1]].contiguous(), r)
+                part = t[e[r]:e[r + 1]].contiguous()
+                dist.send(part.cpu() if via_host else part, r)
     else:
         loc = [torch.empty(n_loc, dtype=torch.int32, device=dev) for _ in range(3)] + \
               [torch.empty(n_loc, dtype=torch.float64, device=dev)]
         for t in loc:
-            dist.recv(t, 0)
+            if via_host:
+                h = torch.empty(t.shape, dtype=t.dtype)
+                dist.recv(h, 0)
+                t.copy_(h)
+            else:
+                dist.recv(t, 0)
         Bt = torch.empty((J, R), dtype=torch.float64, device=dev)
         Ct = torch.empty((Kd, R), dtype=torch.float64, device=dev)
     D.replicate(Bt, src=0)

@@ -110,11 +110,20 @@ def gather_row_blocks(y_local, bounds: Sequence[int], group=None):
     world = dist.get_world_size(group)
     sizes = [int(bounds[p + 1] - bounds[p]) for p in range(world)]
     m = max(sizes)
+    if all(sz == m for sz in sizes) and y_local.is_contiguous():
+        # equal blocks (the weak-scaling slabs): one collective, no copies
+        full = torch.empty(m * world, dtype=y_local.dtype, device=y_local.device)
+        dist.all_gather_into_tensor(full, y_local, group=group)
+        return full
     pad = torch.zeros(m, dtype=y_local.dtype, device=y_local.device)
     pad[:y_local.numel()] = y_local
-    parts = [torch.empty_like(pad) for _ in range(world)]
-    dist.all_gather(parts, pad, group=group)
-    return torch.cat([parts[p][:sizes[p]] for p in range(world)])
+    flat = torch.empty(m * world, dtype=y_local.dtype, device=y_local.device)
+    dist.all_gather_into_tensor(flat, pad, group=group)
+    if not any(sz < m for sz in sizes):
+        return flat
+    keep = torch.cat([torch.arange(p * m, p * m + sizes[p], device=y_local.device)
+                      for p in range(world)])
+    return flat.index_select(0, keep)
 
 
 def shard_add(a_pos, a_crd, a_vals, b_rows, b_cols, b_vals, r0, r1):
