@@ -166,6 +166,19 @@ int sl_hashed_slot_map(int64_t n, int64_t w, const int32_t* crd, void* ws, size_
  * nonzeros are staged, products formed in parallel, and each row is summed in
  * storage order by the thread that owns the row's first nonzero.  Empty rows
  * are written as +0.0 in the same launch (no memset). */
+/* CSR SpMV of a row block with the all-gather of y fused into the epilogue
+ * (each GPU stores its rows straight into every peer's full-y
+ * buffer over NVLink instead of an NCCL all-gather after the kernel).
+ * y_peers: HOST array of npeers (1..8) device pointers — peer buffers mapped
+ * through CUDA IPC / symmetric memory, or local buffers — each already offset
+ * to this block's first global row.  The register hand-off kernel stores
+ * directly (rows averaging <= 28 nonzeros, 16-byte-aligned crd/vals); other
+ * matrices are computed into y_peers[0] and copied to the rest.  The caller
+ * synchronises the ranks (a barrier) before reading its full y. */
+int sl_spmv_csr_peers_f64(int64_t nrows, int64_t ncols, int64_t nnz, const int32_t* pos,
+                          const int32_t* crd, const double* vals, const double* x,
+                          const uint64_t* y_peers, int32_t npeers, void* stream);
+
 /* Optional kernels this build carries: bit 0 = the A/B alternatives (CSR
  * variants 1, 3, 4 and the persistent TMA pipelines of SL_SPMV_PATH=pipe),
  * compiled only with SL_BUILD_ALT=1; without them those variants return

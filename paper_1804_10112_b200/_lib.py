@@ -60,6 +60,7 @@ SIGNATURES = {
     "sl_spmv_coo_f64": ([_i64, _i64, _i64, _p, _p, _p, _p, _p, _p, _sz, _p], ctypes.c_int),
     "sl_spmv_coo_workspace_bytes": ([_i64], _sz),
     "sl_build_features": ([], ctypes.c_int),
+    "sl_spmv_csr_peers_f64": ([_i64, _i64, _i64, _p, _p, _p, _p, _p, _i32, _p], ctypes.c_int),
     "sl_spmv_csr_workspace_bytes": ([_i64, _i64, _i32], _sz),
     "sl_spmv_csr_f64": ([_i64, _i64, _i64, _p, _p, _p, _p, _p, _i32, _p, _sz, _p], ctypes.c_int),
     "sl_spmv_ell_f64": ([_i64, _i64, _i32, _p, _p, _p, _p, _p], ctypes.c_int),

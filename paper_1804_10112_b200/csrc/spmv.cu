@@ -578,11 +578,21 @@ SL_DEV void handoff_terms(const XOperand<kX>& xop, const int32_t* c, const doubl
   }
 }
 
-template <int kCap, int kMaxRow, int kBatch, int kMinBlocks, int kX>
+// Up to kMaxPeers output buffers the epilogue stores every row into: the
+// all-gather of y fused into the SpMV (each GPU writes its row block straight
+// into every peer's full-y buffer over NVLink — symmetric / IPC-mapped
+// pointers, already offset to this rank's first row).
+constexpr int kMaxPeers = 8;
+struct PeerOut {
+  double* p[kMaxPeers];
+  int n;
+};
+
+template <int kCap, int kMaxRow, int kBatch, int kMinBlocks, int kX, bool kPeers = false>
 __global__ void __launch_bounds__(32, kMinBlocks)
 spmv_csr_handoff_kernel(int64_t nrows, const int32_t* __restrict__ pos,
                         const int32_t* __restrict__ crd, const double* __restrict__ vals,
-                        XOperand<kX> xop, double* __restrict__ y) {
+                        XOperand<kX> xop, double* __restrict__ y, PeerOut peers) {
   static_assert(kCap % 4 == 0 && kMaxRow % kBatch == 0, "shapes");
   extern __shared__ __align__(16) unsigned char smem_raw[];
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw);
@@ -687,7 +697,14 @@ spmv_csr_handoff_kernel(int64_t nrows, const int32_t* __restrict__ pos,
       }
       next_staged = issue_next();
     }
-    if (lane < nr) y[r0 + lane] = acc;
+    if (lane < nr) {
+      if (kPeers) {
+#pragma unroll 1
+        for (int q = 0; q < peers.n; ++q) peers.p[q][r0 + lane] = acc;   // posted stores
+      } else {
+        y[r0 + lane] = acc;
+      }
+    }
     if (nnr == 0) break;
     tile = next;
     r0 = nr0;
@@ -703,17 +720,22 @@ spmv_csr_handoff_kernel(int64_t nrows, const int32_t* __restrict__ pos,
 template <int kCap, int kMaxRow, int kBatch, int kMinBlocks, int kX>
 static void launch_csr_handoff(int64_t nrows, const int32_t* pos, const int32_t* crd,
                                const double* vals, XOperand<kX> xop, double* y, int blocks_per_sm,
-                               cudaStream_t s, bool pdl = false) {
+                               cudaStream_t s, bool pdl = false, const PeerOut* peers = nullptr) {
   constexpr size_t smem = 16 + (size_t)kCap * 12;
   const int64_t ntiles = (nrows + 31) / 32;
   const int grid = (int)min64(ntiles, (int64_t)sl_host::sm_count() * blocks_per_sm);
+  if (peers) {
+    spmv_csr_handoff_kernel<kCap, kMaxRow, kBatch, kMinBlocks, kX, true><<<grid, 32, smem, s>>>(
+        nrows, pos, crd, vals, xop, y, *peers);
+    return;
+  }
   if (pdl) {
     sl_host::launch_pdl(spmv_csr_handoff_kernel<kCap, kMaxRow, kBatch, kMinBlocks, kX>, dim3(grid),
-                        dim3(32), s, smem, nrows, pos, crd, vals, xop, y);
+                        dim3(32), s, smem, nrows, pos, crd, vals, xop, y, PeerOut{});
     return;
   }
   spmv_csr_handoff_kernel<kCap, kMaxRow, kBatch, kMinBlocks, kX><<<grid, 32, smem, s>>>(
-      nrows, pos, crd, vals, xop, y);
+      nrows, pos, crd, vals, xop, y, PeerOut{});
 }
 
 // 896-element stage (28 per row), rows of up to 28 nonzeros in registers,
@@ -1257,4 +1279,38 @@ extern "C" int sl_build_features(void) {
 #else
   return 0;
 #endif
+}
+
+// CSR SpMV of a row block with the all-gather fused into the epilogue: rows
+// [0, nrows) of this block are stored into every buffer y_peers[q]
+// (q < npeers <= 8; host array of device pointers, each already offset to the
+// block's first global row — peer buffers mapped through CUDA IPC / symmetric
+// memory, or local buffers).  The register hand-off kernel (rows averaging
+// <= 28 nonzeros, 16-byte-aligned crd / vals) stores directly; any other
+// matrix is computed into y_peers[0] and copied to the other buffers.
+extern "C" int sl_spmv_csr_peers_f64(int64_t nrows, int64_t ncols, int64_t nnz,
+                                     const int32_t* pos, const int32_t* crd, const double* vals,
+                                     const double* x, const uint64_t* y_peers, int32_t npeers,
+                                     void* stream) {
+  if (nrows < 0 || ncols < 0 || nnz < 0 || npeers < 1 || npeers > kMaxPeers || !y_peers)
+    return SL_ERR_INVALID;
+  if (nrows > INT32_MAX || ncols > INT32_MAX || nnz > INT32_MAX) return SL_ERR_RANGE;
+  if (nrows == 0) return SL_OK;
+  cudaStream_t s = as_stream(stream);
+  PeerOut po{};
+  po.n = npeers;
+  for (int q = 0; q < npeers; ++q) po.p[q] = reinterpret_cast<double*>(y_peers[q]);
+  if (nnz > 0 && nnz <= (int64_t)kCsrHandoffMaxRow * nrows && aligned16(crd) && aligned16(vals)) {
+    launch_csr_handoff<kCsrHandoffCap, kCsrHandoffMaxRow, kCsrHandoffBatch, kCsrHandoffBlocks>(
+        nrows, pos, crd, vals, XOperand<0>{x}, po.p[0], kCsrHandoffBlocks, s, false, &po);
+    return sl_host::launch_status();
+  }
+  const int st = sl_spmv_csr_f64(nrows, ncols, nnz, pos, crd, vals, x, po.p[0], 0, nullptr, 0,
+                                 stream);
+  if (st != SL_OK) return st;
+  for (int q = 1; q < npeers; ++q)
+    if (cudaMemcpyAsync(po.p[q], po.p[0], (size_t)nrows * sizeof(double), cudaMemcpyDefault, s) !=
+        cudaSuccess)
+      return SL_ERR_CUDA;
+  return sl_host::launch_status();
 }

@@ -332,8 +332,36 @@ _SHARDED = {"spmv": ("A",), "spmm": ("A",), "add": ("A", "B"), "mttkrp": ("X",),
             "ttv": ("X",), "ttm": ("X",)}
 
 
+def _p2p_spmv_gather(A_loc, x, n, r0, r1, group):
+    """SpMV of this rank's CSR row block with the all-gather fused into the
+    kernel: the full y lives in symmetric memory (one buffer per rank, mapped
+    into every peer), the kernel stores each row into every rank's buffer
+    over NVLink (sl_spmv_csr_peers_f64), and a device-side barrier of the
+    symmetric-memory handle orders the stores before anyone reads y."""
+    import torch
+    import torch.distributed as dist
+
+    from . import kernels as K
+    from .errors import DeviceError
+
+    try:
+        import torch.distributed._symmetric_memory as symm
+    except Exception as e:                       # pragma: no cover - torch without it
+        raise DeviceError(f"symmetric memory unavailable: {e}")
+    dev = A_loc.vals.device
+    grp = group or dist.group.WORLD
+    full = symm.empty(n, dtype=torch.float64, device=dev)
+    handle = symm.rendezvous(full, grp)
+    world = dist.get_world_size(grp)
+    ptrs = [int(handle.buffer_ptrs[q]) + 8 * r0 for q in range(world)]
+    lv = A_loc.levels[1]
+    K.spmv_csr_peers(r1 - r0, A_loc.dims[1], lv.pos, lv.crd, A_loc.vals, x.vals, ptrs)
+    handle.barrier()
+    return full
+
+
 def evaluate_sharded(expr, inputs: Dict[str, "object"], out_format=None, *, group=None,
-                     gather: bool = True, local_eval: Optional[Callable] = None):
+                     gather="nccl", local_eval: Optional[Callable] = None):
     """Multi-GPU `evaluate`, one process per GPU.
 
     Every rank passes the same global operands, resident on its device.  The
@@ -342,11 +370,14 @@ def evaluate_sharded(expr, inputs: Dict[str, "object"], out_format=None, *, grou
     output's) is sliced on the device, the replicated ones (x, B, C, v, U —
     replicate them with `replicate` first if only one rank holds them) are
     used whole, and the rank evaluates its block with the single-GPU
-    `evaluate` (no exchange during compute).  With gather=True the blocks are
-    all-gathered (dense: padded row blocks; CSR / COO: nnz totals first, then
-    the arrays), so every rank returns the full result; with gather=False it
-    returns (local block, (r0, r1)).  `local_eval` replaces the per-rank
-    evaluation (tests inject the CPU oracle on gloo ranks)."""
+    `evaluate` (no exchange during compute).  gather="nccl" (or True) all-
+    gathers the blocks (dense: padded row blocks; CSR / COO: nnz totals first,
+    then the arrays), so every rank returns the full result; gather="p2p"
+    fuses the all-gather of a CSR SpMV's y into the kernel (each rank stores
+    its rows into every rank's symmetric-memory buffer; other patterns use
+    the NCCL gather); gather=False returns (local block, (r0, r1)).
+    `local_eval` replaces the per-rank evaluation (tests inject the CPU oracle
+    on gloo ranks)."""
     import torch
 
     from . import engine as E
@@ -368,6 +399,12 @@ def evaluate_sharded(expr, inputs: Dict[str, "object"], out_format=None, *, grou
     for role in roles:
         name = p.operands[role]
         local[name] = shard_storage(inputs[name], E.format_class(inputs[name].format), r0, r1)
+    if gather == "p2p" and p.kernel == "spmv_csr" and local_eval is None and \
+            inputs[p.operands["A"]].format.levels[1].props.unique and \
+            E.format_class(p.out_format) == "dense1":
+        full = _p2p_spmv_gather(local[p.operands["A"]], inputs[p.operands["x"]], n, r0, r1, group)
+        f = p.out_format
+        return TensorStorage(f, (n,), [LevelStorage(f.levels[0], n=n, device=full.device)], full)
     res = ev(expr, local, out_format)
     if not gather:
         return res, (r0, r1)

@@ -83,6 +83,20 @@ def spmv_csr(nrows, ncols, pos, crd, vals, x, y=None, variant=0, ws=None):
     return y
 
 
+def spmv_csr_peers(nrows, ncols, pos, crd, vals, x, peer_ptrs):
+    """CSR SpMV of a row block storing every row into each buffer of
+    `peer_ptrs` (device pointers, already offset to the block's first row):
+    the all-gather of y fused into the kernel's epilogue (sl_spmv_csr_peers_f64)."""
+    import ctypes
+
+    pos, crd = _t(pos, I32, "pos"), _t(crd, I32, "crd")
+    vals, x = _t(vals, F64, "vals"), _t(x, F64, "x")
+    arr = (ctypes.c_uint64 * len(peer_ptrs))(*[int(p) for p in peer_ptrs])
+    _lib.check(L().sl_spmv_csr_peers_f64(nrows, ncols, crd.numel(), P(pos), P(crd), P(vals), P(x),
+                                         ctypes.cast(arr, ctypes.c_void_p), len(peer_ptrs), S()),
+               "spmv_csr_peers")
+
+
 def spmv_ell(nrows, ncols, nslots, crd, vals, x, y=None):
     crd, vals, x = _t(crd, I32, "crd"), _t(vals, F64, "vals"), _t(x, F64, "x")
     y = _out(y, nrows, F64, x, "y")

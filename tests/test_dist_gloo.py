@@ -201,6 +201,11 @@ def _sharded_worker(rank, world, port, out_dir):
             y = D.evaluate_sharded("y(i) = A(i,j) * x(j)", {"A": A, "x": x},
                                    local_eval=_oracle_eval)
             out[f"y_{name}"] = y.vals.numpy()
+        # gather="p2p" needs the CUDA kernel's peer epilogue; with an injected
+        # local evaluation it takes the collective gather, same result
+        y = D.evaluate_sharded("y(i) = A(i,j) * x(j)", {"A": mats["csr"], "x": x},
+                               gather="p2p", local_eval=_oracle_eval)
+        out["y_p2p"] = y.vals.numpy()
         ab = wl.add_ab(n=4000, nnz_a=16000, nnz_b=16000, seed=8)
         A = F.csr_storage(ab["a_pos"], ab["a_crd"], ab["a_vals"], (4000, 4000), device="cpu")
         B = F.coo_storage(ab["b_rows"], ab["b_cols"], ab["b_vals"], (4000, 4000), device="cpu")
@@ -240,7 +245,7 @@ def test_two_rank_gloo_evaluate_sharded(tmp_path, orc):
     d = wl.coo_spmv(n=3000, nnz=40000, seed=5)
     n, m = d["nrows"], d["ncols"]
     ref, _ = orc.spmv_coo(n, d["rows"], d["cols"], d["vals"], d["x"])
-    for name in ("csr", "coo", "ell"):
+    for name in ("csr", "coo", "ell", "p2p"):
         assert np.array_equal(r[f"y_{name}"].view(np.int64), ref.view(np.int64)), name
     band = np.abs(d["cols"].astype(np.int64) - d["rows"]) <= 300
     dd = wl.dia_from_coo(d["rows"][band], d["cols"][band], d["vals"][band], n, m)

@@ -292,3 +292,33 @@ def test_device_row_shards_reassemble(parts):
     y1 = D.evaluate_sharded("y(i) = A(i,j) * x(j)", {"A": mats["csr"], "x": x}).vals
     assert np.array_equal(bits(y1), bits(slb.evaluate("y(i) = A(i,j) * x(j)",
                                                       {"A": mats["csr"], "x": x}).vals))
+
+
+def test_spmv_peers_epilogue_gathers_row_blocks():
+    """sl_spmv_csr_peers_f64 (the all-gather fused into the SpMV epilogue),
+    with local buffers standing in for the ranks' symmetric-memory buffers:
+    every block's rows land in every buffer, bit-equal to the whole SpMV —
+    through the register hand-off kernel (short rows) and the fallback
+    (rows above its limit: computed into the first buffer, copied)."""
+    from paper_1804_10112_b200 import dist as D
+    from paper_1804_10112_b200 import kernels as K
+    from paper_1804_10112_b200 import workloads as wl
+
+    for lam in (10.0, 60.0):
+        d = wl.coo_spmv(n=5000, ncols=6000, nnz=int(5000 * lam), lam=lam, seed=11)
+        n, m = d["nrows"], d["ncols"]
+        pos = wl.coo_to_csr_pos(d["rows"], n)
+        A = F.csr_storage(pos, d["cols"], d["vals"], (n, m))
+        x = F.dense_storage(d["x"])
+        full = slb.evaluate("y(i) = A(i,j) * x(j)", {"A": A, "x": x}).vals
+        world = 3
+        bufs = [torch.full((n,), float("nan"), dtype=torch.float64, device="cuda")
+                for _ in range(world)]
+        b = D.row_blocks(A, "csr", world, n)
+        for q in range(world):
+            r0, r1 = b[q], b[q + 1]
+            Aq = D.shard_storage(A, "csr", r0, r1)
+            K.spmv_csr_peers(r1 - r0, m, Aq.levels[1].pos, Aq.levels[1].crd, Aq.vals, x.vals,
+                             [t.data_ptr() + 8 * r0 for t in bufs])
+        for t in bufs:
+            assert np.array_equal(bits(t), bits(full)), lam
