@@ -11,6 +11,7 @@
 // the kernels are HBM-bound on the streamed index/value arrays.
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdio.h>
 #include <stdlib.h>
 
 #include "common.cuh"
@@ -738,6 +739,188 @@ static void launch_csr_handoff(int64_t nrows, const int32_t* pos, const int32_t*
       nrows, pos, crd, vals, xop, y, PeerOut{});
 }
 
+#ifdef SL_WITH_ALT
+// K2q: the register hand-off with a ring of two stages per warp.  K2r keeps
+// one tile's bulk copy in flight per warp (12 x 10.5 KB per SM), and a warp
+// then waits out the copy latency once per tile.  Here tiles t+1 and t+2 are
+// in flight while tile t's gathers and adds run (10 warps x 2 x 10.5 KB per
+// SM), and the row pointer of a tile is read two iterations before its copy
+// is issued, so neither latency sits on a warp's path.  Arithmetic per row is
+// K2r's (same terms, same ordered add chain), so the results are bit-equal.
+struct TileRows {
+  int32_t pb, pe;   // this lane's row [pb, pe) (0, 0 past the tile's last row)
+  int nr;           // rows in the tile (0: no such tile)
+};
+
+SL_DEV TileRows load_tile_rows(const int32_t* __restrict__ pos, int64_t nrows, int64_t tile,
+                               int64_t ntiles, int lane) {
+  TileRows t;
+  t.nr = tile < ntiles ? (int)min64(32, nrows - tile * 32) : 0;
+  t.pb = lane < t.nr ? ldg(pos + tile * 32 + lane) : 0;
+  t.pe = lane < t.nr ? ldg(pos + tile * 32 + lane + 1) : 0;
+  return t;
+}
+
+template <int kCap, int kMaxRow, int kBatch, int kMinBlocks, int kX>
+__global__ void __launch_bounds__(32, kMinBlocks)
+spmv_csr_ring_kernel(int64_t nrows, const int32_t* __restrict__ pos,
+                     const int32_t* __restrict__ crd, const double* __restrict__ vals,
+                     XOperand<kX> xop, double* __restrict__ y) {
+  static_assert(kCap % 4 == 0 && kMaxRow % kBatch == 0, "shapes");
+  constexpr uint32_t kStage = (uint32_t)kCap * 12;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw);   // [2]
+  unsigned char* sbase = smem_raw + 16;
+  const int lane = threadIdx.x;
+  const int64_t ntiles = (nrows + 31) / 32, G = gridDim.x;
+  int64_t tile = blockIdx.x;
+  if (tile >= ntiles) return;
+  pdl_wait();            // COO path: launched with PDL behind the row-pointer pass
+  if (lane == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    fence_mbar_init();
+  }
+  __syncwarp();
+  auto s_crd = [&](int s) { return reinterpret_cast<int32_t*>(sbase + s * kStage); };
+  auto s_val = [&](int s) { return reinterpret_cast<double*>(sbase + s * kStage + kCap * 4); };
+  auto issue = [&](int s, int32_t a0, int32_t ee) {   // lane 0: stage [a0, ee) into slot s
+    const uint32_t bc = (uint32_t)(((ee - a0 + 3) & ~3) * 4);
+    const uint32_t bv = (uint32_t)(((ee - a0 + 1) & ~1) * 8);
+    fence_proxy_async_smem();
+    mbar_arrive_expect_tx(&bars[s], bc + bv);
+    bulk_g2s(s_crd(s), crd + a0, bc, &bars[s]);
+    bulk_g2s(s_val(s), vals + a0, bv, &bars[s]);
+  };
+  auto try_issue = [&](const TileRows& t, int s) -> bool {   // stage tile t if it fits
+    if (t.nr == 0) return false;
+    const int32_t eb = __shfl_sync(0xffffffffu, t.pb, 0);
+    const int32_t ee = __shfl_sync(0xffffffffu, t.pe, t.nr - 1);
+    const bool ok = ee > eb && ee - (eb & ~3) <= kCap;
+    if (ok && lane == 0) issue(s, eb & ~3, ee);
+    return ok;
+  };
+  TileRows t0 = load_tile_rows(pos, nrows, tile, ntiles, lane);
+  TileRows t1 = load_tile_rows(pos, nrows, tile + G, ntiles, lane);
+  TileRows t2 = load_tile_rows(pos, nrows, tile + 2 * G, ntiles, lane);
+  bool st0 = try_issue(t0, 0), st1 = try_issue(t1, 1);
+  uint32_t ph = 0;       // bit s: the parity stage s's next wait expects
+  int s = 0;
+  for (;;) {
+    const TileRows t3 = load_tile_rows(pos, nrows, tile + 3 * G, ntiles, lane);
+    const int32_t eb = __shfl_sync(0xffffffffu, t0.pb, 0);
+    const int32_t ee = __shfl_sync(0xffffffffu, t0.pe, t0.nr - 1);
+    const int32_t a0 = eb & ~3;
+    const int len = t0.pe - t0.pb;
+    double acc = 0.0;
+    bool st2 = false, reg = false;
+    if (st0) {
+      mbar_wait(&bars[s], (ph >> s) & 1u);
+      ph ^= 1u << s;
+      reg = __all_sync(0xffffffffu, len <= kMaxRow);
+    }
+    if (reg) {
+      const int off = t0.pb - a0;
+      const int32_t* sc = s_crd(s);
+      const double* sv = s_val(s);
+      int32_t c[kMaxRow];
+      double v[kMaxRow];
+#pragma unroll
+      for (int u = 0; u < kMaxRow; ++u) {
+        c[u] = u < len ? sc[off + u] : 0;
+        v[u] = u < len ? sv[off + u] : 0.0;
+      }
+      __syncwarp();                     // every lane's row is in registers
+      st2 = try_issue(t2, s);
+#pragma unroll
+      for (int u0 = 0; u0 < kMaxRow; u0 += kBatch) {
+        double t[kBatch];
+        handoff_terms<kX, kBatch>(xop, c + u0, v + u0, u0, len, t);
+#pragma unroll
+        for (int b = 0; b < kBatch; ++b)
+          if (u0 + b < len) acc = dadd(acc, t[b]);
+      }
+    } else {
+      // K2r's rounds through this tile's slot (round 0 already there if the
+      // tile was staged); the other slot's copy stays in flight
+      int32_t* sc = s_crd(s);
+      double* sv = s_val(s);
+      const int nch = ee > eb ? (ee - a0 + kCap - 1) / kCap : 0;
+      for (int k = 0; k < nch; ++k) {
+        const int32_t c0 = a0 + k * kCap, c1 = min(c0 + kCap, ee);
+        if (k > 0 || !st0) {
+          if (lane == 0) issue(s, c0, c1);
+          mbar_wait(&bars[s], (ph >> s) & 1u);
+          ph ^= 1u << s;
+        }
+        for (int q = max(eb, c0) - c0 + lane; q < c1 - c0; q += 32) sv[q] = xop.term(sv[q], sc[q]);
+        __syncwarp();
+        const int lo = max(t0.pb, c0) - c0, hi = min(t0.pe, c1) - c0;
+        for (int u = lo; u < hi; ++u) acc = dadd(acc, sv[u]);
+        __syncwarp();
+      }
+      st2 = try_issue(t2, s);
+    }
+    if (lane < t0.nr) y[tile * 32 + lane] = acc;
+    if (t1.nr == 0) break;
+    tile += G;
+    t0 = t1;
+    t1 = t2;
+    t2 = t3;
+    st0 = st1;
+    st1 = st2;
+    s ^= 1;
+  }
+}
+
+// A/B knob: SL_CARVEOUT=1 asks for the maximum shared-memory carveout before
+// the hand-off / ring launches; SL_DEBUG_OCC=1 prints their resident blocks/SM
+template <typename Kern>
+static void occupancy_setup(Kern kern, size_t smem, const char* name) {
+  static int done[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (done[dev & 63]) return;
+  done[dev & 63] = 1;
+  const char* c = getenv("SL_CARVEOUT");
+  if (c && c[0] == '1')
+    cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  const char* d = getenv("SL_DEBUG_OCC");
+  if (d && d[0] == '1') {
+    int nb = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, 32, smem);
+    fprintf(stderr, "[occ] %s smem %zu blocks/SM %d\n", name, smem, nb);
+  }
+}
+
+template <int kCap, int kMaxRow, int kBatch, int kMinBlocks, int kX>
+static void launch_csr_ring(int64_t nrows, const int32_t* pos, const int32_t* crd,
+                            const double* vals, XOperand<kX> xop, double* y, int blocks_per_sm,
+                            cudaStream_t s, bool pdl = false) {
+  constexpr size_t smem = 16 + (size_t)kCap * 24;
+  occupancy_setup(spmv_csr_ring_kernel<kCap, kMaxRow, kBatch, kMinBlocks, kX>, smem, "ring");
+  const int64_t ntiles = (nrows + 31) / 32;
+  const int grid = (int)min64(ntiles, (int64_t)sl_host::sm_count() * blocks_per_sm);
+  if (pdl) {
+    sl_host::launch_pdl(spmv_csr_ring_kernel<kCap, kMaxRow, kBatch, kMinBlocks, kX>, dim3(grid),
+                        dim3(32), s, smem, nrows, pos, crd, vals, xop, y);
+    return;
+  }
+  spmv_csr_ring_kernel<kCap, kMaxRow, kBatch, kMinBlocks, kX><<<grid, 32, smem, s>>>(
+      nrows, pos, crd, vals, xop, y);
+}
+
+// A/B knob while the ring variant is measured: SL_CSR_RING=1 selects K2q
+// wherever K2r would run (blocks per SM from SL_CSR_RING_BLOCKS, default 10)
+static int csr_ring_blocks() {
+  const char* e = getenv("SL_CSR_RING");
+  if (!e || e[0] != '1') return 0;
+  const char* b = getenv("SL_CSR_RING_BLOCKS");
+  return b ? atoi(b) : 10;
+}
+
+#endif  // SL_WITH_ALT
+
 // 896-element stage (28 per row), rows of up to 28 nonzeros in registers,
 // gathers in two batches of 14, 12 one-warp blocks per SM (146 registers):
 // 64^3 stencil 22.4 us, D1 19.3 us, against K2f 23.8 / K2a 20.5 us; 14-27
@@ -1029,6 +1212,13 @@ extern "C" int sl_spmv_coo_f64(int64_t nrows, int64_t ncols, int64_t nnz, const 
       nnz <= (int64_t)kCsrHandoffMaxRow * nrows && !(ck && ck[0] == 't')) {
     int32_t* rowptr = static_cast<int32_t*>(ws);
     sl_host::launch_coo_rowptr(nrows, nnz, rows, rowptr, s);
+#ifdef SL_WITH_ALT
+    if (const int rb = csr_ring_blocks()) {
+      launch_csr_ring<kCsrHandoffCap, kCsrHandoffMaxRow, kCsrHandoffBatch, 10>(
+          nrows, rowptr, cols, vals, XOperand<0>{x}, y, rb, s, true);
+      return sl_host::launch_status();
+    }
+#endif
     launch_csr_handoff<kCsrHandoffCap, kCsrHandoffMaxRow, kCsrHandoffBatch, kCsrHandoffBlocks>(
         nrows, rowptr, cols, vals, XOperand<0>{x}, y, kCsrHandoffBlocks, s, true);
     return sl_host::launch_status();
@@ -1079,6 +1269,13 @@ static int launch_csr(int64_t nrows, int64_t nnz, const int32_t* pos, const int3
     if constexpr (kHashX == 0 || kHashX == 3) {
       if (variant == 0 && nnz >= 0 && nnz <= (int64_t)kCsrHandoffMaxRow * nrows &&
           aligned16(crd) && aligned16(vals)) {
+#ifdef SL_WITH_ALT
+        if (const int rb = csr_ring_blocks()) {
+          launch_csr_ring<kCsrHandoffCap, kCsrHandoffMaxRow, kCsrHandoffBatch, 10>(
+              nrows, pos, crd, vals, xop, y, rb, s);
+          return sl_host::launch_status();
+        }
+#endif
         launch_csr_handoff<kCsrHandoffCap, kCsrHandoffMaxRow, kCsrHandoffBatch, kCsrHandoffBlocks>(
             nrows, pos, crd, vals, xop, y, kCsrHandoffBlocks, s);
         return sl_host::launch_status();
