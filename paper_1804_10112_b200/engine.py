@@ -626,6 +626,8 @@ def _run_on(p: Plan, inputs: Dict[str, TensorStorage], stats: Optional[EvalStats
             y = K.spmv_ell(nrows, ncols, S, A.levels[2].crd, A.vals, x.vals)
         elif p.kernel == "spmv_dia":
             offs = _dia_host_offsets(inputs[p.operands["A"]])
+            if len(offs) > 32:   # beyond the kernel-parameter window: the level's device array
+                offs = A.levels[1].offset
             y = K.spmv_dia(nrows, ncols, offs, A.vals, x.vals)
         elif p.kernel == "spmv_csr_spx":
             sx = x.levels[0]
