@@ -746,9 +746,11 @@ def run_formats(torch, K, F, wl, evaluate, compile_, dev, timer, peak, l2, clk, 
                                 for o in csr_ops]}, steps, 3)
     bh = 4 * (n + 1) + 12 * nnz + 8 * n + 12 * h["width"]
     res["csr_hashx_H1"] = {"ms": round(tt["probe"], 5), "GB/s": round(bh / tt["probe"] / 1e6, 1),
+                           "frac": round(bh / tt["probe"] / 1e6 / peak, 4),
                            "locates/s": round(nnz / tt["probe"] * 1e3, 1), "bytes": bh,
                            "path": "per-nonzero warp-cooperative probing"}
     res["csr_hashx_map_H1"] = {"ms": round(tt["map"], 5), "GB/s": round(bh / tt["map"] / 1e6, 1),
+                               "frac": round(bh / tt["map"] / 1e6 / peak, 4),
                                "locates/s": round(nnz / tt["map"] * 1e3, 1), "bytes": bh,
                                "path": "slot map (one locate per coordinate) + CSR SpMV",
                                "cpu_baseline": cpu_leg("CSR x hash-x H1", lambda: oracle.spmv_csr_hashx(
@@ -1005,8 +1007,9 @@ def run_formats(torch, K, F, wl, evaluate, compile_, dev, timer, peak, l2, clk, 
     res["plus3_coo3_D5"] = {"ms": round(tt["plus3"], 4), "GB/s": round(b_p / tt["plus3"] / 1e6, 1),
                             "frac": round(b_p / tt["plus3"] / 1e6 / peak, 4), "bytes": b_p,
                             "nnz_c": nz_c, "launch": timer.method.get("plus3"),
-                            "path": "evaluate(): union of the operands' fibres, the A + B kernels "
-                                    "over (fibre x k); host syncs for the output sizes"}
+                            "path": "evaluate(): union of the operands' fibres, long fibres cut into "
+                                    "k-blocks, the A + B kernels over (fibre block x k); torch "
+                                    "glue for the keys, host syncs for the output sizes"}
     del X_st, Z_st, out
     return res
 

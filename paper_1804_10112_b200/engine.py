@@ -500,52 +500,84 @@ def _fibre_coo(X: TensorStorage):
     return fkey[leaf_f], L[2].crd, X.vals[:nnz]
 
 
+_PLUS3_ROW = 16    # target entries per row of the 2-D union (a dense fibre is cut into k-blocks)
+
+
 def _plus3(p: Plan, X: TensorStorage, Z: TensorStorage, dev) -> TensorStorage:
-    """A(i,j,k) = X(i,j,k) + Z(i,j,k): the rows of the 2-D union are the
-    union of the operands' (i, j) fibres (sorted keys i*J + j; each nonzero's
-    row located by searchsorted), its columns k — the same gather-append
-    union and duplicate grouping as A + B (X's exact grouped copy, Z's
-    repeats grouped by the kernels; engine.py:107-149, 330-434)."""
+    """A(i,j,k) = X(i,j,k) + Z(i,j,k) as a 2-D union: the same gather-append
+    and duplicate grouping as A + B (X's exact grouped copy, Z's repeats
+    grouped by the kernels; engine.py:107-149, 330-434) with columns k and
+    rows the union of the operands' (i, j) fibres (sorted keys i*J + j, each
+    nonzero's fibre located by searchsorted) — a fibre holding many entries
+    cut into power-of-two k-blocks of ~_PLUS3_ROW entries, each block its own
+    row.  The union over (fibre, k-block, k) is the union over (i, j, k); what
+    changes is the kernels' load balance: D5's power-law fibres (up to K
+    entries each) as single rows serialised the long-row path (22.8 ms of
+    A + B; k-blocked: see DESIGN.md)."""
     I, J, Kd = X.dims
     xk, xc, xv = _fibre_coo(X)
     zk, zc, zv = _fibre_coo(Z)
     uq = lambda t: torch.unique_consecutive(t) if t.numel() else t  # noqa: E731
     U = torch.unique(torch.cat([uq(xk), uq(zk)]))                   # sorted fibre keys
     nU = int(U.numel())
-    xr = torch.searchsorted(U, xk).to(torch.int32)
-    zr = torch.searchsorted(U, zk).to(torch.int32)
-    a_pos, a_crd, a_vals = K.coo_to_csr(nU, xr, xc, xv)
-    c_pos, c_crd, c_vals = K.add_csr(nU, a_pos, a_crd, a_vals, zc, zv, b_rows=zr)
+    xf = torch.searchsorted(U, xk)
+    zf = torch.searchsorted(U, zk)
+    if nU:
+        # entries per union fibre: the keys are sorted, so two boundary searches
+        # (a bincount's atomics pile up on the long fibres: 4 ms at D5)
+        ub = torch.cat([U, U[-1:] + 1])
+        ln = torch.diff(torch.searchsorted(xk, ub)) + torch.diff(torch.searchsorted(zk, ub))
+        kbits = max(int(Kd) - 1, 1).bit_length()
+        want = torch.ceil(torch.log2((ln.double() / _PLUS3_ROW).clamp_(min=1.0))).to(torch.int64)
+        sh = (kbits - want).clamp_(min=0)                # k >> sh: the k-block of a coordinate
+        nblk = ((Kd - 1) >> sh) + 1                      # rows of each fibre
+        rowend = torch.cumsum(nblk, 0)
+        rowbase = rowend - nblk
+        nR = int(rowend[-1].item())
+    else:
+        sh = rowbase = nblk = torch.zeros(0, dtype=torch.int64, device=dev)
+        nR = 0
+    if nR > 2 ** 31 - 1:
+        raise UnsupportedMergeError("3rd-order PLUS: the union's row space exceeds int32")
+    xr = (rowbase[xf] + (xc.to(torch.int64) >> sh[xf])).to(torch.int32)
+    zr = (rowbase[zf] + (zc.to(torch.int64) >> sh[zf])).to(torch.int32)
+    a_pos, a_crd, a_vals = K.coo_to_csr(nR, xr, xc, xv)
+    c_pos, c_crd, c_vals = K.add_csr(nR, a_pos, a_crd, a_vals, zc, zv, b_rows=zr)
     f = p.out_format
     ocls = format_class(f)
     nnz = int(c_crd.numel())
     fi, fj = (U // J).to(torch.int32), (U % J).to(torch.int32)
+
+    def out_fibres():       # union fibre of every output entry
+        rowfib = torch.repeat_interleave(torch.arange(nU, device=dev), nblk)
+        return rowfib[K.csr_rows(nR, c_pos, nnz).to(torch.int64)]
+
     if ocls == "dense3":
         out = torch.zeros(I * J * Kd, dtype=torch.float64, device=dev)
         if nnz:
-            rows = K.csr_rows(nU, c_pos, nnz).to(torch.int64)
-            out[U[rows] * Kd + c_crd.to(torch.int64)] = c_vals
+            out[U[out_fibres()] * Kd + c_crd.to(torch.int64)] = c_vals
         return TensorStorage(f, (I, J, Kd), [LevelStorage(s_, n=d, device=dev)
                                              for s_, d in zip(f.levels, (I, J, Kd))], out)
     if ocls == "coo3":
-        rows = K.csr_rows(nU, c_pos, nnz).to(torch.int64) if nnz else \
-            torch.empty(0, dtype=torch.int64, device=dev)
-        return TensorStorage(f, (I, J, Kd), [LevelStorage(f.levels[0], pos=[0, nnz], crd=fi[rows],
+        fib = out_fibres() if nnz else torch.empty(0, dtype=torch.int64, device=dev)
+        return TensorStorage(f, (I, J, Kd), [LevelStorage(f.levels[0], pos=[0, nnz], crd=fi[fib],
                                                           device=dev),
-                                             LevelStorage(f.levels[1], crd=fj[rows], device=dev),
+                                             LevelStorage(f.levels[1], crd=fj[fib], device=dev),
                                              LevelStorage(f.levels[2], crd=c_crd, device=dev)],
                              c_vals)
-    # CSF: every union fibre holds an entry; slices are the runs of equal i
+    # CSF: every union fibre holds an entry; slices are the runs of equal i;
+    # a fibre's leaves are its k-blocks' rows, consecutive in C
     sst = torch.ones(nU, dtype=torch.bool, device=dev)
     if nU:
         sst[1:] = fi[1:] != fi[:-1]
     spos = torch.nonzero(sst).squeeze(1)
     end = lambda t, v: torch.cat([t.to(torch.int64), torch.tensor([v], device=dev)]).to(  # noqa: E731
         torch.int32)
+    leaf_pos = c_pos[end(rowbase, nR).to(torch.int64)] if nU else c_pos
     return TensorStorage(f, (I, J, Kd), [
         LevelStorage(f.levels[0], pos=[0, int(spos.numel())], crd=fi[spos], device=dev),
         LevelStorage(f.levels[1], pos=end(spos, nU), crd=fj, device=dev),
-        LevelStorage(f.levels[2], pos=c_pos, crd=c_crd, device=dev)], c_vals)
+        LevelStorage(f.levels[2], pos=leaf_pos, crd=c_crd, device=dev)], c_vals)
 
 
 _SKEW_TILE = 4 * 896   # 32-row tiles heavier than four hand-off stages: merge-path

@@ -238,3 +238,58 @@ def test_plus3_full_size_properties():
     want = tv.clone()
     want[::2] = tv[::2] + tv[::2] * 0.5
     assert torch.equal(C.vals, want)
+
+
+@pytest.mark.parametrize("seed", [0, 1])
+def test_plus3_long_fibres_all_outputs(seed):
+    """3rd-order PLUS with fibres far longer than one k-block (the union's
+    rows are (fibre, k-block) pairs, engine._plus3) and short ones beside them,
+    into COO-3, CSF and dense-3, against a numpy union of unique coordinates:
+    0 + (x + z) where both hold the coordinate, 0 + x / 0 + z otherwise."""
+    rng = np.random.default_rng(seed)
+    I, J, Kd = 5, 7, 700
+
+    def draw(p_long):
+        keys = []
+        for f in range(I * J):
+            n = rng.integers(300, 600) if rng.random() < p_long else rng.integers(0, 6)
+            keys.append(f * Kd + np.sort(rng.choice(Kd, size=int(n), replace=False)))
+        k = np.concatenate(keys).astype(np.int64)
+        return k, rng.uniform(-1, 1, len(k))
+
+    xk, xv = draw(0.4)
+    zk, zv = draw(0.4)
+    uk = np.union1d(xk, zk)
+    vx = np.zeros(len(uk))
+    vz = np.zeros(len(uk))
+    inx, inz = np.isin(uk, xk), np.isin(uk, zk)
+    vx[inx], vz[inz] = xv, zv
+    want = 0.0 + np.where(inx & inz, vx + vz, np.where(inx, vx, vz))
+    ui, uj, ukk = uk // (J * Kd), (uk // Kd) % J, uk % Kd
+
+    def st(keys, vals):
+        return F.coo3_storage((keys // (J * Kd)).astype(np.int32), ((keys // Kd) % J).astype(np.int32),
+                              (keys % Kd).astype(np.int32), vals, (I, J, Kd))
+
+    X, Z = st(xk, xv), st(zk, zv)
+    expr = "A(i,j,k) = X(i,j,k) + Z(i,j,k)"
+    C = sl.evaluate(expr, {"X": X, "Z": Z}, F.preset("coo-3"))
+    for lv, t in zip(C.levels, (ui, uj, ukk)):
+        assert np.array_equal(lv.crd.cpu().numpy(), t)
+    assert np.array_equal(bits(C.vals), bits(want))
+    csf = wl.coo3_to_csf(ui, uj, ukk, None)
+    C = sl.evaluate(expr, {"X": X, "Z": Z}, F.preset("csf"))
+    assert np.array_equal(C.levels[0].crd.cpu().numpy(), csf["crd0"])
+    assert np.array_equal(C.levels[1].pos.cpu().numpy(), csf["pos1"])
+    assert np.array_equal(C.levels[1].crd.cpu().numpy(), csf["crd1"])
+    assert np.array_equal(C.levels[2].pos.cpu().numpy(), csf["pos2"])
+    assert np.array_equal(C.levels[2].crd.cpu().numpy(), csf["crd2"])
+    assert np.array_equal(bits(C.vals), bits(want))
+    # CSF operands take the same route (fibre keys from the level arrays)
+    xc = wl.coo3_to_csf(xk // (J * Kd), (xk // Kd) % J, xk % Kd, None)
+    Xc = F.csf_storage(xc["pos0"], xc["crd0"], xc["pos1"], xc["crd1"], xc["pos2"], xc["crd2"],
+                       xv, (I, J, Kd))
+    D = sl.evaluate(expr, {"X": Xc, "Z": Z}, F.preset("dense", order=3))
+    dense = np.zeros(I * J * Kd)
+    dense[uk] = want
+    assert np.array_equal(bits(D.vals), bits(dense))

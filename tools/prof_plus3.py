@@ -29,30 +29,40 @@ def mark(name):
     marks.append((name, e))
 
 
-for rep in range(2):
-    marks.clear()
-    mark("start")
-    xk, xc, xv = E._fibre_coo(X)
-    zk, zc, zv = E._fibre_coo(Z)
-    mark("fibre keys")
-    uq = lambda t: torch.unique_consecutive(t)  # noqa: E731
-    ux, uz = uq(xk), uq(zk)
-    mark("unique_consecutive")
-    U = torch.unique(torch.cat([ux, uz]))
-    mark("union unique")
-    xr = torch.searchsorted(U, xk).to(torch.int32)
-    zr = torch.searchsorted(U, zk).to(torch.int32)
-    mark("searchsorted")
-    nU = int(U.numel())
-    a = K.coo_to_csr(nU, xr, xc, xv)
-    mark("coo_to_csr")
-    c = K.add_csr(nU, *a, zc, zv, b_rows=zr)
-    mark("add_csr")
-    rows = K.csr_rows(nU, c[0], int(c[1].numel())).to(torch.int64)
-    fi, fj = (U // J).to(torch.int32)[rows], (U % J).to(torch.int32)[rows]
-    mark("output coords")
+# the whole evaluate, and the kernel wrappers inside it (events around each)
+timed = {}
+
+
+def wrap(name):
+    fn = getattr(K, name)
+
+    def w(*a, **k):
+        e0, e1 = ev(), ev()
+        e0.record()
+        r = fn(*a, **k)
+        e1.record()
+        timed.setdefault(name, []).append((e0, e1))
+        return r
+    setattr(K, name, w)
+
+
+for name in ("coo_to_csr", "add_csr", "csr_rows"):
+    wrap(name)
+for rep in range(3):
+    timed.clear()
+    e0, e1 = ev(), ev()
+    e0.record()
+    C = E.evaluate("A(i,j,k) = X(i,j,k) + Z(i,j,k)", {"X": X, "Z": Z}, F.preset("coo-3"))
+    e1.record()
     torch.cuda.synchronize()
     if rep:
-        for (n0, e0), (n1, e1) in zip(marks, marks[1:]):
-            print(f"{n1:20s} {e0.elapsed_time(e1):8.3f} ms")
-        print("nU", nU)
+        print(f"evaluate total       {e0.elapsed_time(e1):8.3f} ms   nnz(C) {C.vals.numel()}")
+        for name, evs in timed.items():
+            print(f"  {name:18s} {sum(a.elapsed_time(b) for a, b in evs):8.3f} ms")
+
+from torch.profiler import ProfilerActivity, profile  # noqa: E402
+
+with profile(activities=[ProfilerActivity.CUDA, ProfilerActivity.CPU]) as prof:
+    E.evaluate("A(i,j,k) = X(i,j,k) + Z(i,j,k)", {"X": X, "Z": Z}, F.preset("coo-3"))
+    torch.cuda.synchronize()
+print(prof.key_averages().table(sort_by="cuda_time_total", row_limit=28, max_name_column_width=60))
