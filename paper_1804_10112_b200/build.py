@@ -27,14 +27,17 @@ FLAGS = ["-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr",
          "-Xcompiler", "-fPIC,-O2", "-cudart", "static", "-I", str(INCLUDE), "-I", str(CSRC)]
 if os.environ.get("SL_BUILD_ALT", "") not in ("", "0"):
     FLAGS += ["-DSL_WITH_ALT"]
+# A/B experiments: extra -D definitions for an SL_BUILD_ALT build (e.g. SL_DEFS="-DSL_XGATHER=1")
+FLAGS += os.environ.get("SL_DEFS", "").split()
 
 
 # SL_BUILD_ALT=1: also the A/B alternatives kept for measurement (CSR variants
-# 1 / 3 / 4 and the persistent TMA pipelines of pipe.cu), into _lib/alt/ —
+# 1 / 3 / 4, the persistent TMA pipelines of pipe.cu, the resident-range COO
+# kernel of coo_resident.cu), into _lib/alt/ —
 # load it with SL_LIB_PATH.  The default library carries only the kernels the
 # dispatch chooses.
 ALT = os.environ.get("SL_BUILD_ALT", "") not in ("", "0")
-ALT_ONLY = {"pipe.cu"}
+ALT_ONLY = {"pipe.cu", "coo_resident.cu"}
 
 
 def sources():

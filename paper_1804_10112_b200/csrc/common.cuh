@@ -124,6 +124,9 @@ int launch_csr_pipe(int64_t nrows, const int32_t* pos, const int32_t* crd, const
                     const double* x, double* y, cudaStream_t s);
 void launch_coo_rowptr(int64_t nrows, int64_t nnz, const int32_t* rows, int32_t* rowptr,
                        cudaStream_t s);       // add.cu: row pointer of a row-sorted COO
+bool launch_coo_resident(int64_t nrows, int64_t nnz, const int32_t* rows, const int32_t* cols,
+                         const double* vals, const double* x, double* y,
+                         cudaStream_t s);    // coo_resident.cu: false when the matrix does not fit
 int sm_count();                              // cached per current device
 inline int ceil_div(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
 int launch_status();                         // SL_OK or SL_ERR_CUDA after a launch

@@ -933,6 +933,10 @@ constexpr int kCsrHandoffMaxRow = 28;
 constexpr int kCsrHandoffBatch = 14;
 constexpr int kCsrHandoffBlocks = 12;
 
+// (A smaller stage for short rows — 384 / 448 / 512 / 640 elements, leaving the
+// L1 more room for the x gathers — measured 16.6 / 14.3 / 14.3 / 14.3 us on D1
+// CSR against 14.5 us: no gain, profiles/r2_ab_coo_resident.txt.)
+
 // K2d: CSR warp row-block.  Each warp owns 32 consecutive rows; their
 // nonzeros (contiguous) are staged in warp-private shared memory in rounds of
 // 256 products (8 coalesced loads per lane), and lane r adds the round's
@@ -1207,7 +1211,14 @@ extern "C" int sl_spmv_coo_f64(int64_t nrows, int64_t ncols, int64_t nnz, const 
   // while the pass drains.  D1: 20.4 us (staged tiles below) -> see DESIGN.md.
   // The staged-tile kernel K1 computes on the coordinates alone (no
   // workspace): the path for longer rows, misaligned arrays, or ws == NULL.
-  const char* ck = getenv("SL_COO_KERNEL");       // A/B knob: "tile" forces K1
+  const char* ck = getenv("SL_COO_KERNEL");       // A/B knob: "tile" forces K1, "res" K1s
+#ifdef SL_WITH_ALT
+  // K1s (coo_resident.cu, A/B build): one resident range per SM — measured
+  // 26.5 us on D1 against 18.4 us here (profiles/r2_ab_coo_resident.txt)
+  if (ck && ck[0] == 'r' && vec_ok &&
+      sl_host::launch_coo_resident(nrows, nnz, rows, cols, vals, x, y, s))
+    return sl_host::launch_status();
+#endif
   if (ws && ws_bytes >= sl_spmv_coo_workspace_bytes(nrows) && vec_ok &&
       nnz <= (int64_t)kCsrHandoffMaxRow * nrows && !(ck && ck[0] == 't')) {
     int32_t* rowptr = static_cast<int32_t*>(ws);
