@@ -1,9 +1,9 @@
 """`compile`: `evaluate` bound once to its operands and replayed as a CUDA graph.
 
 The reference plans an expression on every `evaluate` call and, for repeated
-use, lowers it to a specialised kernel once (its code generator; SPEC.md's
-"kernel handle").  The B200 equivalent of that handle is a captured CUDA
-graph: the sparse operands stay resident in HBM, the dense operands a caller
+use, lowers it once to a specialised kernel (its codegen mode, SPEC.md:503-552;
+the module itself is absent from the reference tree).  The B200 equivalent of
+that compiled kernel is a captured CUDA graph: the sparse operands stay resident in HBM, the dense operands a caller
 streams in (x, factor matrices) are read from pinned host memory by copy nodes
 inside the graph, the kernels are exactly the ones `evaluate` launches, and
 the result is written back to pinned host memory by copy nodes — one
