@@ -51,10 +51,10 @@ class Compiled:
 
     def __init__(self, statements: Sequence[Statement], *, fuse: bool = True,
                  host_result: bool = True, device=None):
-        if not torch.cuda.is_available():
-            raise DeviceError("compile needs a CUDA device: there is no CPU fallback")
         if not statements:
             raise ValueError("compile needs at least one statement")
+        if not torch.cuda.is_available():
+            raise DeviceError("compile needs a CUDA device: there is no CPU fallback")
         dev = device
         for _, ins, _ in statements:
             for st in ins.values():

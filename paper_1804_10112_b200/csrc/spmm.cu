@@ -80,6 +80,79 @@ spmm_csr_kernel(int64_t nrows, int64_t K, const int32_t* __restrict__ pos,
   }
 }
 
+// Two columns per lane (K even, X and Y 16-byte aligned): a group of G lanes
+// covers 2G columns with one 16-byte load per lane and nonzero, so a K = 16
+// row gather is 8 lanes and a warp walks four rows at once — half the
+// shuffles, loads and loop instructions per nonzero of the kernel above, which
+// ncu shows issue-bound (the 64^3 stencil, K = 16: 34M warp instructions).
+// The next G entries of the row are loaded while the current ones are used.
+// Same order per output element: acc = dadd(acc, dmul(a, x)) over the row in
+// storage order, so Y is bit-identical.
+SL_DEV double2 ldg2(const double* p) { return __ldg(reinterpret_cast<const double2*>(p)); }
+
+template <int G, int kB = 4>
+__global__ void __launch_bounds__(256)
+spmm_csr_vec2_kernel(int64_t nrows, int64_t K, const int32_t* __restrict__ pos,
+                     const int32_t* __restrict__ crd, const double* __restrict__ vals,
+                     const double* __restrict__ X, double* __restrict__ Y,
+                     int32_t long_min = INT32_MAX) {
+  constexpr int kRowsPerWarp = 32 / G;
+  const int lane = threadIdx.x & 31;
+  const int g = lane / G, gl = lane % G;
+  const unsigned gmask = G == 32 ? 0xffffffffu : (((1u << G) - 1u) << (g * G));
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t w = warp; w * kRowsPerWarp < nrows; w += nwarps) {
+    const int64_t row = w * kRowsPerWarp + g;
+    const int32_t b = row < nrows ? ldg(pos + row) : 0;
+    int32_t e = row < nrows ? ldg(pos + row + 1) : 0;
+    const bool live = row < nrows && e - b <= long_min;   // longer rows: spmm_long_rows_kernel
+    if (!live) e = b;
+    for (int64_t k0 = 0; k0 < K; k0 += 2 * G) {
+      const int64_t k = k0 + 2 * gl;
+      const bool kin = live && k < K;
+      double acc0 = 0.0, acc1 = 0.0;
+      int32_t cq = b + gl < e ? ldg(crd + b + gl) : 0;
+      double vq = b + gl < e ? ldg(vals + b + gl) : 0.0;
+      for (int32_t c0 = b; c0 < e; c0 += G) {
+        const int32_t cn = cq;
+        const double vn = vq;
+        const int32_t qn = c0 + G + gl;                    // the next G entries, in flight
+        cq = qn < e ? ldg(crd + qn) : 0;
+        vq = qn < e ? ldg(vals + qn) : 0.0;
+        const int n = min(G, e - c0);
+        int u = 0;
+        for (; u + kB <= n; u += kB) {
+          int32_t c[kB];
+          double a[kB];
+          double2 xv[kB];
+#pragma unroll
+          for (int t = 0; t < kB; ++t) {
+            c[t] = __shfl_sync(gmask, cn, u + t, G);
+            a[t] = __shfl_sync(gmask, vn, u + t, G);
+          }
+#pragma unroll
+          for (int t = 0; t < kB; ++t)
+            xv[t] = kin ? ldg2(X + (int64_t)c[t] * K + k) : make_double2(0.0, 0.0);
+#pragma unroll
+          for (int t = 0; t < kB; ++t) {
+            acc0 = dadd(acc0, dmul(a[t], xv[t].x));
+            acc1 = dadd(acc1, dmul(a[t], xv[t].y));
+          }
+        }
+        for (; u < n; ++u) {
+          const int32_t c = __shfl_sync(gmask, cn, u, G);
+          const double a = __shfl_sync(gmask, vn, u, G);
+          const double2 xv = kin ? ldg2(X + (int64_t)c * K + k) : make_double2(0.0, 0.0);
+          acc0 = dadd(acc0, dmul(a, xv.x));
+          acc1 = dadd(acc1, dmul(a, xv.y));
+        }
+      }
+      if (kin) *reinterpret_cast<double2*>(Y + row * K + k) = make_double2(acc0, acc1);
+    }
+  }
+}
+
 // Rows longer than long_min, listed by spmm_mark_long_kernel: one CTA per
 // row.  A lone group walking a power-law row keeps only kB gathers in flight
 // per lane, so a 10^5-nonzero row costs ~10^5/kB dependent gather latencies.
@@ -159,6 +232,23 @@ namespace {
 int spmm_launch(int64_t nrows, int64_t ncols, int64_t K, const int32_t* pos, const int32_t* crd,
                 const double* vals, const double* X, double* Y, int32_t long_min,
                 cudaStream_t s) {
+  // even K >= 8, 16-byte aligned X and Y: two columns per lane (A/B knob SL_SPMM_VEC2=0)
+  static const bool vec2_on = [] {
+    const char* e = getenv("SL_SPMM_VEC2");
+    return !(e && e[0] == '0');
+  }();
+  if (vec2_on && K >= 8 && K % 2 == 0 && sl_host::aligned16(X) && sl_host::aligned16(Y)) {
+    const int G2 = K > 32 ? 32 : (K > 16 ? 16 : (K > 8 ? 8 : 4));
+    const int64_t rpb = 8 * (32 / G2);
+    const int grid2 = (int)std::min<int64_t>(ceil_div(nrows, rpb), (int64_t)sl_host::sm_count() * 64);
+    switch (G2) {
+      case 32: spmm_csr_vec2_kernel<32><<<grid2, 256, 0, s>>>(nrows, K, pos, crd, vals, X, Y, long_min); break;
+      case 16: spmm_csr_vec2_kernel<16><<<grid2, 256, 0, s>>>(nrows, K, pos, crd, vals, X, Y, long_min); break;
+      case 8: spmm_csr_vec2_kernel<8><<<grid2, 256, 0, s>>>(nrows, K, pos, crd, vals, X, Y, long_min); break;
+      default: spmm_csr_vec2_kernel<4><<<grid2, 256, 0, s>>>(nrows, K, pos, crd, vals, X, Y, long_min); break;
+    }
+    return sl_host::launch_status();
+  }
   const int G = K >= 32 ? 32 : (K > 8 ? 16 : (K > 4 ? 8 : (K > 2 ? 4 : (K > 1 ? 2 : 1))));
   const int64_t rows_per_block = 8 * (32 / G);
   const int grid = (int)std::min<int64_t>(ceil_div(nrows, rows_per_block),

@@ -282,3 +282,20 @@ def test_plan_cache_identity_fast_path(monkeypatch):
     ph = Eng.evaluate(expr, {"A": A, "x": x}, out_format=hv)
     assert ph.out_format is hv and ph is not p1
     assert Eng.evaluate(expr, {"A": A, "x": x}) is p1
+
+
+# ---- compile: no CPU fallback ---------------------------------------------------
+
+def test_compile_without_a_gpu_raises_device_error():
+    import torch
+
+    import paper_1804_10112_b200 as slb
+    from paper_1804_10112_b200.errors import DeviceError
+
+    if torch.cuda.is_available():
+        pytest.skip("a CUDA device is present")
+    x = F.dense_storage(np.ones(4), device=None)
+    with pytest.raises(DeviceError):
+        slb.compile("y(i) = x(i)", {"x": x})
+    with pytest.raises(ValueError):
+        slb.compile_many([])
