@@ -284,6 +284,13 @@ int sl_spmv_csr_spx_f64(int64_t nrows, int64_t n, int64_t nnz, const int32_t* po
 int sl_spmm_csr_f64(int64_t nrows, int64_t ncols, int64_t K, const int32_t* pos,
                     const int32_t* crd, const double* vals, const double* X, double* Y,
                     void* stream);
+/* The same product with the nonzero count known to the caller (nnz =
+ * pos[nrows]; -1: unknown): the average row length picks the kernel shape
+ * (two columns per lane for rows averaging >= 16 nonzeros).  Bit-identical
+ * to sl_spmm_csr_f64; same reference loop nest. */
+int sl_spmm_csr_nnz_f64(int64_t nrows, int64_t ncols, int64_t K, int64_t nnz, const int32_t* pos,
+                        const int32_t* crd, const double* vals, const double* X, double* Y,
+                        void* stream);
 /* The same product with rows longer than long_min split out (power-law
  * rows): a device pass lists them (workspace: a counter and the list), the
  * group kernel skips them, and one CTA per listed row gathers its X rows with

@@ -98,6 +98,7 @@ SIGNATURES = {
     "sl_spmv_csr_spx_f64": ([_i64, _i64, _i64, _p, _p, _p, _i64, _p, _p, _p, _p, _sz, _p],
                             ctypes.c_int),
     "sl_spmm_csr_f64": ([_i64, _i64, _i64, _p, _p, _p, _p, _p, _p], ctypes.c_int),
+    "sl_spmm_csr_nnz_f64": ([_i64, _i64, _i64, _i64, _p, _p, _p, _p, _p, _p], ctypes.c_int),
     "sl_spmm_csr_split_workspace_bytes": ([_i64, _i64, ctypes.c_int32], _i64),
     "sl_spmm_csr_split_f64": ([_i64, _i64, _i64, _i64, _p, _p, _p, _p, _p, ctypes.c_int32, _p,
                                _i64, _p], ctypes.c_int),

@@ -90,13 +90,17 @@ spmm_csr_kernel(int64_t nrows, int64_t K, const int32_t* __restrict__ pos,
 // storage order, so Y is bit-identical.
 SL_DEV double2 ldg2(const double* p) { return __ldg(reinterpret_cast<const double2*>(p)); }
 
-template <int G, int kB = 4>
+#ifndef SL_SPMM_KB
+#define SL_SPMM_KB 4
+#endif
+template <int G, int kB = SL_SPMM_KB, int kE = 2>
 __global__ void __launch_bounds__(256)
 spmm_csr_vec2_kernel(int64_t nrows, int64_t K, const int32_t* __restrict__ pos,
                      const int32_t* __restrict__ crd, const double* __restrict__ vals,
                      const double* __restrict__ X, double* __restrict__ Y,
                      int32_t long_min = INT32_MAX) {
   constexpr int kRowsPerWarp = 32 / G;
+  constexpr int kChunk = kE * G;          // row entries per load step (kE per lane)
   const int lane = threadIdx.x & 31;
   const int g = lane / G, gl = lane % G;
   const unsigned gmask = G == 32 ? 0xffffffffu : (((1u << G) - 1u) << (g * G));
@@ -112,40 +116,54 @@ spmm_csr_vec2_kernel(int64_t nrows, int64_t K, const int32_t* __restrict__ pos,
       const int64_t k = k0 + 2 * gl;
       const bool kin = live && k < K;
       double acc0 = 0.0, acc1 = 0.0;
-      int32_t cq = b + gl < e ? ldg(crd + b + gl) : 0;
-      double vq = b + gl < e ? ldg(vals + b + gl) : 0.0;
-      for (int32_t c0 = b; c0 < e; c0 += G) {
-        const int32_t cn = cq;
-        const double vn = vq;
-        const int32_t qn = c0 + G + gl;                    // the next G entries, in flight
-        cq = qn < e ? ldg(crd + qn) : 0;
-        vq = qn < e ? ldg(vals + qn) : 0.0;
-        const int n = min(G, e - c0);
-        int u = 0;
-        for (; u + kB <= n; u += kB) {
-          int32_t c[kB];
-          double a[kB];
-          double2 xv[kB];
+      int32_t cq[kE];
+      double vq[kE];
 #pragma unroll
-          for (int t = 0; t < kB; ++t) {
-            c[t] = __shfl_sync(gmask, cn, u + t, G);
-            a[t] = __shfl_sync(gmask, vn, u + t, G);
-          }
+      for (int h = 0; h < kE; ++h) {
+        const int32_t q = b + h * G + gl;
+        cq[h] = q < e ? ldg(crd + q) : 0;
+        vq[h] = q < e ? ldg(vals + q) : 0.0;
+      }
+      for (int32_t c0 = b; c0 < e; c0 += kChunk) {
+        int32_t cn[kE];
+        double vn[kE];
 #pragma unroll
-          for (int t = 0; t < kB; ++t)
-            xv[t] = kin ? ldg2(X + (int64_t)c[t] * K + k) : make_double2(0.0, 0.0);
-#pragma unroll
-          for (int t = 0; t < kB; ++t) {
-            acc0 = dadd(acc0, dmul(a[t], xv[t].x));
-            acc1 = dadd(acc1, dmul(a[t], xv[t].y));
-          }
+        for (int h = 0; h < kE; ++h) {
+          cn[h] = cq[h];
+          vn[h] = vq[h];
+          const int32_t q = c0 + kChunk + h * G + gl;      // the next chunk, in flight
+          cq[h] = q < e ? ldg(crd + q) : 0;
+          vq[h] = q < e ? ldg(vals + q) : 0.0;
         }
-        for (; u < n; ++u) {
-          const int32_t c = __shfl_sync(gmask, cn, u, G);
-          const double a = __shfl_sync(gmask, vn, u, G);
-          const double2 xv = kin ? ldg2(X + (int64_t)c * K + k) : make_double2(0.0, 0.0);
-          acc0 = dadd(acc0, dmul(a, xv.x));
-          acc1 = dadd(acc1, dmul(a, xv.y));
+#pragma unroll
+        for (int h = 0; h < kE; ++h) {
+          const int n = min(G, e - c0 - h * G);             // entries of this register (<= 0: none)
+          int u = 0;
+          for (; u + kB <= n; u += kB) {
+            int32_t c[kB];
+            double a[kB];
+            double2 xv[kB];
+#pragma unroll
+            for (int t = 0; t < kB; ++t) {
+              c[t] = __shfl_sync(gmask, cn[h], u + t, G);
+              a[t] = __shfl_sync(gmask, vn[h], u + t, G);
+            }
+#pragma unroll
+            for (int t = 0; t < kB; ++t)
+              xv[t] = kin ? ldg2(X + (int64_t)c[t] * K + k) : make_double2(0.0, 0.0);
+#pragma unroll
+            for (int t = 0; t < kB; ++t) {
+              acc0 = dadd(acc0, dmul(a[t], xv[t].x));
+              acc1 = dadd(acc1, dmul(a[t], xv[t].y));
+            }
+          }
+          for (; u < n; ++u) {
+            const int32_t c = __shfl_sync(gmask, cn[h], u, G);
+            const double a = __shfl_sync(gmask, vn[h], u, G);
+            const double2 xv = kin ? ldg2(X + (int64_t)c * K + k) : make_double2(0.0, 0.0);
+            acc0 = dadd(acc0, dmul(a, xv.x));
+            acc1 = dadd(acc1, dmul(a, xv.y));
+          }
         }
       }
       if (kin) *reinterpret_cast<double2*>(Y + row * K + k) = make_double2(acc0, acc1);
@@ -231,13 +249,20 @@ namespace {
 
 int spmm_launch(int64_t nrows, int64_t ncols, int64_t K, const int32_t* pos, const int32_t* crd,
                 const double* vals, const double* X, double* Y, int32_t long_min,
-                cudaStream_t s) {
-  // even K >= 8, 16-byte aligned X and Y: two columns per lane (A/B knob SL_SPMM_VEC2=0)
-  static const bool vec2_on = [] {
+                cudaStream_t s, int64_t nnz = -1) {
+  // Even K >= 8, 16-byte aligned X and Y, rows averaging >= 16 nonzeros: two
+  // columns per lane (64^3 stencil, K = 8 / 16 / 32: 76.2 / 115.9 / 204.7 ->
+  // 55.7 / 92.2 / 152.7 us).  Short ragged rows stay with one column per lane:
+  // a warp walking four rows waits for the longest (D1, K = 16: 56.9 us there,
+  // 61.8 us here).  Gathers in flight per lane 1 / 2 / 4 / 8: 123.0 / 96.9 /
+  // 92.2 / 104.4 us (K = 16).  A/B knob SL_SPMM_VEC2=0 / 1 (1: whatever the rows).
+  static const int vec2_knob = [] {
     const char* e = getenv("SL_SPMM_VEC2");
-    return !(e && e[0] == '0');
+    return e ? (e[0] == '0' ? 0 : 2) : 1;
   }();
-  if (vec2_on && K >= 8 && K % 2 == 0 && sl_host::aligned16(X) && sl_host::aligned16(Y)) {
+  const bool rows_ok = vec2_knob == 2 || (nnz >= 0 && nnz >= 16 * nrows);
+  if (vec2_knob && rows_ok && K >= 8 && K % 2 == 0 && sl_host::aligned16(X) &&
+      sl_host::aligned16(Y)) {
     const int G2 = K > 32 ? 32 : (K > 16 ? 16 : (K > 8 ? 8 : 4));
     const int64_t rpb = 8 * (32 / G2);
     const int grid2 = (int)std::min<int64_t>(ceil_div(nrows, rpb), (int64_t)sl_host::sm_count() * 64);
@@ -286,6 +311,14 @@ extern "C" int sl_spmm_csr_f64(int64_t nrows, int64_t ncols, int64_t K, const in
   return spmm_launch(nrows, ncols, K, pos, crd, vals, X, Y, INT32_MAX, as_stream(stream));
 }
 
+extern "C" int sl_spmm_csr_nnz_f64(int64_t nrows, int64_t ncols, int64_t K, int64_t nnz,
+                                   const int32_t* pos, const int32_t* crd, const double* vals,
+                                   const double* X, double* Y, void* stream) {
+  const int st = spmm_check(nrows, ncols, K, pos, X, Y);
+  if (st >= 0) return st;
+  return spmm_launch(nrows, ncols, K, pos, crd, vals, X, Y, INT32_MAX, as_stream(stream), nnz);
+}
+
 extern "C" int64_t sl_spmm_csr_split_workspace_bytes(int64_t nrows, int64_t nnz,
                                                      int32_t long_min) {
   if (nrows <= 0 || long_min < 0) return 0;
@@ -310,7 +343,7 @@ extern "C" int sl_spmm_csr_split_f64(int64_t nrows, int64_t ncols, int64_t K, in
                           0, s>>>(nrows, pos, long_min, list, count);
   int rc = sl_host::launch_status();
   if (rc != SL_OK) return rc;
-  rc = spmm_launch(nrows, ncols, K, pos, crd, vals, X, Y, long_min, s);
+  rc = spmm_launch(nrows, ncols, K, pos, crd, vals, X, Y, long_min, s, nnz);
   if (rc != SL_OK) return rc;
   const int64_t nlong = std::min<int64_t>(nrows, nnz / ((int64_t)long_min + 1) + 1);
   const int lgrid = (int)std::min<int64_t>(nlong, 4LL * sl_host::sm_count());

@@ -167,11 +167,11 @@ def spmm_csr(nrows, ncols, pos, crd, vals, X, Y=None, long_min=None):
     X = _t(X, F64, "X")
     K = X.shape[-1] if X.dim() == 2 else X.numel() // max(ncols, 1)
     Y = _out(Y, nrows * K, F64, vals, "Y").view(nrows, K) if Y is None else _t(Y, F64, "Y")
-    if long_min is None:
-        _lib.check(L().sl_spmm_csr_f64(nrows, ncols, K, P(pos), P(crd), P(vals), P(X), P(Y),
-                                       S()), "spmm_csr")
-        return Y
     nnz = crd.numel()
+    if long_min is None:
+        _lib.check(L().sl_spmm_csr_nnz_f64(nrows, ncols, K, nnz, P(pos), P(crd), P(vals), P(X),
+                                           P(Y), S()), "spmm_csr")
+        return Y
     ws = _ws(L().sl_spmm_csr_split_workspace_bytes(nrows, nnz, long_min), vals)
     _lib.check(L().sl_spmm_csr_split_f64(nrows, ncols, K, nnz, P(pos), P(crd), P(vals), P(X),
                                          P(Y), long_min, P(ws), 0 if ws is None else ws.numel(),

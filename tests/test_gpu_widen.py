@@ -55,7 +55,7 @@ def test_widen_goldens_kernels_and_evaluate():
     assert seen >= 16
 
 
-@pytest.mark.parametrize("Kc", [1, 2, 5, 8, 16, 32, 40, 64])
+@pytest.mark.parametrize("Kc", [1, 2, 5, 8, 16, 32, 40, 64, 72])
 def test_spmm_stencil_vs_oracle(orc, Kc):
     st = wl.stencil27(g=24, seed=4)
     n = st["nrows"]
