@@ -748,7 +748,12 @@ def run_formats(torch, K, F, wl, evaluate, compile_, dev, timer, peak, l2, clk, 
     res["csr_hashx_H1"] = {"ms": round(tt["probe"], 5), "GB/s": round(bh / tt["probe"] / 1e6, 1),
                            "frac": round(bh / tt["probe"] / 1e6 / peak, 4),
                            "locates/s": round(nnz / tt["probe"] * 1e3, 1), "bytes": bh,
-                           "path": "per-nonzero warp-cooperative probing"}
+                           "path": "per-nonzero warp-cooperative probing",
+                           "note": "H1's table (c mod 131072 over coordinates in [0, 200000)) "
+                                   "holds one 20.6K-slot probe cluster: mean probe length 1963 "
+                                   "over all coordinates (max 20.5K), so this path reads ~3.9G "
+                                   "slots per SpMV; evaluate() resolves each coordinate once "
+                                   "(slot map, next entry) whenever nnz >= table width"}
     res["csr_hashx_map_H1"] = {"ms": round(tt["map"], 5), "GB/s": round(bh / tt["map"] / 1e6, 1),
                                "frac": round(bh / tt["map"] / 1e6 / peak, 4),
                                "locates/s": round(nnz / tt["map"] * 1e3, 1), "bytes": bh,
