@@ -239,8 +239,10 @@ class KernelTimer:
                 f"in use; its K launches back to back in one event pair (no flush), submitted "
                 f"as one CUDA graph replay")
 
-    def run(self, fns, steps, warmup):
-        """fns: {name: [callable per operand copy]}; returns {name: ms per launch}."""
+    def run(self, fns, steps, warmup, capture=True):
+        """fns: {name: [callable per operand copy]}; returns {name: ms per launch}.
+        capture=False: the callables read the device between launches (data-
+        dependent output sizes), so no graph capture is attempted."""
         torch = self.torch
         out = {}
         for name, copies in fns.items():
@@ -260,11 +262,11 @@ class KernelTimer:
                 torch.cuda.synchronize()
                 out[name] = float(np.mean([a.elapsed_time(b) for a, b in evs]))
             else:
-                out[name] = self._rotate(name, copies, steps)
+                out[name] = self._rotate(name, copies, steps, capture)
             self.launches += steps
         return out
 
-    def _rotate(self, name, copies, steps):
+    def _rotate(self, name, copies, steps, capture=True):
         """K launches rotating over the copies, back to back in one event pair.
         They are captured once into a CUDA graph and the graph is replayed
         inside the events, so the host's per-call cost (ctypes marshalling,
@@ -274,7 +276,7 @@ class KernelTimer:
         nc = len(copies)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         g = None
-        if self.graphs:
+        if self.graphs and capture:
             try:
                 g = torch.cuda.CUDAGraph()
                 with torch.cuda.graph(g):
@@ -1006,7 +1008,7 @@ def run_formats(torch, K, F, wl, evaluate, compile_, dev, timer, peak, l2, clk, 
                             F.preset("coo-3"))
 
     with clk.timed("formats"):
-        tt = timer.run({"plus3": [plus3, plus3]}, 3, 1)
+        tt = timer.run({"plus3": [plus3, plus3]}, 3, 2, capture=False)
     nz_c = int(out["c"].levels[2].crd.numel())
     b_p = 20 * nnz + 20 * (nnz // 2) + 20 * nz_c
     res["plus3_coo3_D5"] = {"ms": round(tt["plus3"], 4), "GB/s": round(b_p / tt["plus3"] / 1e6, 1),
