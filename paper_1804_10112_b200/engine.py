@@ -481,13 +481,18 @@ def _coo3_grouped(X: TensorStorage):
             LevelStorage(X.levels[2].spec, pos=pos, crd=crd, device=dev)], vals
 
 
-def _fibre_coo(X: TensorStorage):
-    """(fibre key i*J + j as int64, k, vals) of a COO-3 or CSF operand, in
-    storage order."""
-    J = X.dims[1]
+def _fibre_coo(X: TensorStorage, narrow: bool = False):
+    """(fibre key i*J + j, k, vals) of a COO-3 or CSF operand, in storage
+    order.  Keys are int64; with `narrow`, int32 when I*J fits (half the
+    traffic of every pass over the keys)."""
+    I, J = X.dims[0], X.dims[1]
+    kt = torch.int32 if narrow and I * J <= 2 ** 31 - 1 else torch.int64
     if format_class(X.format) == "coo3":
-        key = X.levels[0].crd.to(torch.int64) * J + X.levels[1].crd.to(torch.int64)
+        key = X.levels[0].crd.to(kt) * J + X.levels[1].crd.to(kt)
         return key, X.levels[2].crd, X.vals[:X.levels[2].crd.numel()]
+    if kt is torch.int32:
+        key, kc, v = _fibre_coo(X)
+        return key.to(kt), kc, v
     L = X.levels
     n1 = int(L[1].crd.numel())
     nnz = int(L[2].crd.numel())
@@ -515,17 +520,17 @@ def _plus3(p: Plan, X: TensorStorage, Z: TensorStorage, dev) -> TensorStorage:
     entries each) as single rows serialised the long-row path (22.8 ms of
     A + B; k-blocked: see DESIGN.md)."""
     I, J, Kd = X.dims
-    xk, xc, xv = _fibre_coo(X)
-    zk, zc, zv = _fibre_coo(Z)
+    xk, xc, xv = _fibre_coo(X, narrow=True)
+    zk, zc, zv = _fibre_coo(Z, narrow=True)
     uq = lambda t: torch.unique_consecutive(t) if t.numel() else t  # noqa: E731
     U = torch.unique(torch.cat([uq(xk), uq(zk)]))                   # sorted fibre keys
     nU = int(U.numel())
-    xf = torch.searchsorted(U, xk)
-    zf = torch.searchsorted(U, zk)
+    xf = torch.searchsorted(U, xk, out_int32=True)
+    zf = torch.searchsorted(U, zk, out_int32=True)
     if nU:
         # entries per union fibre: the keys are sorted, so two boundary searches
         # (a bincount's atomics pile up on the long fibres: 4 ms at D5)
-        ub = torch.cat([U, U[-1:] + 1])
+        ub = torch.cat([U, U[-1:] + 1])       # (a narrow key is at most 2^31 - 2)
         ln = torch.diff(torch.searchsorted(xk, ub)) + torch.diff(torch.searchsorted(zk, ub))
         kbits = max(int(Kd) - 1, 1).bit_length()
         want = torch.ceil(torch.log2((ln.double() / _PLUS3_ROW).clamp_(min=1.0))).to(torch.int64)
@@ -539,8 +544,9 @@ def _plus3(p: Plan, X: TensorStorage, Z: TensorStorage, dev) -> TensorStorage:
         nR = 0
     if nR > 2 ** 31 - 1:
         raise UnsupportedMergeError("3rd-order PLUS: the union's row space exceeds int32")
-    xr = (rowbase[xf] + (xc.to(torch.int64) >> sh[xf])).to(torch.int32)
-    zr = (rowbase[zf] + (zc.to(torch.int64) >> sh[zf])).to(torch.int32)
+    rb32, sh32 = rowbase.to(torch.int32), sh.to(torch.int32)
+    xr = rb32[xf] + (xc >> sh32[xf])
+    zr = rb32[zf] + (zc >> sh32[zf])
     a_pos, a_crd, a_vals = K.coo_to_csr(nR, xr, xc, xv)
     c_pos, c_crd, c_vals = K.add_csr(nR, a_pos, a_crd, a_vals, zc, zv, b_rows=zr)
     f = p.out_format
@@ -549,17 +555,17 @@ def _plus3(p: Plan, X: TensorStorage, Z: TensorStorage, dev) -> TensorStorage:
     fi, fj = (U // J).to(torch.int32), (U % J).to(torch.int32)
 
     def out_fibres():       # union fibre of every output entry
-        rowfib = torch.repeat_interleave(torch.arange(nU, device=dev), nblk)
-        return rowfib[K.csr_rows(nR, c_pos, nnz).to(torch.int64)]
+        rowfib = torch.repeat_interleave(torch.arange(nU, dtype=torch.int32, device=dev), nblk)
+        return rowfib[K.csr_rows(nR, c_pos, nnz)]
 
     if ocls == "dense3":
         out = torch.zeros(I * J * Kd, dtype=torch.float64, device=dev)
         if nnz:
-            out[U[out_fibres()] * Kd + c_crd.to(torch.int64)] = c_vals
+            out[U.to(torch.int64)[out_fibres()] * Kd + c_crd.to(torch.int64)] = c_vals
         return TensorStorage(f, (I, J, Kd), [LevelStorage(s_, n=d, device=dev)
                                              for s_, d in zip(f.levels, (I, J, Kd))], out)
     if ocls == "coo3":
-        fib = out_fibres() if nnz else torch.empty(0, dtype=torch.int64, device=dev)
+        fib = out_fibres() if nnz else torch.empty(0, dtype=torch.int32, device=dev)
         return TensorStorage(f, (I, J, Kd), [LevelStorage(f.levels[0], pos=[0, nnz], crd=fi[fib],
                                                           device=dev),
                                              LevelStorage(f.levels[1], crd=fj[fib], device=dev),
