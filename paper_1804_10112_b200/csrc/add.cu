@@ -177,11 +177,13 @@ SL_DEV int count_row_idx(int ia, int iah, int ib, int ibh, const int32_t* s_col)
 // is grouped before it gets here), and A comes first on ties, so an A entry is
 // always the first of its output.  The values are read from global memory by
 // emit_outputs, coalesced across the tile's consecutive outputs.
-SL_DEV int fill_row_src(int ia, int iah, int ib, int ibh, int kcs, const int32_t* s_col,
-                        int32_t* oc, uint32_t* os) {
+SL_DEV void fill_row_src(int ia, int iah, int ib, int ibh, int kcs, const int32_t* s_col,
+                         uint2* out) {
   const uint32_t base = smem_u32(s_col);
-  uint32_t pc = smem_u32(oc) - 4u, ps = smem_u32(os) - 4u;   // output n at pc + 4 (n + 1)
-  int n = -1;
+  // one 8-byte record (column, sources) per output, rewritten by every
+  // element of the output (a single st.shared.v2 and one running address per
+  // step; two arrays cost a second store and a second address)
+  uint32_t po = smem_u32(out) - 8u;                            // output n at po + 8 (n + 1)
   int32_t last = -1;
   uint32_t src = 0;
   int32_t ca = lds32(base + 4u * ia);
@@ -192,15 +194,12 @@ SL_DEV int fill_row_src(int ia, int iah, int ib, int ibh, int kcs, const int32_t
     const bool ta = ca <= cb;
     const int32_t c = ta ? ca : cb;
     const bool fresh = c != last;
-    n += fresh;
-    pc += fresh ? 4u : 0u;
-    ps += fresh ? 4u : 0u;
+    po += fresh ? 8u : 0u;
     last = c;
     src = fresh ? 0u : src;
     const uint32_t bsrc = ((src >> 11) & 0x7ffu) ? src : (src | ((uint32_t)(ib - kcs + 1) << 11));
     src = ta ? (src | (uint32_t)(ia + 1)) : bsrc + (1u << 22);
-    sts32(pc, (uint32_t)c);
-    sts32(ps, src);
+    sts64(po, (uint32_t)c, src);
     ia += ta;
     ib += !ta;
     const int idx = ta ? ia : ib;
@@ -209,7 +208,6 @@ SL_DEV int fill_row_src(int ia, int iah, int ib, int ibh, int kcs, const int32_t
     ca = ta ? nx : ca;
     cb = ta ? cb : nx;
   }
-  return n + 1;
 }
 
 // Writes outputs [0, n) of a staged run: column from the stage, value
@@ -221,18 +219,21 @@ SL_DEV int fill_row_src(int ia, int iah, int ib, int ibh, int kcs, const int32_t
 constexpr int kEmitUnroll = SL_EMIT_UNROLL;
 
 template <int kThreads>
-SL_DEV void emit_outputs(int n, const int32_t* s_ccrd, const uint32_t* s_src, int64_t a0,
+SL_DEV void emit_outputs(int n, const uint2* s_out, int64_t a0,
                          int64_t b0, const double* __restrict__ a_vals,
                          const double* __restrict__ b_vals, int32_t* gc, double* gv) {
   const double* ap = a_vals + a0 - 1;      // source fields hold stage index + 1
   const double* bp = b_vals + b0 - 1;
   for (int q0 = threadIdx.x; q0 < n; q0 += kEmitUnroll * kThreads) {
     uint32_t src[kEmitUnroll];
+    int32_t col[kEmitUnroll];
     double av[kEmitUnroll], bv[kEmitUnroll];
 #pragma unroll
     for (int u = 0; u < kEmitUnroll; ++u) {
       const int q = q0 + u * kThreads;
-      src[u] = q < n ? s_src[q] : 0u;
+      const uint2 o = q < n ? s_out[q] : make_uint2(0u, 0u);
+      col[u] = (int32_t)o.x;
+      src[u] = o.y;
     }
 #pragma unroll
     for (int u = 0; u < kEmitUnroll; ++u) {
@@ -258,7 +259,7 @@ SL_DEV void emit_outputs(int n, const int32_t* s_ccrd, const uint32_t* s_src, in
         // either way) — no selects on the 64-bit values (ncu: 6 of the
         // emitter's ~46 instructions per output)
         const double e = dadd(av[u], g);
-        gc[q] = s_ccrd[q];
+        gc[q] = col[u];
         gv[q] = dadd(0.0, e);
       }
     }
@@ -464,8 +465,7 @@ add_tile_kernel(int64_t nrows, const int32_t* __restrict__ a_pos, const int32_t*
   // output its column and its sources (fill_row_src) — the values are read
   // from global memory when the stage is written out, so only columns are
   // staged and the block's shared memory stays at ~17 KB
-  __shared__ int32_t s_ccrd[kValues ? 2 * kAddCap : 1];
-  __shared__ uint32_t s_src[kValues ? 2 * kAddCap : 1];
+  __shared__ __align__(8) uint2 s_out[kValues ? 2 * kAddCap : 1];
   const int tid = threadIdx.x;
   if (tid == 0) {
     mbar_init(&bar, 1);
@@ -671,11 +671,10 @@ add_tile_kernel(int64_t nrows, const int32_t* __restrict__ a_pos, const int32_t*
         const int row = g0 + tid;
         if (row < g1)
           fill_row_src(s_apos[row] - oa, s_apos[row + 1] - oa, kCS + s_bpos[row] - ob,
-                       kCS + s_bpos[row + 1] - ob, kCS, s_col, s_ccrd + (s_rbase[row] - ob0),
-                       s_src + (s_rbase[row] - ob0));
+                       kCS + s_bpos[row + 1] - ob, kCS, s_col, s_out + (s_rbase[row] - ob0));
         __syncthreads();
         // the group's outputs, coalesced
-        emit_outputs<kAddRows>(ob1 - ob0, s_ccrd, s_src, oa, ob, a_vals, b_vals,
+        emit_outputs<kAddRows>(ob1 - ob0, s_out, oa, ob, a_vals, b_vals,
                                c_crd + tile_out + ob0, c_vals + tile_out + ob0);
       }
       __syncthreads();                     // stages free for the next group
@@ -698,9 +697,9 @@ add_tile_kernel(int64_t nrows, const int32_t* __restrict__ a_pos, const int32_t*
     if (row < nr)
       fill_row_src(s_apos[row] - (int32_t)ra.lo0, s_apos[row + 1] - (int32_t)ra.lo0,
                    kCS + s_bpos[row] - (int32_t)rb.lo0, kCS + s_bpos[row + 1] - (int32_t)rb.lo0,
-                   kCS, s_col, s_ccrd + s_rbase[row], s_src + s_rbase[row]);
+                   kCS, s_col, s_out + s_rbase[row]);
     __syncthreads();
-    emit_outputs<kAddRows>((int)n_out, s_ccrd, s_src, ra.lo0, rb.lo0, a_vals, b_vals,
+    emit_outputs<kAddRows>((int)n_out, s_out, ra.lo0, rb.lo0, a_vals, b_vals,
                            c_crd + tile_out, c_vals + tile_out);
   } else if (mine) {                       // unaligned operands: merged from global memory
     merge_row<true>(s_apos[tid], s_apos[tid + 1], s_bpos[tid], s_bpos[tid + 1], gacc,
