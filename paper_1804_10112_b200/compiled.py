@@ -153,6 +153,9 @@ class Compiled:
         """Launch the graph on `stream` (default: the current stream) and return
         the result storage(s) without waiting; call `synchronize()` before
         reading a host result."""
+        if self.device.index is not None and self.device.index != torch.cuda.current_device():
+            with torch.cuda.device(self.device):     # replay on the operands' device
+                return self(stream)
         if stream is None:
             self._graph.replay()
             self._last_stream = torch.cuda.current_stream(self.device)
