@@ -445,7 +445,7 @@ add_tile_kernel(int64_t nrows, const int32_t* __restrict__ a_pos, const int32_t*
                 int32_t* __restrict__ c_pos, int32_t* __restrict__ c_crd,
                 double* __restrict__ c_vals, int64_t* __restrict__ tile_tot,
                 int64_t* __restrict__ super_tot, bool staged_ok,
-                const int32_t* __restrict__ guard = nullptr) {
+                const int32_t* __restrict__ guard = nullptr, uint8_t* __restrict__ perm = nullptr) {
   constexpr bool kValues = kMode != 0;
   constexpr int kAddCap = kValues ? kAddCapFill : kAddCapCount;
   if (guard != nullptr) {                  // nothing to merge (see the exact convert)
@@ -611,6 +611,9 @@ add_tile_kernel(int64_t nrows, const int32_t* __restrict__ a_pos, const int32_t*
       cnt = mine ? s_rbase[tid] : 0;
     } else if (fits) {
       const int row = sorted_row();
+      // the fill merges the same rows in the same order: it reads the
+      // permutation back instead of sorting again (four barriers per tile)
+      if (perm) perm[tile * kAddRows + tid] = (uint8_t)row;
       if (row < nr)
         s_rbase[row] = count_row_idx(s_apos[row] - (int32_t)ra.lo0, s_apos[row + 1] - (int32_t)ra.lo0,
                                      kCS + s_bpos[row] - (int32_t)rb.lo0,
@@ -636,6 +639,8 @@ add_tile_kernel(int64_t nrows, const int32_t* __restrict__ a_pos, const int32_t*
   // fill launched with PDL behind the count pass: the stage copies above are
   // in flight; the counts, totals and c_pos it wrote are read from here on
   pdl_wait();
+  // a tile that fits the fill's stage fitted the count's: its merge order is in perm
+  const int prow = fits && perm ? (int)ldg(perm + tile * kAddRows + tid) : -1;
   if (kMode == 1) {
     tile_out = ldg(c_pos + r0);
     n_out = ldg(c_pos + r0 + nr) - tile_out;
@@ -691,7 +696,7 @@ add_tile_kernel(int64_t nrows, const int32_t* __restrict__ a_pos, const int32_t*
     return;
   }
   if (fits) {
-    const int row = sorted_row();
+    const int row = perm ? prow : sorted_row();
     mbar_wait(&bar, 0);
     // n_out <= na + nb <= 2 kAddCap: the tile's outputs fit the output stage
     if (row < nr)
@@ -822,10 +827,13 @@ static size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
 static size_t add_tiles_bytes(int64_t nrows) { return al256((size_t)add_ntiles(nrows) * 8); }
 static size_t add_super_bytes(int64_t nrows) { return al256((size_t)add_nsuper(nrows) * 8); }
 
+static size_t add_rowptr_bytes(int64_t nrows) { return al256((size_t)(nrows + 1) * sizeof(int32_t)); }
+static size_t add_perm_bytes(int64_t nrows) { return al256((size_t)add_ntiles(nrows) * kAddRows); }
+
 extern "C" size_t sl_add_csr_workspace_bytes(int64_t nrows, int64_t b_nnz) {
   (void)b_nnz;
-  return add_tiles_bytes(nrows) + add_super_bytes(nrows) + (size_t)(nrows + 1) * sizeof(int32_t) +
-         256;
+  return add_tiles_bytes(nrows) + add_super_bytes(nrows) + add_rowptr_bytes(nrows) +
+         add_perm_bytes(nrows) + 256;
 }
 
 // the fill stages values at their columns' indices: needs 16-byte-aligned operands
@@ -839,12 +847,15 @@ struct AddWs {
   int64_t* tiles;
   int64_t* supers;
   int32_t* rowptr;
+  uint8_t* perm;       // [ntiles][kAddRows]: each staged tile's merge order (count -> fill)
 };
 
 static AddWs add_ws(void* ws, int64_t nrows) {
   char* p = static_cast<char*>(ws);
+  char* rp = p + add_tiles_bytes(nrows) + add_super_bytes(nrows);
   return AddWs{reinterpret_cast<int64_t*>(p), reinterpret_cast<int64_t*>(p + add_tiles_bytes(nrows)),
-               reinterpret_cast<int32_t*>(p + add_tiles_bytes(nrows) + add_super_bytes(nrows))};
+               reinterpret_cast<int32_t*>(rp),
+               reinterpret_cast<uint8_t*>(rp + add_rowptr_bytes(nrows))};
 }
 
 void sl_host::launch_coo_rowptr(int64_t nrows, int64_t nnz, const int32_t* rows,
@@ -887,7 +898,7 @@ static const int32_t* add_count_pass(int64_t nrows, const int32_t* a_pos, const 
   sl_host::launch_pdl(add_tile_kernel<0>, dim3((unsigned)add_ntiles(nrows)), dim3(kAddRows), s,
                       (size_t)0, nrows, a_pos, a_crd, (const double*)nullptr, bp, b_cols,
                       (const double*)nullptr, c_pos, (int32_t*)nullptr, (double*)nullptr, w.tiles,
-                      w.supers, true, (const int32_t*)nullptr);
+                      w.supers, true, (const int32_t*)nullptr, w.perm);
   return bp;
 }
 
@@ -921,7 +932,7 @@ extern "C" int sl_add_csr_fill(int64_t nrows, const int32_t* a_pos, const int32_
   const int32_t* bp = add_rowptr(nrows, b_nnz, b_pos, b_rows, w, false, s);
   add_tile_kernel<1><<<(int)add_ntiles(nrows), kAddRows, 0, s>>>(
       nrows, a_pos, a_crd, a_vals, bp, b_cols, b_vals, const_cast<int32_t*>(c_pos), c_crd, c_vals,
-      w.tiles, w.supers, add_staged_ok(a_crd, a_vals, b_cols, b_vals));
+      w.tiles, w.supers, add_staged_ok(a_crd, a_vals, b_cols, b_vals), nullptr, w.perm);
   return sl_host::launch_status();
 }
 
@@ -940,7 +951,7 @@ extern "C" int sl_add_csr_f64(int64_t nrows, const int32_t* a_pos, const int32_t
   sl_host::launch_pdl(add_tile_kernel<2>, dim3((unsigned)add_ntiles(nrows)), dim3(kAddRows), s,
                       (size_t)0, nrows, a_pos, a_crd, a_vals, bp, b_cols, b_vals, c_pos, c_crd, c_vals,
                       w.tiles, w.supers, add_staged_ok(a_crd, a_vals, b_cols, b_vals),
-                      (const int32_t*)nullptr);
+                      (const int32_t*)nullptr, w.perm);
   return sl_host::launch_status();
 }
 
