@@ -130,3 +130,41 @@ def test_compile_rejects_data_dependent_outputs_and_host_sparse():
     # evaluate is unaffected afterwards
     y = slb.evaluate(EXPR, {"A": _matrices(d)["csr"], "x": x}).vals
     assert y.numel() == 500
+
+
+def test_compiled_other_dense_output_patterns_match_evaluate():
+    """SpMM with X streamed, TTV / TTM / MTTKRP over CSF with the dense operands
+    streamed, CSR x hashed x (all operands resident): the replayed graph gives
+    evaluate()'s bits, or compile refuses the statement outright."""
+    st = wl.stencil27(g=12, seed=3)
+    n = st["nrows"]
+    A = F.csr_storage(st["pos"], st["crd"], st["vals"], (n, n))
+    rng = np.random.default_rng(1)
+    t = wl.mttkrp(I=60, J=50, K=40, nnz=6000, R=16, seed=5)
+    csf = wl.coo3_to_csf(t["i"], t["j"], t["k"], None)
+    X = F.csf_storage(csf["pos0"], csf["crd0"], csf["pos1"], csf["crd1"], csf["pos2"], csf["crd2"],
+                      t["vals"], (60, 50, 40))
+    d = wl.coo_spmv(n=3000, nnz=30000, seed=7)
+    pos = wl.coo_to_csr_pos(d["rows"], 3000)
+    Ah = F.csr_storage(pos, d["cols"], d["vals"], (3000, d["ncols"]))
+    h = wl.hash_vector(n=d["ncols"], m=d["ncols"] // 2, width=4096, seed=9)
+    cases = [
+        ("Y(i,k) = A(i,j) * X(j,k)", {"A": A}, {"X": (rng.uniform(-1, 1, (n, 16)), (n, 16))}),
+        ("Y(i,j) = X(i,j,k) * v(k)", {"X": X}, {"v": (rng.uniform(-1, 1, 40), (40,))}),
+        ("Y(i,j,r) = X(i,j,k) * U(k,r)", {"X": X}, {"U": (rng.uniform(-1, 1, (40, 8)), (40, 8))}),
+        ("A(i,r) = X(i,j,k) * B(j,r) * C(k,r)", {"X": X},
+         {"B": (t["B"], (50, 16)), "C": (t["C"], (40, 16))}),
+        ("y(i) = A(i,j) * x(j)",
+         {"A": Ah, "x": F.hash_vector_storage(h["crd"], h["vals"], d["ncols"], 4096)}, {}),
+    ]
+    for expr, resident, streamed in cases:
+        host = {k: F.dense_storage(v, dims, device=None) for k, (v, dims) in streamed.items()}
+        dev = {k: F.dense_storage(v, dims) for k, (v, dims) in streamed.items()}
+        want = slb.evaluate(expr, {**resident, **dev}).vals
+        try:
+            step = slb.compile(expr, {**resident, **host})
+        except UnsupportedOutputError:
+            continue                      # refused: evaluate() is the path for it
+        for _ in range(2):
+            got = step.run().vals
+            assert np.array_equal(bits(got), bits(want)), expr
