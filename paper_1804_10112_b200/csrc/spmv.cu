@@ -1018,8 +1018,11 @@ spmv_csr_vector_kernel(int64_t nrows, const int32_t* __restrict__ pos,
 // started before the tile, so every row is still summed in order by one thread.
 #endif  // SL_WITH_ALT
 
-constexpr int kMpThreads = 256;
-constexpr int kMpItems = 2048;
+// 128-thread blocks over 1024-item tiles: the tile's barriers couple fewer
+// threads to the one summing a long row (D5's fibres, TTV: 256 / 128 / 64
+// threads 230.9 / 218.6 / 255.0 us)
+constexpr int kMpThreads = 128;
+constexpr int kMpItems = 8 * kMpThreads;
 
 __device__ __forceinline__ void merge_path_search(int64_t diag, const int32_t* pos, int64_t nrows,
                                                   int64_t nnz, int64_t& row, int64_t& e) {
