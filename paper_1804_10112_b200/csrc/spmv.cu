@@ -1064,13 +1064,21 @@ spmv_csr_merge_kernel(int64_t nrows, const int32_t* __restrict__ pos,
     for (int64_t r = rb + tid; r < re; r += kMpThreads) y[r] = 0.0;
     return;
   }
+  // this thread's first row's bounds: in flight during the staging, not after
+  // the barrier (most tiles hold fewer rows than threads)
+  const int64_t r_first = rb + tid;
+  int64_t pb = 0, pe = 0;
+  if (r_first < re) {
+    pb = ldg(pos + r_first);
+    pe = ldg(pos + r_first + 1);
+  }
   for (int64_t cs = eb; cs < ee; cs += kMpItems) {
     const int n_in = (int)min64(kMpItems, ee - cs);
     stage_products<kMpThreads, kMpItems / kMpThreads>(crd, vals, cs, n_in, xop, s_prod);
     __syncthreads();
     // rows are few per tile (<= kMpItems) — thread-per-row over the chunk
-    for (int64_t r = rb + tid; r < re; r += kMpThreads) {
-      const int64_t b = ldg(pos + r), e = ldg(pos + r + 1);
+    for (int64_t r = r_first; r < re; r += kMpThreads) {
+      const int64_t b = r == r_first ? pb : ldg(pos + r), e = r == r_first ? pe : ldg(pos + r + 1);
       const int64_t lo = max64(b, cs) - cs, hi = min64(e, cs + n_in) - cs;
       double acc = cs == eb ? 0.0 : y[r];
       for (int64_t u = lo; u < hi; ++u) acc = dadd(acc, s_prod[u]);
