@@ -1136,8 +1136,9 @@ spmv_ell_kernel(int64_t nrows, int32_t nslots, const int32_t* __restrict__ crd,
 // Offsets in the constant bank (kernel parameter); all of a row's in-range
 // value and x loads are issued before the in-order add chain.
 template <int kMaxD>
-// 4 blocks/SM (measured 39.4 -> 33.5 us on D3 against 8 blocks/SM)
-__global__ void __launch_bounds__(256, 4)
+// 5 blocks/SM, 47 registers (D3: 3 / 4 / 5 / 6 blocks 26.8 / 26.7 / 25.8 / 32.3 us, the last
+// with spills; round 1: 39.4 -> 33.5 us from 8 to 4 blocks/SM under the flush protocol)
+__global__ void __launch_bounds__(256, 5)
 spmv_dia_kernel(int64_t nrows, int64_t row0, int64_t ncols, int32_t ndiag, DiaOffsets offs,
                 const double* __restrict__ vals, const double* __restrict__ x,
                 double* __restrict__ y) {
