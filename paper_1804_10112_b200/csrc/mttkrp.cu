@@ -32,7 +32,7 @@ namespace sl {
 
 constexpr int kMtWarps = 8;
 constexpr int kMtThreads = kMtWarps * 32;
-constexpr int kMtChunk = 2048;
+constexpr int kMtChunk = 1024;   // 512 / 1024 / 2048 / 4096: COO-3 0.990 / 0.966 / 0.990 / 1.103 ms, CSF 1.127 / 1.067 / 1.064 / 1.170 ms
 constexpr int kMtBatch = 8;   // products issued ahead of the accumulation chain
 
 struct CarryWs {

@@ -922,7 +922,9 @@ static int csr_ring_blocks() {
 #endif  // SL_WITH_ALT
 
 // 896-element stage (28 per row), rows of up to 28 nonzeros in registers,
-// gathers in two batches of 14, 12 one-warp blocks per SM (146 registers):
+// gathers in one batch of 28 (rotating-copies protocol: batches of 7 / 14 / 28
+// 17.37 / 17.39 / 16.43 us on the 64^3 stencil, D1 CSR 14.50 -> 14.20 us), 12
+// one-warp blocks per SM (148 registers).  Round 1, two batches of 14:
 // 64^3 stencil 22.4 us, D1 19.3 us, against K2f 23.8 / K2a 20.5 us; 14-27
 // element batches, 10-24 blocks/SM and a 32-nonzero register row measured
 // 22.4-27.2 / 19.3-24.4 us; two stages per block (tiles t+1 and t+2 in
@@ -930,7 +932,7 @@ static int csr_ring_blocks() {
 // per-launch flush protocol; logs not retained)
 constexpr int kCsrHandoffCap = 896;
 constexpr int kCsrHandoffMaxRow = 28;
-constexpr int kCsrHandoffBatch = 14;
+constexpr int kCsrHandoffBatch = 28;   // one batch: all of a row's gathers in flight before the adds
 constexpr int kCsrHandoffBlocks = 12;
 
 // (A smaller stage for short rows — 384 / 448 / 512 / 640 elements, leaving the
@@ -1299,8 +1301,10 @@ static int launch_csr(int64_t nrows, int64_t nnz, const int32_t* pos, const int3
           return sl_host::launch_status();
         }
 #endif
-        launch_csr_handoff<kCsrHandoffCap, kCsrHandoffMaxRow, kCsrHandoffBatch, kCsrHandoffBlocks>(
-            nrows, pos, crd, vals, xop, y, kCsrHandoffBlocks, s);
+        // dense x: one batch of 28 gathers; a located x (slot, then value: two
+        // dependent gathers and 64-bit slots in registers) keeps two batches of 14
+        launch_csr_handoff<kCsrHandoffCap, kCsrHandoffMaxRow, kHashX == 0 ? kCsrHandoffBatch : 14,
+                           kCsrHandoffBlocks>(nrows, pos, crd, vals, xop, y, kCsrHandoffBlocks, s);
         return sl_host::launch_status();
       }
     }
