@@ -35,12 +35,17 @@ namespace sl {
 
 
 // ---- pass 0: row pointer of a row-sorted COO level ---------------------------
-constexpr int kRowptrIpt = 8;   // elements per thread (two 16-byte loads when aligned)
-
+// kRowptrIpt elements per thread (16-byte loads when aligned): 8 behind A + B's
+// 5M coordinates (4 / 8 / 16: 82.7 / 81.7 / 85.0 us for the chain), 4 for the
+// SpMV / SpDM row pointer (D1's 2M coordinates: 17.3 / 18.2 / 18.9 us for the
+// COO SpMV) — the smaller pass wants more, shorter threads
+#ifndef SL_ROWPTR_IPT_SPMV
+#define SL_ROWPTR_IPT_SPMV 4
+#endif
+template <int kRowptrIpt>
 __global__ void __launch_bounds__(256)
 coo_rowptr_kernel(int64_t nrows, int64_t nnz, const int32_t* __restrict__ rows,
-                  int32_t* __restrict__ rowptr, int64_t* __restrict__ zero = nullptr,
-                  int64_t nzero = 0) {
+                  int32_t* __restrict__ rowptr, int64_t* __restrict__ zero, int64_t nzero) {
   pdl_trigger();                           // the count pass may begin launching
   // the count pass's super-tile totals start at zero (saves a memset node)
   for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < nzero;
@@ -53,9 +58,14 @@ coo_rowptr_kernel(int64_t nrows, int64_t nnz, const int32_t* __restrict__ rows,
   int32_t r[kRowptrIpt];
   const bool vec = e0 + kRowptrIpt <= nnz && ((reinterpret_cast<uintptr_t>(rows + e0) & 15u) == 0);
   if (vec) {
-    const int4 a = ld_stream(reinterpret_cast<const int4*>(rows + e0));
-    const int4 b = ld_stream(reinterpret_cast<const int4*>(rows + e0 + 4));
-    r[0] = a.x; r[1] = a.y; r[2] = a.z; r[3] = a.w; r[4] = b.x; r[5] = b.y; r[6] = b.z; r[7] = b.w;
+    int4 q[kRowptrIpt / 4];
+#pragma unroll
+    for (int t = 0; t < kRowptrIpt / 4; ++t)
+      q[t] = ld_stream(reinterpret_cast<const int4*>(rows + e0 + 4 * t));
+#pragma unroll
+    for (int t = 0; t < kRowptrIpt / 4; ++t) {
+      r[4 * t] = q[t].x; r[4 * t + 1] = q[t].y; r[4 * t + 2] = q[t].z; r[4 * t + 3] = q[t].w;
+    }
   } else {
 #pragma unroll
     for (int t = 0; t < kRowptrIpt; ++t) r[t] = e0 + t < nnz ? ldg(rows + e0 + t) : (int32_t)nrows;
@@ -860,8 +870,9 @@ static AddWs add_ws(void* ws, int64_t nrows) {
 
 void sl_host::launch_coo_rowptr(int64_t nrows, int64_t nnz, const int32_t* rows,
                                 int32_t* rowptr, cudaStream_t s) {
-  coo_rowptr_kernel<<<ceil_div(ceil_div(nnz + 1, kRowptrIpt), 256), 256, 0, s>>>(nrows, nnz, rows,
-                                                                               rowptr);
+  coo_rowptr_kernel<SL_ROWPTR_IPT_SPMV>
+      <<<ceil_div(ceil_div(nnz + 1, SL_ROWPTR_IPT_SPMV), 256), 256, 0, s>>>(
+          nrows, nnz, rows, rowptr, (int64_t*)nullptr, (int64_t)0);
 }
 
 static const int32_t* add_rowptr(int64_t nrows, int64_t b_nnz, const int32_t* b_pos,
@@ -891,7 +902,7 @@ static const int32_t* add_count_pass(int64_t nrows, const int32_t* a_pos, const 
   if (b_pos) {
     cudaMemsetAsync(w.supers, 0, (size_t)add_nsuper(nrows) * 8, s);
   } else {
-    coo_rowptr_kernel<<<ceil_div(ceil_div(b_nnz + 1, kRowptrIpt), 256), 256, 0, s>>>(
+    coo_rowptr_kernel<8><<<ceil_div(ceil_div(b_nnz + 1, 8), 256), 256, 0, s>>>(
         nrows, b_nnz, b_rows, w.rowptr, w.supers, add_nsuper(nrows));
     bp = w.rowptr;
   }
