@@ -30,7 +30,7 @@
 
 namespace sl {
 
-constexpr int kMtWarps = 8;
+constexpr int kMtWarps = 4;     // 2 / 4 / 8 / 16 warps per block at 16 warps/SM: COO-3 0.957 / 0.958 / 0.965 / 0.974 ms
 constexpr int kMtThreads = kMtWarps * 32;
 constexpr int kMtChunk = 1024;   // 512 / 1024 / 2048 / 4096: COO-3 0.990 / 0.966 / 0.990 / 1.103 ms, CSF 1.127 / 1.067 / 1.064 / 1.170 ms
 constexpr int kMtBatch = 8;   // products issued ahead of the accumulation chain
@@ -412,7 +412,7 @@ SL_DEV void mttkrp_vec_body(int64_t I, int64_t e0, int64_t e1, int32_t row_first
 }
 
 template <int kR>
-__global__ void __launch_bounds__(kMtThreads, 2)
+__global__ void __launch_bounds__(kMtThreads, 16 / kMtWarps)
 mttkrp_coo3_vec_kernel(int64_t I, int64_t nnz, int64_t nchunks, const int32_t* __restrict__ ii,
                        const int32_t* __restrict__ jj, const int32_t* __restrict__ kk,
                        const double* __restrict__ vals, const double* __restrict__ B,
@@ -432,7 +432,7 @@ mttkrp_coo3_vec_kernel(int64_t I, int64_t nnz, int64_t nchunks, const int32_t* _
 }
 
 template <int kR>
-__global__ void __launch_bounds__(kMtThreads, 2)
+__global__ void __launch_bounds__(kMtThreads, 16 / kMtWarps)
 mttkrp_csf_vec_kernel(int64_t I, int64_t nslices, int64_t nfibers, int64_t nnz, int64_t nchunks,
                       const int32_t* __restrict__ crd0, const int32_t* __restrict__ pos1,
                       const int32_t* __restrict__ crd1, const int32_t* __restrict__ pos2,
