@@ -1137,10 +1137,12 @@ spmv_ell_kernel(int64_t nrows, int32_t nslots, const int32_t* __restrict__ crd,
 
 // Offsets in the constant bank (kernel parameter); all of a row's in-range
 // value and x loads are issued before the in-order add chain.
+constexpr int kDiaThreads = 128;
 template <int kMaxD>
-// 5 blocks/SM, 47 registers (D3: 3 / 4 / 5 / 6 blocks 26.8 / 26.7 / 25.8 / 32.3 us, the last
+// 1280 threads per SM in 128-thread blocks (256 x 5: 25.85 us, 128 x 10: 25.13 us, 64 x 20: 25.21 us
+// on D3), 47 registers (D3: 3 / 4 / 5 / 6 blocks 26.8 / 26.7 / 25.8 / 32.3 us, the last
 // with spills; round 1: 39.4 -> 33.5 us from 8 to 4 blocks/SM under the flush protocol)
-__global__ void __launch_bounds__(256, 5)
+__global__ void __launch_bounds__(kDiaThreads, 1280 / kDiaThreads)
 spmv_dia_kernel(int64_t nrows, int64_t row0, int64_t ncols, int32_t ndiag, DiaOffsets offs,
                 const double* __restrict__ vals, const double* __restrict__ x,
                 double* __restrict__ y) {
@@ -1450,7 +1452,8 @@ extern "C" int sl_spmv_ell_f64(int64_t nrows, int64_t ncols, int32_t nslots, con
   // batch's loads before the current batch's gathers (register software
   // pipelining, 20.6-24.6 us) and a grid-stride persistent grid of 2-8
   // blocks/SM (20.6-25.3 us)
-  spmv_ell_kernel<kEllBatch, 256, 4><<<ceil_div(nrows, 256), 256, 0, s>>>(nrows, nslots, crd, vals,
+  // 128-thread blocks, 8 per SM (256 x 4: 15.44 us, 128 x 8 / 64 x 16: 15.36 us on the 64^3 stencil)
+  spmv_ell_kernel<kEllBatch, 128, 8><<<ceil_div(nrows, 128), 128, 0, s>>>(nrows, nslots, crd, vals,
                                                                           x, y);
   return sl_host::launch_status();
 }
@@ -1472,19 +1475,19 @@ extern "C" int sl_spmv_dia_rows_f64(int64_t nrows, int64_t row0, int64_t ncols, 
   } else {
     doffs = offsets;
   }
-  const int grid = ceil_div(nrows, 256);
+  const int grid = ceil_div(nrows, kDiaThreads);
 #ifdef SL_WITH_ALT
   if (!doffs && row0 == 0 && aligned16(vals) && aligned16(x) && ndiag > 0 && spmv_path() == 2)
     return sl_host::launch_dia_pipe(nrows, ncols, ndiag, p, vals, x, y, s);
 #endif
   if (doffs) {
-    spmv_dia_dev_kernel<<<grid, 256, 0, s>>>(nrows, row0, ncols, ndiag, doffs, vals, x, y);
+    spmv_dia_dev_kernel<<<ceil_div(nrows, 256), 256, 0, s>>>(nrows, row0, ncols, ndiag, doffs, vals, x, y);
   } else if (ndiag <= 8) {
-    spmv_dia_kernel<8><<<grid, 256, 0, s>>>(nrows, row0, ncols, ndiag, p, vals, x, y);
+    spmv_dia_kernel<8><<<grid, kDiaThreads, 0, s>>>(nrows, row0, ncols, ndiag, p, vals, x, y);
   } else if (ndiag <= 16) {
-    spmv_dia_kernel<16><<<grid, 256, 0, s>>>(nrows, row0, ncols, ndiag, p, vals, x, y);
+    spmv_dia_kernel<16><<<grid, kDiaThreads, 0, s>>>(nrows, row0, ncols, ndiag, p, vals, x, y);
   } else {
-    spmv_dia_kernel<32><<<grid, 256, 0, s>>>(nrows, row0, ncols, ndiag, p, vals, x, y);
+    spmv_dia_kernel<32><<<grid, kDiaThreads, 0, s>>>(nrows, row0, ncols, ndiag, p, vals, x, y);
   }
   return sl_host::launch_status();
 }
