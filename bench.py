@@ -58,7 +58,7 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 METRIC = "SpMV effective HBM GB/s (% of peak) per format; MTTKRP nnz/s"
-E2E_STREAMS = 4                         # e2e pipelining depth (tools/e2e_probe.py: 4 beats 3, 6 no better)
+E2E_STREAMS = int(os.environ.get("SL_E2E_STREAMS", "4"))   # e2e pipelining depth (tools/e2e_probe.py: 4 beats 3, 6 no better)
 WORKLOAD = "ELL vs CSR SpMV fp64, 27-point stencil 64^3 (BASELINE configs[1])"
 G = 64
 L2_MARGIN = float(os.environ.get("SL_BENCH_L2_MARGIN", "8"))   # rotated copies exceed L2 by this factor
