@@ -489,7 +489,8 @@ def run_ours(args, rank, world, local_rank):
                     "ms_per_step": round(t_e2e * 1e3, 4),
                     "path": "compile_many([y = A_csr * x, y = A_ell * x]) bound once (public API), "
                             "one CUDA-graph launch per step: pinned host x -> device, both SpMV "
-                            "kernels, both y -> pinned host, every step; matrices resident in "
+                            "kernels, both y packed and sent to pinned host in one copy, every "
+                            "step; matrices resident in "
                             f"HBM; steps rotate over {ns} streams",
                     "timing": f"wall clock, synchronised both sides; median of 5 batches of "
                               f"{e2e_steps} steps after {max(args.warmup, 2 * ns)} warm-up steps",
